@@ -1,0 +1,938 @@
+// K2/K5: fused neural-field forward and backward (field.py:208-331), plus the lean
+// SDF-only query and the occupancy refresh (renderer.py:108-142).
+//
+// Layout.  Every kernel works in a padded "36-wide" encoding space regardless of L:
+// e_aug = [x(3), level features (32, zero beyond 2L), const 1], so one compiled kernel
+// serves 1..16 levels.  The block prologue copies the MLP weights into shared memory
+// in that padded layout (H1p 64x36, H2 16x64 + its transpose, C1p 64x28, C2 64x64,
+// C3p 4x64); every per-sample mat-vec then reads weights as warp-broadcast LDS.128.
+//
+// Forward: thread per sample.  The hash gather writes the 32x3 feature Jacobian to
+// shared memory (needed once the SDF net has produced j_d, for the normal).
+// Backward: thread per sample, warps own 32-sample chunks of a persistent loop.  The
+// forward is recomputed (no per-sample activations are stored between the passes),
+// then colour bwd -> SDF first-order bwd -> fused first+second-order table scatter
+// (one float2 RED per corner) -> Theorem-1 vectors.  The weight gradients are
+// sum-over-samples outer products: each warp stages the per-sample vectors of its
+// 32 samples in shared memory and reduces them as a 32-deep rank-k update into
+// block-shared fp32 accumulators; the block flushes them with one global RED per
+// element at exit.
+#include "common.cuh"
+
+namespace ns2b {
+
+constexpr int H = 64;        // hidden width
+constexpr int EP = 36;       // padded e_aug width (3 + 32 + 1)
+constexpr int EC = 35;       // const-channel column in the padded layout
+constexpr int CIN = 25;      // colour-net input
+constexpr int CINP = 28;     // padded
+constexpr int NOUT = 16;     // sdf-net outputs (d + 15 geometry features)
+
+// shared-memory weight block (floats)
+constexpr int OFF_H1 = 0;                       // 64 x 36
+constexpr int OFF_H2 = OFF_H1 + H * EP;         // 16 x 64
+constexpr int OFF_H2T = OFF_H2 + NOUT * H;      // 64 x 16
+constexpr int OFF_C1 = OFF_H2T + H * NOUT;      // 64 x 28
+constexpr int OFF_C2 = OFF_C1 + H * CINP;       // 64 x 64
+constexpr int OFF_C3 = OFF_C2 + H * H;          // 4 x 64
+constexpr int W_FLOATS = OFF_C3 + 4 * H;        // 10496
+
+// weight-gradient accumulators (padded layouts, floats)
+constexpr int G_H1 = 0;                          // 64 x 36
+constexpr int G_H2 = G_H1 + H * EP;              // 16 x 64
+constexpr int G_C1 = G_H2 + NOUT * H;            // 64 x 28
+constexpr int G_C2 = G_C1 + H * CINP;            // 64 x 64
+constexpr int G_C3 = G_C2 + H * H;               // 4 x 64
+constexpr int G_FLOATS = G_C3 + 4 * H;           // 9472
+
+struct FieldDev {
+    int L, n_active;
+    int64_t T;
+    LevelInfo lv[NS2B_MAX_LEVELS];
+    float sx[NS2B_MAX_LEVELS], sy[NS2B_MAX_LEVELS], sz[NS2B_MAX_LEVELS];
+    float lo[3], ext[3];
+    const float *tables, *sdf_w, *color_w;
+};
+
+static int make_field_dev(const ns2b_field_t *f, FieldDev &d) {
+    NS2B_REQUIRE(f != nullptr, "null field");
+    NS2B_REQUIRE(f->num_levels >= 1 && f->num_levels <= NS2B_MAX_LEVELS,
+                 "shape error: 1..16 levels supported (got %d)", f->num_levels);
+    NS2B_REQUIRE(f->features_per_level == 2, "shape error: features_per_level must be 2");
+    if (f->hidden_width != NS2B_HIDDEN)
+        return set_error(NS2B_EUNSUPPORTED, "hidden_width %d unsupported (kernels are built for 64)",
+                         f->hidden_width);
+    NS2B_REQUIRE(f->n_active >= 0 && f->n_active <= f->num_levels, "n_active out of range");
+    NS2B_REQUIRE(f->table_size >= 1, "table size must be positive");
+    NS2B_REQUIRE(f->tables && f->sdf_w && f->color_w, "null parameter pointer");
+    d.L = f->num_levels;
+    d.n_active = f->n_active;
+    d.T = f->table_size;
+    for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
+        int n = l < d.L ? f->resolutions[l] : 1;
+        d.lv[l] = make_level(n, d.T);
+        d.sx[l] = static_cast<float>(static_cast<double>(n) * f->inv_extent[0]);
+        d.sy[l] = static_cast<float>(static_cast<double>(n) * f->inv_extent[1]);
+        d.sz[l] = static_cast<float>(static_cast<double>(n) * f->inv_extent[2]);
+    }
+    for (int k = 0; k < 3; ++k) {
+        d.lo[k] = f->aabb_min[k];
+        d.ext[k] = f->aabb_extent[k];
+    }
+    d.tables = f->tables;
+    d.sdf_w = f->sdf_w;
+    d.color_w = f->color_w;
+    return NS2B_OK;
+}
+
+// ------------------------------------------------------------ prologue ----
+__device__ void load_weights(float *sw, const FieldDev &f) {
+    const int E = 3 + 2 * f.L;  // real encoding dim; H1 is (64, E+1)
+    for (int i = threadIdx.x; i < W_FLOATS; i += blockDim.x) {
+        float v = 0.f;
+        if (i < OFF_H2) {
+            int j = i / EP, c = i % EP;
+            int src = c < E ? c : (c == EC ? E : -1);
+            if (src >= 0) v = f.sdf_w[j * (E + 1) + src];
+        } else if (i < OFF_H2T) {
+            v = f.sdf_w[H * (E + 1) + (i - OFF_H2)];
+        } else if (i < OFF_C1) {
+            int r = i - OFF_H2T, j = r / NOUT, o = r % NOUT;  // H2T[j][o] = H2[o][j]
+            v = f.sdf_w[H * (E + 1) + o * H + j];
+        } else if (i < OFF_C2) {
+            int r = i - OFF_C1, j = r / CINP, c = r % CINP;
+            if (c < CIN) v = f.color_w[j * CIN + c];
+        } else if (i < OFF_C3) {
+            v = f.color_w[H * CIN + (i - OFF_C2)];
+        } else {
+            int r = i - OFF_C3;
+            if (r < 3 * H) v = f.color_w[H * CIN + H * H + r];
+        }
+        sw[i] = v;
+    }
+}
+
+__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+__device__ __forceinline__ float sigmoid_f(float z) {
+    // two-branch logistic (field.py:40-46)
+    if (z >= 0.f) return 1.f / (1.f + expf(-z));
+    float ez = expf(z);
+    return ez / (1.f + ez);
+}
+
+// ------------------------------------------------------------- gather -----
+// Trilinear features + d feature / d x for all active levels (_kernels.py:67-119,
+// without corner records).  e[3..34] receives the features; the Jacobian rows go to
+// shared memory at Js[(a*3+k)*stride].
+__device__ __forceinline__ void gather_full(const FieldDev &f, float x0, float x1, float x2,
+                                            float (&e)[EP], float *Js, int stride) {
+    const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+    const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+    const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+#pragma unroll
+    for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
+        float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
+        if (l < f.n_active) {
+            const LevelInfo lv = f.lv[l];
+            int cx, cy, cz;
+            float fx, fy, fz;
+            cell_frac(u0, lv.n, cx, fx);
+            cell_frac(u1, lv.n, cy, fy);
+            cell_frac(u2, lv.n, cz, fz);
+            const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+            float2 v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+            const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                const float w = wx * wy * wz;
+                const float dwx = (ox ? sx : -sx) * (wy * wz);
+                const float dwy = (oy ? sy : -sy) * (wx * wz);
+                const float dwz = (oz ? sz : -sz) * (wx * wy);
+                f0 = fmaf(w, v[c].x, f0);
+                f1 = fmaf(w, v[c].y, f1);
+                j00 = fmaf(dwx, v[c].x, j00);
+                j01 = fmaf(dwy, v[c].x, j01);
+                j02 = fmaf(dwz, v[c].x, j02);
+                j10 = fmaf(dwx, v[c].y, j10);
+                j11 = fmaf(dwy, v[c].y, j11);
+                j12 = fmaf(dwz, v[c].y, j12);
+            }
+        }
+        e[3 + 2 * l] = f0;
+        e[4 + 2 * l] = f1;
+        if (Js) {
+            float *jr = Js + (2 * l) * 3 * stride;
+            jr[0 * stride] = j00;
+            jr[1 * stride] = j01;
+            jr[2 * stride] = j02;
+            jr[3 * stride] = j10;
+            jr[4 * stride] = j11;
+            jr[5 * stride] = j12;
+        }
+    }
+}
+
+__device__ __forceinline__ void gather_features(const FieldDev &f, float x0, float x1, float x2,
+                                                float (&e)[EP]) {
+    const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+    const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+    const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+#pragma unroll
+    for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
+        float f0 = 0.f, f1 = 0.f;
+        if (l < f.n_active) {
+            const LevelInfo lv = f.lv[l];
+            int cx, cy, cz;
+            float fx, fy, fz;
+            cell_frac(u0, lv.n, cx, fx);
+            cell_frac(u1, lv.n, cy, fy);
+            cell_frac(u2, lv.n, cz, fz);
+            const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+            float2 v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                const float w = (ox ? fx : 1.f - fx) * (oy ? fy : 1.f - fy) * (oz ? fz : 1.f - fz);
+                f0 = fmaf(w, v[c].x, f0);
+                f1 = fmaf(w, v[c].y, f1);
+            }
+        }
+        e[3 + 2 * l] = f0;
+        e[4 + 2 * l] = f1;
+    }
+}
+
+// -------------------------------------------------------- SDF forward -----
+// y = H2 relu(H1 e_aug); j_d = (H2[0] . m1) H1  (relu_mlp.py:94-129, field.py:218-219).
+// Returns the hidden mask as two 32-bit words.
+template <bool kJd>
+__device__ __forceinline__ void sdf_forward(const float *sw, const float (&e)[EP], float (&y)[NOUT],
+                                            float (&jd)[EP], uint32_t &mlo, uint32_t &mhi) {
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) y[o] = 0.f;
+    if (kJd) {
+#pragma unroll
+        for (int i = 0; i < EP; ++i) jd[i] = 0.f;
+    }
+    mlo = mhi = 0u;
+#pragma unroll 2
+    for (int j = 0; j < H; ++j) {
+        const float *h1 = sw + OFF_H1 + j * EP;
+        float z = 0.f;
+#pragma unroll
+        for (int i = 0; i < EP; i += 4) {
+            float4 w = lds4(h1 + i);
+            z = fmaf(w.x, e[i], z);
+            z = fmaf(w.y, e[i + 1], z);
+            z = fmaf(w.z, e[i + 2], z);
+            z = fmaf(w.w, e[i + 3], z);
+        }
+        const bool on = z > 0.f;
+        const float a = on ? z : 0.f;
+        if (on) {
+            if (j < 32) mlo |= 1u << j;
+            else mhi |= 1u << (j - 32);
+        }
+        const float *h2t = sw + OFF_H2T + j * NOUT;
+#pragma unroll
+        for (int o = 0; o < NOUT; o += 4) {
+            float4 w = lds4(h2t + o);
+            y[o] = fmaf(w.x, a, y[o]);
+            y[o + 1] = fmaf(w.y, a, y[o + 1]);
+            y[o + 2] = fmaf(w.z, a, y[o + 2]);
+            y[o + 3] = fmaf(w.w, a, y[o + 3]);
+        }
+        if (kJd) {
+            const float s = on ? sw[OFF_H2 + j] : 0.f;  // H2[0][j] * m_j
+#pragma unroll
+            for (int i = 0; i < EP; i += 4) {
+                float4 w = lds4(h1 + i);
+                jd[i] = fmaf(s, w.x, jd[i]);
+                jd[i + 1] = fmaf(s, w.y, jd[i + 1]);
+                jd[i + 2] = fmaf(s, w.z, jd[i + 2]);
+                jd[i + 3] = fmaf(s, w.w, jd[i + 3]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool mask_bit(uint32_t lo, uint32_t hi, int j) {
+    return j < 32 ? ((lo >> j) & 1u) : ((hi >> (j - 32)) & 1u);
+}
+
+// n = j_d[:E] @ J with J rows 0..2 = I (field.py:220-221).
+__device__ __forceinline__ void normal_from(const float (&jd)[EP], const float *Js, int stride,
+                                            int n_active, float &n0, float &n1, float &n2) {
+    n0 = jd[0];
+    n1 = jd[1];
+    n2 = jd[2];
+#pragma unroll
+    for (int a = 0; a < 2 * NS2B_MAX_LEVELS; ++a) {
+        if (a < 2 * n_active) {
+            const float s = jd[3 + a];
+            const float *jr = Js + a * 3 * stride;
+            n0 = fmaf(s, jr[0], n0);
+            n1 = fmaf(s, jr[stride], n1);
+            n2 = fmaf(s, jr[2 * stride], n2);
+        }
+    }
+}
+
+// colour net first layer: a1c = relu(C1 cin)
+__device__ __forceinline__ void color_layer1(const float *sw, const float (&cin)[CINP], float (&a1)[H],
+                                             uint32_t &mlo, uint32_t &mhi) {
+    mlo = mhi = 0u;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        const float *c1 = sw + OFF_C1 + j * CINP;
+        float z = 0.f;
+#pragma unroll
+        for (int i = 0; i < CINP; i += 4) {
+            float4 w = lds4(c1 + i);
+            z = fmaf(w.x, cin[i], z);
+            z = fmaf(w.y, cin[i + 1], z);
+            z = fmaf(w.z, cin[i + 2], z);
+            z = fmaf(w.w, cin[i + 3], z);
+        }
+        const bool on = z > 0.f;
+        a1[j] = on ? z : 0.f;
+        if (on) {
+            if (j < 32) mlo |= 1u << j;
+            else mhi |= 1u << (j - 32);
+        }
+    }
+}
+
+__device__ __forceinline__ float dot64(const float *w, const float (&a)[H]) {
+    float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < H; i += 8) {
+        float4 p = lds4(w + i), q = lds4(w + i + 4);
+        z0 = fmaf(p.x, a[i], z0);
+        z0 = fmaf(p.y, a[i + 1], z0);
+        z0 = fmaf(p.z, a[i + 2], z0);
+        z0 = fmaf(p.w, a[i + 3], z0);
+        z1 = fmaf(q.x, a[i + 4], z1);
+        z1 = fmaf(q.y, a[i + 5], z1);
+        z1 = fmaf(q.z, a[i + 6], z1);
+        z1 = fmaf(q.w, a[i + 7], z1);
+    }
+    return z0 + z1;
+}
+
+// ------------------------------------------------------------ forward -----
+constexpr int FWD_BLOCK = 128;
+
+__global__ void __launch_bounds__(FWD_BLOCK)
+field_forward_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
+                     const double *__restrict__ dirs, const int32_t *__restrict__ count,
+                     float *__restrict__ sdf, float *__restrict__ colors, float *__restrict__ normals,
+                     float *__restrict__ geo, double *__restrict__ eik_sum) {
+    extern __shared__ float4 smem4[];
+    float *sw = reinterpret_cast<float *>(smem4);
+    float *Js = sw + W_FLOATS;  // 96 x FWD_BLOCK
+    load_weights(sw, f);
+    __syncthreads();
+    const int P = *count;
+    float eik = 0.f;
+    for (int64_t base = (int64_t)blockIdx.x * FWD_BLOCK; base < P; base += (int64_t)gridDim.x * FWD_BLOCK) {
+        const int64_t p = base + threadIdx.x;
+        if (p >= P) break;
+        const float x0 = pos[3 * p], x1 = pos[3 * p + 1], x2 = pos[3 * p + 2];
+        float e[EP];
+        e[0] = x0;
+        e[1] = x1;
+        e[2] = x2;
+        e[EC] = 1.f;
+        float *jt = Js + threadIdx.x;
+        gather_full(f, x0, x1, x2, e, jt, FWD_BLOCK);
+        float y[NOUT], jd[EP];
+        uint32_t mlo, mhi;
+        sdf_forward<true>(sw, e, y, jd, mlo, mhi);
+        float n0, n1, n2;
+        normal_from(jd, jt, FWD_BLOCK, f.n_active, n0, n1, n2);
+        const int r = ray_ids[p];
+        float cin[CINP];
+        cin[0] = x0;
+        cin[1] = x1;
+        cin[2] = x2;
+        cin[3] = n0;
+        cin[4] = n1;
+        cin[5] = n2;
+        cin[6] = static_cast<float>(dirs[3 * r]);
+        cin[7] = static_cast<float>(dirs[3 * r + 1]);
+        cin[8] = static_cast<float>(dirs[3 * r + 2]);
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) cin[9 + o] = y[o];
+        cin[25] = cin[26] = cin[27] = 0.f;
+        float a1[H];
+        uint32_t clo, chi;
+        color_layer1(sw, cin, a1, clo, chi);
+        float l0 = 0.f, l1 = 0.f, l2 = 0.f;
+#pragma unroll 4
+        for (int k = 0; k < H; ++k) {
+            float z = dot64(sw + OFF_C2 + k * H, a1);
+            float a = z > 0.f ? z : 0.f;
+            l0 = fmaf(sw[OFF_C3 + k], a, l0);
+            l1 = fmaf(sw[OFF_C3 + H + k], a, l1);
+            l2 = fmaf(sw[OFF_C3 + 2 * H + k], a, l2);
+        }
+        sdf[p] = y[0];
+        colors[3 * p] = sigmoid_f(l0);
+        colors[3 * p + 1] = sigmoid_f(l1);
+        colors[3 * p + 2] = sigmoid_f(l2);
+        if (normals) {
+            normals[3 * p] = n0;
+            normals[3 * p + 1] = n1;
+            normals[3 * p + 2] = n2;
+        }
+        if (geo) {
+#pragma unroll
+            for (int o = 1; o < NOUT; ++o) geo[15 * p + o - 1] = y[o];
+        }
+        const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2) - 1.f;
+        eik += nn * nn;
+    }
+    if (eik_sum) {
+        double v = warp_sum(static_cast<double>(eik));
+        if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(eik_sum, v);
+    }
+}
+
+// -------------------------------------------------------- SDF only --------
+__global__ void __launch_bounds__(FWD_BLOCK)
+field_sdf_kernel(FieldDev f, const float *__restrict__ pos, int64_t npts, float *__restrict__ sdf) {
+    extern __shared__ float4 smem4[];
+    float *sw = reinterpret_cast<float *>(smem4);
+    load_weights(sw, f);
+    __syncthreads();
+    for (int64_t p = blockIdx.x * (int64_t)FWD_BLOCK + threadIdx.x; p < npts;
+         p += (int64_t)gridDim.x * FWD_BLOCK) {
+        float e[EP];
+        e[0] = pos[3 * p];
+        e[1] = pos[3 * p + 1];
+        e[2] = pos[3 * p + 2];
+        e[EC] = 1.f;
+        gather_features(f, e[0], e[1], e[2], e);
+        float y[NOUT], jd[EP];
+        uint32_t mlo, mhi;
+        sdf_forward<false>(sw, e, y, jd, mlo, mhi);
+        sdf[p] = y[0];
+    }
+}
+
+// update_occupancy (renderer.py:108-128): centres lo + (i+0.5)*ext/G per axis (fp64),
+// cast to fp32 for the field, logistic density in fp64, max-decay EMA, threshold.
+__global__ void __launch_bounds__(FWD_BLOCK)
+occupancy_kernel(FieldDev f, int G, double lo0, double lo1, double lo2, double e0, double e1,
+                 double e2, double sharp, double step, double thresh, double *__restrict__ ema,
+                 uint8_t *__restrict__ bits) {
+    extern __shared__ float4 smem4[];
+    float *sw = reinterpret_cast<float *>(smem4);
+    load_weights(sw, f);
+    __syncthreads();
+    const int64_t n = (int64_t)G * G * G;
+    for (int64_t c = blockIdx.x * (int64_t)FWD_BLOCK + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * FWD_BLOCK) {
+        const int ix = static_cast<int>(c / ((int64_t)G * G));
+        const int iy = static_cast<int>((c / G) % G);
+        const int iz = static_cast<int>(c % G);
+        const double gd = static_cast<double>(G);
+        double cx = __dadd_rn(lo0, __ddiv_rn(__dmul_rn(ix + 0.5, e0), gd));
+        double cy = __dadd_rn(lo1, __ddiv_rn(__dmul_rn(iy + 0.5, e1), gd));
+        double cz = __dadd_rn(lo2, __ddiv_rn(__dmul_rn(iz + 0.5, e2), gd));
+        float e[EP];
+        e[0] = static_cast<float>(cx);
+        e[1] = static_cast<float>(cy);
+        e[2] = static_cast<float>(cz);
+        e[EC] = 1.f;
+        gather_features(f, e[0], e[1], e[2], e);
+        float y[NOUT], jd[EP];
+        uint32_t mlo, mhi;
+        sdf_forward<false>(sw, e, y, jd, mlo, mhi);
+        double z = sharp * static_cast<double>(y[0]);
+        z = fmin(fmax(z, -80.0), 80.0);
+        double cdf;
+        if (z >= 0.0) {
+            cdf = 1.0 / (1.0 + exp(-z));
+        } else {
+            double ez = exp(z);
+            cdf = ez / (1.0 + ez);
+        }
+        double dens = __dmul_rn(__dmul_rn(sharp, cdf), 1.0 - cdf);
+        double prev = __dmul_rn(0.95, ema[c]);
+        double v = fmax(dens, prev);
+        ema[c] = v;
+        bits[c] = __dmul_rn(v, step) > thresh ? 1 : 0;
+    }
+}
+
+// ----------------------------------------------------------- backward -----
+constexpr int BWD_BLOCK = 128;
+constexpr int BWD_WARPS = BWD_BLOCK / 32;
+constexpr int SROW = 132;  // staging row stride (floats): 4 * odd -> conflict-free LDS.128 rows
+
+// acc[M x N] (row stride ldc) += sum_{s<32} A[s][a_off+m] * B[s][b_off+n]
+// over the warp's 32 staged sample rows; M, N multiples of 4.  4x4 micro-tile per
+// lane per step, accumulators folded into block shared memory with RED.shared.
+__device__ __forceinline__ void warp_rank32(float *acc, int ldc, int M, int N, const float *stage,
+                                            int a_off, int b_off, int lane) {
+    const int tn = N >> 2;
+    const int tiles = (M >> 2) * tn;
+    for (int t = lane; t < tiles; t += 32) {
+        const int m0 = (t / tn) << 2, n0 = (t % tn) << 2;
+        float c[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[i][j] = 0.f;
+#pragma unroll 8
+        for (int s = 0; s < 32; ++s) {
+            const float4 a = lds4(stage + s * SROW + a_off + m0);
+            const float4 b = lds4(stage + s * SROW + b_off + n0);
+            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) c[i][j] = fmaf(av[i], bv[j], c[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c[i][j] != 0.f) atomicAdd(acc + (m0 + i) * ldc + n0 + j, c[i][j]);
+    }
+}
+
+__global__ void __launch_bounds__(BWD_BLOCK, 1)
+field_backward_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
+                      const double *__restrict__ dirs, const int32_t *__restrict__ count,
+                      const float *__restrict__ dl_dc, const float *__restrict__ dl_dsdf,
+                      const float *__restrict__ dl_dn_extra, float eik_w,
+                      const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf,
+                      float *__restrict__ g_color, float *__restrict__ g_tab) {
+    extern __shared__ float4 smem4[];
+    float *sw = reinterpret_cast<float *>(smem4);
+    float *gacc = sw + W_FLOATS;                 // G_FLOATS
+    float *Js = gacc + G_FLOATS;                 // 96 x BWD_BLOCK
+    float *Es = Js + 96 * BWD_BLOCK;             // EP x BWD_BLOCK (e_aug, column-major per thread)
+    float *stage_all = Es + EP * BWD_BLOCK;      // BWD_WARPS x 32 x SROW
+    load_weights(sw, f);
+    for (int i = threadIdx.x; i < G_FLOATS; i += BWD_BLOCK) gacc[i] = 0.f;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *stage = stage_all + warp * 32 * SROW;
+    float *my = stage + lane * SROW;  // this lane's staging row
+    float *jt = Js + threadIdx.x;
+    float *et = Es + threadIdx.x;
+    const int P = *count;
+    const float inv_p = eik_count ? 1.f / static_cast<float>(*eik_count) : 0.f;
+    const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
+    (void)inv_p;
+    const int64_t stride = (int64_t)gridDim.x * BWD_BLOCK;
+
+    for (int64_t base = (int64_t)blockIdx.x * BWD_BLOCK + warp * 32; base < P; base += stride) {
+        const int64_t p = base + lane;
+        const bool valid = p < P;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
+        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
+        if (valid) {
+            x0 = pos[3 * p];
+            x1 = pos[3 * p + 1];
+            x2 = pos[3 * p + 2];
+            const int r = ray_ids[p];
+            v0 = static_cast<float>(dirs[3 * r]);
+            v1 = static_cast<float>(dirs[3 * r + 1]);
+            v2 = static_cast<float>(dirs[3 * r + 2]);
+            gc0 = dl_dc[3 * p];
+            gc1 = dl_dc[3 * p + 1];
+            gc2 = dl_dc[3 * p + 2];
+            gd = dl_dsdf[p];
+            if (dl_dn_extra) {
+                gn0 = dl_dn_extra[3 * p];
+                gn1 = dl_dn_extra[3 * p + 1];
+                gn2 = dl_dn_extra[3 * p + 2];
+            }
+        }
+        // ---- recompute forward ----
+        float e[EP];
+        e[0] = x0;
+        e[1] = x1;
+        e[2] = x2;
+        e[EC] = 1.f;
+        gather_full(f, x0, x1, x2, e, jt, BWD_BLOCK);
+#pragma unroll
+        for (int i = 0; i < EP; ++i) et[i * BWD_BLOCK] = e[i];
+        float y[NOUT], jd[EP];
+        uint32_t mlo, mhi;
+        sdf_forward<true>(sw, e, y, jd, mlo, mhi);
+        float n0, n1, n2;
+        normal_from(jd, jt, BWD_BLOCK, f.n_active, n0, n1, n2);
+        // Eikonal cotangent (trainer.py:229-235), fp32 as numpy evaluates it.
+        if (valid && eik_w != 0.f) {
+            const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+            const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
+            gn0 += coef * n0 / Pf;
+            gn1 += coef * n1 / Pf;
+            gn2 += coef * n2 / Pf;
+        }
+        float cin[CINP];
+        cin[0] = x0;
+        cin[1] = x1;
+        cin[2] = x2;
+        cin[3] = n0;
+        cin[4] = n1;
+        cin[5] = n2;
+        cin[6] = v0;
+        cin[7] = v1;
+        cin[8] = v2;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) cin[9 + o] = y[o];
+        cin[25] = cin[26] = cin[27] = 0.f;
+        float dlg0, dlg1, dlg2;
+        uint32_t clo, chi, c2lo = 0u, c2hi = 0u;
+        {
+            float a1[H];
+            color_layer1(sw, cin, a1, clo, chi);
+            float l0 = 0.f, l1 = 0.f, l2 = 0.f;
+            __syncwarp();
+#pragma unroll 4
+            for (int k = 0; k < H; ++k) {
+                const float z = dot64(sw + OFF_C2 + k * H, a1);
+                const bool on = z > 0.f;
+                const float a = on ? z : 0.f;
+                if (on) {
+                    if (k < 32) c2lo |= 1u << k;
+                    else c2hi |= 1u << (k - 32);
+                }
+                l0 = fmaf(sw[OFF_C3 + k], a, l0);
+                l1 = fmaf(sw[OFF_C3 + H + k], a, l1);
+                l2 = fmaf(sw[OFF_C3 + 2 * H + k], a, l2);
+                my[64 + k] = a;  // AC2 -> slot B
+            }
+            // dlogits = dl_dc * c * (1 - c) (field.py:304)
+            const float c0 = sigmoid_f(l0), c1 = sigmoid_f(l1), c2 = sigmoid_f(l2);
+            dlg0 = gc0 * c0 * (1.f - c0);
+            dlg1 = gc1 * c1 * (1.f - c1);
+            dlg2 = gc2 * c2 * (1.f - c2);
+            my[0] = dlg0;
+            my[1] = dlg1;
+            my[2] = dlg2;
+            my[3] = 0.f;
+            __syncwarp();
+            warp_rank32(gacc + G_C3, H, 4, H, stage, 0, 64, lane);  // dC3 += dlogits^T AC2
+            __syncwarp();
+            // u2 = (C3^T dlogits) . m2  -> slot B ; AC1 -> slot A
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const float u = sw[OFF_C3 + k] * dlg0 + sw[OFF_C3 + H + k] * dlg1 + sw[OFF_C3 + 2 * H + k] * dlg2;
+                my[64 + k] = mask_bit(c2lo, c2hi, k) ? u : 0.f;
+                my[k] = a1[k];
+            }
+        }
+        __syncwarp();
+        warp_rank32(gacc + G_C2, H, H, H, stage, 64, 0, lane);  // dC2 += U2^T AC1
+        __syncwarp();
+        // u1 = (C2^T u2) . m1c
+        float u1[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) u1[j] = 0.f;
+#pragma unroll 2
+        for (int k4 = 0; k4 < H; k4 += 4) {
+            const float4 u2 = lds4(my + 64 + k4);
+            const float uv[4] = {u2.x, u2.y, u2.z, u2.w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const float *c2 = sw + OFF_C2 + (k4 + kk) * H;
+#pragma unroll
+                for (int j = 0; j < H; j += 4) {
+                    const float4 w = lds4(c2 + j);
+                    u1[j] = fmaf(w.x, uv[kk], u1[j]);
+                    u1[j + 1] = fmaf(w.y, uv[kk], u1[j + 1]);
+                    u1[j + 2] = fmaf(w.z, uv[kk], u1[j + 2]);
+                    u1[j + 3] = fmaf(w.w, uv[kk], u1[j + 3]);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            u1[j] = mask_bit(clo, chi, j) ? u1[j] : 0.f;
+            my[64 + j] = u1[j];
+        }
+#pragma unroll
+        for (int i = 0; i < CINP; ++i) my[i] = cin[i];
+        __syncwarp();
+        warp_rank32(gacc + G_C1, CINP, H, CINP, stage, 64, 0, lane);  // dC1 += U1^T CIN
+        // dcin = C1^T u1
+        float dcin[CINP];
+#pragma unroll
+        for (int i = 0; i < CINP; ++i) dcin[i] = 0.f;
+#pragma unroll 4
+        for (int j = 0; j < H; ++j) {
+            const float *c1 = sw + OFF_C1 + j * CINP;
+#pragma unroll
+            for (int i = 0; i < CINP; i += 4) {
+                const float4 w = lds4(c1 + i);
+                dcin[i] = fmaf(w.x, u1[j], dcin[i]);
+                dcin[i + 1] = fmaf(w.y, u1[j], dcin[i + 1]);
+                dcin[i + 2] = fmaf(w.z, u1[j], dcin[i + 2]);
+                dcin[i + 3] = fmaf(w.w, u1[j], dcin[i + 3]);
+            }
+        }
+        // total normal / sdf / geometry cotangents (field.py:308-314)
+        const float q0 = gn0 + dcin[3], q1 = gn1 + dcin[4], q2 = gn2 + dcin[5];
+        float dly[NOUT];
+        dly[0] = gd + dcin[9];
+#pragma unroll
+        for (int o = 1; o < NOUT; ++o) dly[o] = dcin[9 + o];
+        // SDF first-order: u = (H2^T dl_dy) . m1 ; de = H1^T u
+        float de[EP];
+#pragma unroll
+        for (int i = 0; i < EP; ++i) de[i] = 0.f;
+        __syncwarp();
+#pragma unroll 2
+        for (int j = 0; j < H; ++j) {
+            const float *h2t = sw + OFF_H2T + j * NOUT;
+            float u = 0.f;
+#pragma unroll
+            for (int o = 0; o < NOUT; o += 4) {
+                const float4 w = lds4(h2t + o);
+                u = fmaf(w.x, dly[o], u);
+                u = fmaf(w.y, dly[o + 1], u);
+                u = fmaf(w.z, dly[o + 2], u);
+                u = fmaf(w.w, dly[o + 3], u);
+            }
+            u = mask_bit(mlo, mhi, j) ? u : 0.f;
+            my[j] = u;  // U -> slot A
+            const float *h1 = sw + OFF_H1 + j * EP;
+#pragma unroll
+            for (int i = 0; i < EP; i += 4) {
+                const float4 w = lds4(h1 + i);
+                de[i] = fmaf(w.x, u, de[i]);
+                de[i + 1] = fmaf(w.y, u, de[i + 1]);
+                de[i + 2] = fmaf(w.z, u, de[i + 2]);
+                de[i + 3] = fmaf(w.w, u, de[i + 3]);
+            }
+        }
+        // mvec = [q, J q, 0] (field.py:326-327)
+        float mv[EP];
+        mv[0] = q0;
+        mv[1] = q1;
+        mv[2] = q2;
+#pragma unroll
+        for (int a = 0; a < 2 * NS2B_MAX_LEVELS; ++a) {
+            const float *jr = jt + a * 3 * BWD_BLOCK;
+            mv[3 + a] = (a < 2 * f.n_active) ? (jr[0] * q0 + jr[BWD_BLOCK] * q1 + jr[2 * BWD_BLOCK] * q2) : 0.f;
+        }
+        mv[EC] = 0.f;
+        // ---- fused first + second order table scatter (Eq. 9) ----
+        if (valid) {
+            const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+            const float uu1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+            const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+#pragma unroll
+            for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
+                if (l < f.n_active) {
+                    const LevelInfo lv = f.lv[l];
+                    int cx, cy, cz;
+                    float fx, fy, fz;
+                    cell_frac(u0, lv.n, cx, fx);
+                    cell_frac(uu1, lv.n, cy, fy);
+                    cell_frac(u2, lv.n, cz, fz);
+                    const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
+                    const float de0 = de[3 + 2 * l], de1 = de[4 + 2 * l];
+                    const float jd0 = jd[3 + 2 * l], jd1 = jd[4 + 2 * l];
+                    float *gt = g_tab + l * f.T * 2;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                        const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                        const float w = wx * wy * wz;
+                        const float dwx = (ox ? sx : -sx) * (wy * wz);
+                        const float dwy = (oy ? sy : -sy) * (wx * wz);
+                        const float dwz = (oz ? sz : -sz) * (wx * wy);
+                        const float qd = dwx * q0 + dwy * q1 + dwz * q2;
+                        const uint32_t row = corner_row(lv, cx + ox, cy + oy, cz + oz);
+                        red_add_f32x2(gt + 2 * row, fmaf(w, de0, jd0 * qd), fmaf(w, de1, jd1 * qd));
+                    }
+                }
+            }
+        }
+        // ---- SDF weight gradients ----
+        // slot B <- e_aug ; dH1 += U^T E
+#pragma unroll
+        for (int i = 0; i < EP; ++i) my[64 + i] = et[i * BWD_BLOCK];
+        __syncwarp();
+        warp_rank32(gacc + G_H1, EP, H, EP, stage, 0, 64, lane);
+        __syncwarp();
+        // slot A <- s1 = H2[0] . m1 ; slot B <- mvec ; dH1 += S1^T MV  (Theorem 1, l = 1)
+        // pvec = (H1 mvec) . m1 -> slot C (cols 100..)?  computed below into registers
+#pragma unroll
+        for (int j = 0; j < H; ++j) my[j] = mask_bit(mlo, mhi, j) ? sw[OFF_H2 + j] : 0.f;
+#pragma unroll
+        for (int i = 0; i < EP; ++i) my[64 + i] = mv[i];
+        __syncwarp();
+        warp_rank32(gacc + G_H1, EP, H, EP, stage, 0, 64, lane);
+        __syncwarp();
+        // slot A <- dl_dy (16) ; slot B <- a1 (recomputed from e) ; dH2 += DLY^T A1
+        //   plus Theorem-1 row 0: dH2[0] += pvec, folded in as an extra rank-1 term by
+        //   staging pvec with dl_dy-row [1,0,..] in the second half of the chunk below.
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) my[o] = dly[o];
+#pragma unroll 2
+        for (int j = 0; j < H; ++j) {
+            const float *h1 = sw + OFF_H1 + j * EP;
+            float z = 0.f, zp = 0.f;
+#pragma unroll
+            for (int i = 0; i < EP; i += 4) {
+                const float4 w = lds4(h1 + i);
+                z = fmaf(w.x, e[i], z);
+                z = fmaf(w.y, e[i + 1], z);
+                z = fmaf(w.z, e[i + 2], z);
+                z = fmaf(w.w, e[i + 3], z);
+                zp = fmaf(w.x, mv[i], zp);
+                zp = fmaf(w.y, mv[i + 1], zp);
+                zp = fmaf(w.z, mv[i + 2], zp);
+                zp = fmaf(w.w, mv[i + 3], zp);
+            }
+            const bool on = mask_bit(mlo, mhi, j);
+            my[64 + j] = on ? z : 0.f;  // a1
+            my[16 + j] = on ? zp : 0.f;  // pvec (slot A cols 16..79)
+        }
+        __syncwarp();
+        warp_rank32(gacc + G_H2, H, NOUT, H, stage, 0, 64, lane);
+        // dH2[0][j] += sum_s pvec[s][j]
+        for (int j = lane; j < H; j += 32) {
+            float s = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) s += stage[r * SROW + 16 + j];
+            if (s != 0.f) atomicAdd(gacc + G_H2 + j, s);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // flush block accumulators to the real (unpadded) gradient layouts
+    const int E = 3 + 2 * f.L;
+    for (int i = threadIdx.x; i < G_FLOATS; i += BWD_BLOCK) {
+        const float v = gacc[i];
+        if (v == 0.f) continue;
+        if (i < G_H2) {
+            const int j = i / EP, c = i % EP;
+            const int dst = c < E ? c : (c == EC ? E : -1);
+            if (dst >= 0) atomicAdd(g_sdf + j * (E + 1) + dst, v);
+        } else if (i < G_C1) {
+            atomicAdd(g_sdf + H * (E + 1) + (i - G_H2), v);
+        } else if (i < G_C2) {
+            const int r = i - G_C1, j = r / CINP, c = r % CINP;
+            if (c < CIN) atomicAdd(g_color + j * CIN + c, v);
+        } else if (i < G_C3) {
+            atomicAdd(g_color + H * CIN + (i - G_C2), v);
+        } else {
+            const int r = i - G_C3;
+            if (r < 3 * H) atomicAdd(g_color + H * CIN + H * H + r, v);
+        }
+    }
+}
+
+constexpr size_t FWD_SMEM = (W_FLOATS + 96 * FWD_BLOCK) * sizeof(float);
+constexpr size_t SDF_SMEM = W_FLOATS * sizeof(float);
+constexpr size_t BWD_SMEM =
+    (W_FLOATS + G_FLOATS + 96 * BWD_BLOCK + EP * BWD_BLOCK + BWD_WARPS * 32 * SROW) * sizeof(float);
+
+static int g_attr_done = 0;
+static int ensure_attrs() {
+    if (g_attr_done) return NS2B_OK;
+    cudaError_t e = cudaFuncSetAttribute(field_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(FWD_SMEM));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(field_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(BWD_SMEM));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(field_sdf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SDF_SMEM));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(occupancy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SDF_SMEM));
+    if (e != cudaSuccess) return set_error(NS2B_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+    g_attr_done = 1;
+    return NS2B_OK;
+}
+
+}  // namespace ns2b
+
+using namespace ns2b;
+
+extern "C" {
+
+int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                       const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
+                       float *colors, float *normals, float *geo, double *eik_sum,
+                       void *stream) {
+    FieldDev f;
+    int rc = make_field_dev(field, f);
+    if (rc) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    if (capacity <= 0) return NS2B_OK;
+    int blocks = grid_for(capacity, FWD_BLOCK, kNumSMs * 2);
+    field_forward_kernel<<<blocks, FWD_BLOCK, FWD_SMEM, as_stream(stream)>>>(
+        f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum);
+    return check_launch("field_forward");
+}
+
+int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,
+                   void *stream) {
+    FieldDev f;
+    int rc = make_field_dev(field, f);
+    if (rc) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    if (npts <= 0) return NS2B_OK;
+    field_sdf_kernel<<<grid_for(npts, FWD_BLOCK, kNumSMs * 8), FWD_BLOCK, SDF_SMEM, as_stream(stream)>>>(
+        f, pos32, npts, sdf);
+    return check_launch("field_sdf");
+}
+
+int ns2b_occupancy_update(const ns2b_field_t *field, const ns2b_occ_t *occ, double sharpness,
+                          double threshold, double *ema, uint8_t *bits, void *stream) {
+    FieldDev f;
+    int rc = make_field_dev(field, f);
+    if (rc) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    NS2B_REQUIRE(occ && occ->resolution > 0, "invalid occupancy grid");
+    const int G = occ->resolution;
+    int64_t n = (int64_t)G * G * G;
+    occupancy_kernel<<<grid_for(n, FWD_BLOCK, kNumSMs * 8), FWD_BLOCK, SDF_SMEM, as_stream(stream)>>>(
+        f, G, occ->lo[0], occ->lo[1], occ->lo[2], occ->hi[0] - occ->lo[0], occ->hi[1] - occ->lo[1],
+        occ->hi[2] - occ->lo[2], sharpness, occ->step_size, threshold, ema, bits);
+    return check_launch("occupancy_update");
+}
+
+int ns2b_field_backward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                        const double *dirs, const int32_t *count, int64_t capacity,
+                        const float *dl_dc, const float *dl_dsdf, const float *dl_dn_extra,
+                        double eik_weight, const int64_t *eik_count, float *grad_sdf,
+                        float *grad_color, float *grad_tables, void *stream) {
+    FieldDev f;
+    int rc = make_field_dev(field, f);
+    if (rc) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
+    if (capacity <= 0) return NS2B_OK;
+    int blocks = grid_for(capacity, BWD_BLOCK, kNumSMs);
+    field_backward_kernel<<<blocks, BWD_BLOCK, BWD_SMEM, as_stream(stream)>>>(
+        f, pos32, ray_ids, dirs, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight),
+        eik_count, grad_sdf, grad_color, grad_tables);
+    return check_launch("field_backward");
+}
+
+}  // extern "C"

@@ -1,0 +1,231 @@
+"""Datasets, rays and ray-batch sampling (API of `hashsdf/scene_io.py`).
+
+Host side (numpy), because the reference's training loop consumes its single seeded
+generator here and only here (`trainer.py:287-289`); the fused step uploads the
+sampled batch (pinned, asynchronous).  `make_synthetic` builds the analytic sphere
+scenes in memory with the same uint8 quantisation the reference's PNG round trip
+applies; `make_dtu_shaped` builds the rectangular 49-view 1600x1200 variant the
+benchmark uses.  `DeviceRaySource` keeps a dataset's rays for a set of
+pre-drawn pixel picks resident in HBM for the kernel-only benchmark leg.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+LIGHT = np.array([0.35, 0.45, 0.82]) / np.linalg.norm([0.35, 0.45, 0.82])
+AMBIENT = 0.3
+
+
+@dataclass
+class CameraFrame:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    pose: np.ndarray
+    image: np.ndarray
+    mask: np.ndarray
+    time_index: int = 0
+
+
+@dataclass
+class MultiViewDataset:
+    frames: list
+    scene_aabb: tuple = ((-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    num_time_steps: int = 1
+
+    def frames_at(self, time_index):
+        return [f for f in self.frames if f.time_index == time_index]
+
+    def __post_init__(self):
+        self._pools = {}
+
+    def pools(self, time_index):
+        """(frames, fg pool, bg pool) cached per time index (scene_io.py:137-146)."""
+        if time_index not in self._pools:
+            frames = self.frames_at(time_index)
+            fg, bg = [], []
+            for k, f in enumerate(frames):
+                ys, xs = np.nonzero(f.mask > 0.5)
+                fg.append(np.stack([np.full_like(xs, k), xs, ys], axis=1))
+                ys, xs = np.nonzero(f.mask <= 0.5)
+                bg.append(np.stack([np.full_like(xs, k), xs, ys], axis=1))
+            self._pools[time_index] = (frames, np.concatenate(fg) if fg else np.zeros((0, 3), np.int64),
+                                       np.concatenate(bg) if bg else np.zeros((0, 3), np.int64))
+        return self._pools[time_index]
+
+
+@dataclass
+class RayBatch:
+    origins: object
+    directions: object
+    target_colors: object
+    foreground_flags: object
+
+    @property
+    def count(self):
+        return self.origins.shape[0]
+
+
+def generate_rays_grid(frame, pixels=None):
+    """Pinhole rays through pixel centres (`scene_io.py:98-116`)."""
+    if pixels is None:
+        ys, xs = np.mgrid[0:frame.height, 0:frame.width]
+        pixels = np.stack([xs.ravel(), ys.ravel()], axis=1)
+    px = pixels[:, 0].astype(np.float64)
+    py = pixels[:, 1].astype(np.float64)
+    d_cam = np.stack([(px + 0.5 - frame.cx) / frame.fx, (py + 0.5 - frame.cy) / frame.fy,
+                      np.ones_like(px)], axis=1)
+    d = d_cam @ frame.pose[:3, :3].T
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.broadcast_to(frame.pose[:3, 3], d.shape).copy(), d
+
+
+def sample_ray_batch(dataset, time_index, count, fg_fraction, rng):
+    """floor(fg*count) foreground + background pixels uniformly over the frames,
+    targets image*mask (`scene_io.py:129-172`); identical rng consumption."""
+    if count < 1:
+        raise ValueError("count must be >= 1")
+    frames, fg, bg = dataset.pools(time_index)
+    if not frames:
+        raise ValueError("empty foreground: no frames at this time index")
+    if fg.shape[0] == 0:
+        raise ValueError("empty foreground")
+    n_fg = int(np.floor(fg_fraction * count))
+    n_bg = count - n_fg
+    pick_fg = fg[rng.integers(0, fg.shape[0], size=n_fg)]
+    if n_bg > 0 and bg.shape[0] == 0:
+        pick_bg = fg[rng.integers(0, fg.shape[0], size=n_bg)]
+        flags = np.ones(count, bool)
+    else:
+        pick_bg = bg[rng.integers(0, bg.shape[0], size=n_bg)]
+        flags = np.concatenate([np.ones(n_fg, bool), np.zeros(n_bg, bool)])
+    picks = np.concatenate([pick_fg, pick_bg])
+    o, d, tgt = np.empty((count, 3)), np.empty((count, 3)), np.empty((count, 3))
+    for k, f in enumerate(frames):
+        sel = picks[:, 0] == k
+        if not np.any(sel):
+            continue
+        o[sel], d[sel] = generate_rays_grid(f, picks[sel, 1:3])
+        xs, ys = picks[sel, 1], picks[sel, 2]
+        tgt[sel] = f.image[ys, xs] * f.mask[ys, xs, None]
+    return RayBatch(o, d, tgt, flags)
+
+
+def preset_scene(name, num_frames=1):
+    """Static presets of `scene_io.py:229-263`."""
+    if name == "sphere":
+        spheres = [(np.zeros(3), 0.5, np.array([0.85, 0.35, 0.25]))]
+    elif name == "two-spheres":
+        spheres = [(np.array([0.32, 0.0, 0.0]), 0.30, np.array([0.85, 0.35, 0.25])),
+                   (np.array([-0.30, 0.05, 0.10]), 0.25, np.array([0.25, 0.45, 0.85]))]
+    else:
+        raise ValueError("unknown preset")
+    return spheres, [(np.eye(3), np.zeros(3))] * num_frames
+
+
+def trace_spheres(origins, dirs, spheres, rot, trans):
+    """Exact first hit + Lambertian shading (`scene_io.py:269-300`)."""
+    n = origins.shape[0]
+    best = np.full(n, np.inf)
+    which = np.full(n, -1)
+    for si, (c, r, _) in enumerate(spheres):
+        oc = origins - (rot @ c + trans)
+        b = np.einsum("ij,ij->i", oc, dirs)
+        disc = b * b - (np.einsum("ij,ij->i", oc, oc) - r * r)
+        t = np.where(disc >= 0, -b - np.sqrt(np.maximum(disc, 0.0)), np.inf)
+        t = np.where(t > 1e-6, t, np.inf)
+        closer = t < best
+        best = np.where(closer, t, best)
+        which = np.where(closer, si, which)
+    hit = np.isfinite(best)
+    col = np.zeros((n, 3))
+    for si, (c, r, albedo) in enumerate(spheres):
+        sel = hit & (which == si)
+        if not np.any(sel):
+            continue
+        p = origins[sel] + best[sel, None] * dirs[sel]
+        nrm = ((p - (rot @ c + trans)) / r) @ rot
+        lam = np.maximum(nrm @ LIGHT, 0.0)
+        col[sel] = albedo[None, :] * (AMBIENT + (1 - AMBIENT) * lam)[:, None]
+    return best, hit, np.clip(col, 0.0, 1.0)
+
+
+def orbit_pose(azimuth, elevation, distance):
+    """`scene_io.py:303-316`."""
+    eye = distance * np.array([np.cos(azimuth) * np.cos(elevation),
+                               np.sin(azimuth) * np.cos(elevation), np.sin(elevation)])
+    fwd = -eye / np.linalg.norm(eye)
+    right = np.cross(fwd, np.array([0.0, 0.0, 1.0]))
+    if np.linalg.norm(right) < 1e-6:
+        right = np.array([1.0, 0.0, 0.0])
+    right /= np.linalg.norm(right)
+    pose = np.eye(4)
+    pose[:3, 0], pose[:3, 1], pose[:3, 2], pose[:3, 3] = right, np.cross(fwd, right), fwd, eye
+    return pose
+
+
+def make_synthetic(preset, views=16, seed=0, image_size=128, width=None, height=None,
+                   focal=None, distance=2.6, chunk=1 << 20):
+    """In-memory `make_synthetic` (`scene_io.py:319-378`); with width/height/focal it
+    builds a rectangular variant.  Images are uint8-quantised like the PNG round trip."""
+    spheres, motion = preset_scene(preset)
+    w = int(width or image_size)
+    h = int(height or image_size)
+    f = float(focal) if focal is not None else image_size * 1.4
+    rng = np.random.default_rng(seed)
+    elev = np.deg2rad(np.where(np.arange(views) % 2 == 0, 18.0, -12.0))
+    azim = 2 * np.pi * np.arange(views) / views + rng.uniform(0, 2 * np.pi / views)
+    rot, trans = motion[0]
+    frames = []
+    for v in range(views):
+        pose = orbit_pose(azim[v], elev[v], distance)
+        fr = CameraFrame(f, f, w / 2.0, h / 2.0, w, h, pose, None, None, 0)
+        img = np.empty((h * w, 3), np.uint8)
+        msk = np.empty(h * w, np.float64)
+        ys, xs = np.mgrid[0:h, 0:w]
+        pix = np.stack([xs.ravel(), ys.ravel()], axis=1)
+        for s in range(0, h * w, chunk):
+            o, d = generate_rays_grid(fr, pix[s:s + chunk])
+            _, hit, col = trace_spheres(o, d, spheres, rot, trans)
+            img[s:s + chunk] = (col * 255).round().astype(np.uint8)
+            msk[s:s + chunk] = hit
+        fr.image = img.reshape(h, w, 3).astype(np.float64) / 255.0
+        fr.mask = msk.reshape(h, w)
+        frames.append(fr)
+    return MultiViewDataset(frames)
+
+
+def make_dtu_shaped(views=49, width=1600, height=1200, seed=0, preset="two-spheres"):
+    """Config-2 scene: 49 orbit cameras, 1600x1200, fx=fy=1.4*1200."""
+    return make_synthetic(preset, views=views, seed=seed, width=width, height=height,
+                          focal=1.4 * height)
+
+
+class DeviceRaySource:
+    """Pre-drawn ray batches resident in HBM (benchmark inputs): `n_batches` batches of
+    `count` rays sampled with the reference sampler semantics from one seeded rng."""
+
+    def __init__(self, dataset, count, n_batches, fg_fraction=0.9, seed=0, device=None,
+                 pin_host=True):
+        rng = np.random.default_rng(seed)
+        self.host = []
+        self.dev = []
+        for _ in range(n_batches):
+            b = sample_ray_batch(dataset, 0, count, fg_fraction, rng)
+            hb = tuple(torch.from_numpy(np.ascontiguousarray(a, np.float64)) for a in
+                       (b.origins, b.directions, b.target_colors))
+            if pin_host:
+                hb = tuple(t.pin_memory() for t in hb)
+            self.host.append(hb)
+            if device is not None:
+                self.dev.append(tuple(t.to(device) for t in hb))
+
+    def __len__(self):
+        return len(self.host)

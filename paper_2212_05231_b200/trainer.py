@@ -1,0 +1,345 @@
+"""Static-scene training step on B200 (API of `hashsdf/trainer.py`).
+
+`train_step` runs the whole NeuS2 step on the device through libns2b:
+
+  level schedule -> [occupancy refresh every 16 steps]            (host int / K-occ)
+  host ray batch (same rng draws as the reference) -> pinned H2D
+  march count -> scan -> fill                                    (K1)
+  [DP: all-reduce P]
+  field forward: encoding, SDF net, analytic normal, colour net   (K2)
+  composite + Huber loss + compositing backward (per ray)         (K3/K4)
+  field backward: recompute, colour bwd, SDF bwd, Eq. 9 scatter,
+      Theorem-1 weight grads, Eikonal cotangent fused             (K5)
+  [DP: all-reduce gradient prefix + step scalars]
+  divergence check -> s_log Adam -> multi-group Adam             (K6)
+  one D2H of the step scalars for the LossReport
+
+Parameter groups, learning rates, per-group step counters, masked-level skipping
+and the divergence error follow `trainer.py:152-172, 243-278`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import field as fieldmod
+from . import hash_encoding as enc
+from . import renderer, scene_io
+from .parallel import DataParallel
+
+
+@dataclass
+class TrainConfig:
+    """`trainer.py:28-71` (same fields and defaults)."""
+
+    total_steps: int = 15000
+    batch_size: int = 4096
+    seed: int = 0
+    eikonal_weight: float = 0.1
+    huber_delta: float = 0.1
+    fg_fraction: float = 0.9
+    lr_tables: float = 1e-2
+    lr_mlp: float = 1e-3
+    lr_final_fraction: float = 0.1
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.99
+    adam_eps: float = 1e-15
+    level_init: int = 2
+    level_increment_fraction: float = 0.025
+    occupancy_resolution: int = 128
+    occupancy_update_every: int = 16
+    occupancy_threshold: float = 0.01
+    num_levels: int = 14
+    min_resolution: int = 16
+    max_resolution: int = 2048
+    features_per_level: int = 2
+    table_size: int = 2**19
+    hidden_width: int = 64
+    init_radius: float = 0.5
+    init_sharpness: float = 20.0
+    dtype: str = "float32"
+    first_frame_steps: int = 2000
+    frame_steps: int = 1100
+    transform_only_steps: int = 100
+    transform_lr: float = 1e-3
+    transform_joint_lr: float = 1e-4
+    frame_lr_scale: float = 0.3
+
+    def replace(self, **kw):
+        return dataclasses.replace(self, **kw)
+
+
+@dataclass
+class LossReport:
+    step: int
+    color: float
+    eikonal: float
+    total: float
+    level: int
+    psnr: float
+    sample_count: int = 0
+
+
+@dataclass
+class AdamState:
+    """Per-group moments (device views into the flat moment buffers) and step t."""
+
+    m: torch.Tensor
+    v: torch.Tensor
+    t: int = 0
+
+
+def level_schedule(step, config):
+    """`trainer.py:123-126`."""
+    window = config.level_increment_fraction * config.total_steps
+    return int(min(config.num_levels, config.level_init + np.floor(step / window)))
+
+
+def lr_factor(step, total_steps, final_fraction):
+    """`trainer.py:129-131`."""
+    t = np.clip(step / max(total_steps, 1), 0.0, 1.0)
+    return final_fraction + (1.0 - final_fraction) * 0.5 * (1.0 + np.cos(np.pi * t))
+
+
+def huber(residual, delta):
+    r = np.asarray(residual)
+    a = np.abs(r)
+    return np.where(a <= delta, 0.5 * r * r / delta, a - 0.5 * delta)
+
+
+def huber_grad(residual, delta):
+    r = np.asarray(residual)
+    return np.where(np.abs(r) <= delta, r / delta, np.sign(r))
+
+
+def psnr_from_mse(mse):
+    return 100.0 if mse < 1e-10 else float(10.0 * np.log10(1.0 / mse))
+
+
+def psnr(image_a, image_b):
+    """`trainer.py:134-143` (host helper)."""
+    a, b = np.asarray(image_a), np.asarray(image_b)
+    if a.shape != b.shape:
+        raise ValueError("psnr: shape mismatch")
+    return psnr_from_mse(float(np.mean((a - b) ** 2)))
+
+
+# group order of the divergence check in the reference (trainer.py:249-278)
+_CHECK_ORDER = ["tables", "sdf_0", "sdf_1", "color_0", "color_1", "color_2", "sharpness_log"]
+
+
+class StepWorkspace:
+    """Device buffers of one step, grown geometrically with the kept-sample count."""
+
+    def __init__(self, params, dev):
+        self.dev = dev
+        self.m = 0
+        self.cap = 0
+        self.grads = torch.zeros_like(params.flat)
+        self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.count64 = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.report = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.report_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        self.p_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+
+    def rays(self, m):
+        if m != self.m:
+            d = self.dev
+            self.o = torch.empty((m, 3), dtype=torch.float64, device=d)
+            self.d = torch.empty((m, 3), dtype=torch.float64, device=d)
+            self.tgt = torch.empty((m, 3), dtype=torch.float64, device=d)
+            self.counts = torch.empty(m, dtype=torch.int32, device=d)
+            self.offsets = torch.empty(m + 1, dtype=torch.int32, device=d)
+            self.rendered = torch.empty((m, 3), dtype=torch.float64, device=d)
+            self.resid = torch.empty(m, dtype=torch.float64, device=d)
+            self.m = m
+
+    def samples(self, P):
+        if P > self.cap:
+            cap = max(int(P * 1.25), 1 << 16)
+            d = self.dev
+            self.ray_ids = torch.empty(cap, dtype=torch.int32, device=d)
+            self.pos32 = torch.empty((cap, 3), dtype=torch.float32, device=d)
+            self.sdf = torch.empty(cap, dtype=torch.float32, device=d)
+            self.colors = torch.empty((cap, 3), dtype=torch.float32, device=d)
+            self.alphas = torch.empty(cap, dtype=torch.float64, device=d)
+            self.weights = torch.empty(cap, dtype=torch.float64, device=d)
+            self.tb = torch.empty(cap, dtype=torch.float64, device=d)
+            self.dl_dc = torch.empty((cap, 3), dtype=torch.float32, device=d)
+            self.dl_dsdf = torch.empty(cap, dtype=torch.float32, device=d)
+            self.cap = cap
+
+
+class TrainState:
+    """Parameters, moments, occupancy, rng and step (`trainer.py:175-212`)."""
+
+    def __init__(self, params, occ, config, rng, step=0, dp=None):
+        self.params, self.occ, self.config, self.rng, self.step = params, occ, config, rng, step
+        self.dp = dp or DataParallel.from_env()
+        dev = params.flat.device
+        self.m_flat = torch.zeros_like(params.flat)
+        self.v_flat = torch.zeros_like(params.flat)
+        lay = params.layout
+        sdf_m, col_m, tab_m = lay.views(self.m_flat)
+        sdf_v, col_v, tab_v = lay.views(self.v_flat)
+        self.adam = {"tables": AdamState(tab_m, tab_v)}
+        for i in range(len(sdf_m)):
+            self.adam[f"sdf_{i}"] = AdamState(sdf_m[i], sdf_v[i])
+        for i in range(len(col_m)):
+            self.adam[f"color_{i}"] = AdamState(col_m[i], col_v[i])
+        self.adam["sharpness_log"] = AdamState(torch.zeros(1, dtype=torch.float64, device=dev),
+                                               torch.zeros(1, dtype=torch.float64, device=dev))
+        self.ws = StepWorkspace(params, dev)
+
+    @classmethod
+    def create(cls, config, aabb=((-1, -1, -1), (1, 1, 1)), dp=None):
+        """Seeded init in the reference's draw order (`trainer.py:192-212`)."""
+        rng = np.random.default_rng(config.seed)
+        fcfg = fieldmod.FieldConfig(config.num_levels, config.min_resolution,
+                                    config.max_resolution, config.features_per_level,
+                                    config.table_size, config.hidden_width, aabb)
+        params = fieldmod.SdfFieldParams.create(fcfg, rng, sharpness=config.init_sharpness)
+        fieldmod.sal_geometry_init(params, config.init_radius, rng)
+        occ = renderer.OccupancyGrid(config.occupancy_resolution, aabb, config.occupancy_threshold)
+        return cls(params, occ, config, rng, dp=dp)
+
+
+def _upload_batch(ws, batch, lo, hi, stream):
+    """Copy rays [lo, hi) of the batch into the workspace (pinned, async)."""
+    for dst, src in ((ws.o, batch.origins), (ws.d, batch.directions), (ws.tgt, batch.target_colors)):
+        if isinstance(src, torch.Tensor):
+            s = src[lo:hi]
+            dst.copy_(s, non_blocking=True)
+        else:
+            h = torch.from_numpy(np.ascontiguousarray(src[lo:hi], np.float64))
+            dst.copy_(h.pin_memory(), non_blocking=True)
+
+
+def train_step(state, dataset, time_index=0, batch=None):
+    """One optimisation step (`trainer.py:281-310`); returns a LossReport.
+
+    `batch` (a RayBatch of numpy arrays or CUDA/pinned tensors) replays a given global
+    batch instead of sampling; the rng is then not consumed."""
+    cfg = state.config
+    params, occ, ws, dp = state.params, state.occ, state.ws, state.dp
+    st = torch.cuda.current_stream()
+    sp = _lib.stream_ptr(st)
+    level = level_schedule(state.step, cfg)
+    if state.step % cfg.occupancy_update_every == 0:
+        renderer.update_occupancy(occ, params, level)
+    if batch is None:
+        batch = scene_io.sample_ray_batch(dataset, time_index, cfg.batch_size, cfg.fg_fraction,
+                                          state.rng)
+    m_total = batch.count
+    lo, hi = dp.shard(m_total)
+    m = hi - lo
+    ws.rays(m)
+    _upload_batch(ws, batch, lo, hi, st)
+
+    # K1: march (count, scan) -> P -> fill
+    renderer.march_count_and_scan(ws.o, ws.d, occ, ws.counts, ws.offsets, st)
+    ws.p_host.copy_(ws.offsets[m:m + 1], non_blocking=True)
+    st.synchronize()
+    P = int(ws.p_host[0])
+    P_glob = dp.allreduce_count(P, ws.dev)
+    ws.samples(max(P, 1))
+    o = occ.struct()
+    _lib.call("ns2b_march_fill", _lib.ptr(ws.o), _lib.ptr(ws.d), m, ctypes.byref(o),
+              _lib.ptr(ws.offsets), _lib.ptr(ws.ray_ids), None, None, _lib.ptr(ws.pos32), sp)
+    count = ws.offsets[m:m + 1]
+    ws.sums.zero_()
+    s = params.sharpness
+    na = enc.active_level_count(params.grid, level)
+    f = params.field_struct(na)
+    # K2: field forward (+ Eikonal sum)
+    _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
+              _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf), _lib.ptr(ws.colors), None,
+              None, _lib.ptr(ws.sums[3:4]), sp)
+    # K3/K4: composite + Huber + compositing backward
+    _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf), _lib.ptr(ws.colors),
+              s, _lib.ptr(ws.tgt), cfg.huber_delta, float(m_total), _lib.ptr(ws.rendered),
+              _lib.ptr(ws.resid), _lib.ptr(ws.alphas), _lib.ptr(ws.weights), _lib.ptr(ws.tb),
+              _lib.ptr(ws.dl_dc), _lib.ptr(ws.dl_dsdf), _lib.ptr(ws.sums), sp)
+    lay = params.layout
+    end = lay.active_end(na)
+    ws.flag.zero_()
+    if P_glob > 0:
+        ws.grads[:end].zero_()
+        ws.count64.fill_(P_glob)
+        # K5: field backward with the fused Eikonal cotangent
+        sdf_g, col_g, tab_g = lay.views(ws.grads)
+        _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
+                  _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.dl_dc), _lib.ptr(ws.dl_dsdf),
+                  None, cfg.eikonal_weight, _lib.ptr(ws.count64), _lib.ptr(sdf_g[0]),
+                  _lib.ptr(col_g[0]), _lib.ptr(tab_g), sp)
+        if dp.active:
+            dp.allreduce_(ws.grads[:end])
+            dp.allreduce_(ws.sums[:4])
+        _apply_gradients(state, na, s)
+    elif dp.active:
+        dp.allreduce_(ws.sums[:4])
+    # one D2H: [huber sum, dslog, sq err, eik sum, flag, slog]
+    ws.report[:4].copy_(ws.sums[:4])
+    ws.report[4:5].copy_(ws.flag.to(torch.float64))
+    ws.report[5:6].copy_(params.sharpness_log)
+    ws.report_host.copy_(ws.report, non_blocking=True)
+    st.synchronize()
+    rep = ws.report_host.tolist()
+    if rep[4] != 0:
+        bits = int(rep[4])
+        name = next(n for n in _CHECK_ORDER if bits & (1 << _CHECK_ORDER.index(n)))
+        raise FloatingPointError(f"divergence: non-finite gradient for {name}")
+    params.refresh_host_mirror(rep[5])
+    c_loss = rep[0] / m_total
+    e_loss = rep[3] / P_glob if P_glob > 0 else 0.0
+    report = LossReport(step=state.step, color=c_loss, eikonal=e_loss,
+                        total=c_loss + cfg.eikonal_weight * e_loss, level=level,
+                        psnr=psnr_from_mse(rep[2] / (3.0 * m_total)), sample_count=P_glob)
+    state.last_dslog = rep[1] * s
+    state.step += 1
+    return report
+
+
+def _apply_gradients(state, n_active, sharpness):
+    """Divergence check, s_log Adam, then one multi-group Adam launch over
+    [sdf_0 | sdf_1 | color_0..2 | tables[:n_active]] (`trainer.py:243-278`)."""
+    cfg = state.config
+    params, ws = state.params, state.ws
+    lay = params.layout
+    sp = _lib.stream_ptr()
+    scale = lr_factor(state.step, cfg.total_steps, cfg.lr_final_fraction)
+    lr_t, lr_m = cfg.lr_tables * scale, cfg.lr_mlp * scale
+    names = ["sdf_0", "sdf_1", "color_0", "color_1", "color_2", "tables"]
+    offs = lay.sdf_offs + lay.color_offs + [lay.tables_off]
+    lens = [a * b for a, b in lay.sdf_shapes + lay.color_shapes] + [n_active * lay.T * 2]
+    lrs = [lr_m] * 5 + [lr_t]
+    if n_active == 0:
+        names, offs, lens, lrs = names[:5], offs[:5], lens[:5], lrs[:5]
+    for n in names:
+        state.adam[n].t += 1
+    state.adam["sharpness_log"].t += 1
+    # one finite check over all fp32 groups; segment k sets bit k, listed in the
+    # reference's check order so bit k names _CHECK_ORDER[k]
+    chk = [n for n in _CHECK_ORDER[:-1] if n in names]
+    idx = [names.index(n) for n in chk]
+    _lib.call("ns2b_check_finite", _lib.ptr(ws.grads), _lib.i64_array([offs[i] for i in idx]),
+              _lib.i64_array([lens[i] for i in idx]), len(idx), _lib.ptr(ws.flag), sp)
+    sl = state.adam["sharpness_log"]
+    _lib.call("ns2b_adam_scalar_f64", _lib.ptr(params.sharpness_log), _lib.ptr(ws.sums[1:2]),
+              float(sharpness), _lib.ptr(sl.m), _lib.ptr(sl.v), sl.t, lr_m, cfg.adam_beta1,
+              cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), _lib.ptr(ws.flag),
+              _CHECK_ORDER.index("sharpness_log"), sp)
+    ts = [state.adam[n].t for n in names]
+    _lib.call("ns2b_adam_multi", _lib.ptr(params.flat), _lib.ptr(ws.grads), _lib.ptr(state.m_flat),
+              _lib.ptr(state.v_flat), _lib.i64_array(offs), _lib.i64_array(lens),
+              _lib.f64_array(lrs), _lib.i64_array(ts), len(names), cfg.adam_beta1,
+              cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
+

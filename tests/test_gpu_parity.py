@@ -1,0 +1,248 @@
+"""GPU parity: libns2b kernels vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE north star): hash indices and sample counts bit-exact; encodings,
+SDF, normals, colours, losses and gradients within 1e-3 (relL2 and max-abs over
+max|ref|) in fp32 arithmetic with fp32 table storage.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers skip at collection
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import cases  # noqa: E402
+from helpers import np_, product_params_from_oracle, product_state_from_oracle  # noqa: E402
+from oracle import field as ofield  # noqa: E402
+from oracle import hashgrid as ohg  # noqa: E402
+from oracle import kernels as ok  # noqa: E402
+from oracle import render as orender  # noqa: E402
+from oracle import scene as oscene  # noqa: E402
+from oracle import train as otrain  # noqa: E402
+from paper_2212_05231_b200 import _kernels as pk  # noqa: E402
+from paper_2212_05231_b200 import _lib  # noqa: E402
+from paper_2212_05231_b200 import field as pfield  # noqa: E402
+from paper_2212_05231_b200 import renderer as prender  # noqa: E402
+from paper_2212_05231_b200 import trainer as ptrain  # noqa: E402
+from parity import assert_close, assert_exact  # noqa: E402
+
+TOL = 1e-3
+
+
+def test_library_is_the_cuda_path():
+    n0 = _lib.launch_count()
+    xn = cases.grid_points(seed=1)
+    tables = cases.trained_tables(8, 2**14)
+    grid = ohg.HashGrid(**cases.GRIDS["c1"])
+    pk.interp_features(xn, tables, grid.resolutions, 8)
+    assert _lib.launch_count() > n0
+
+
+@pytest.mark.parametrize("name", list(cases.GRIDS))
+@pytest.mark.parametrize("na_kind", ["all", "masked"])
+def test_interp_and_scatter(name, na_kind):
+    spec = cases.GRIDS[name]
+    L, T = spec["num_levels"], spec["table_size"]
+    na = L if na_kind == "all" else 3
+    grid = ohg.HashGrid(**spec)
+    tables = cases.trained_tables(L, T)
+    rng = np.random.default_rng(4)
+    xn = np.concatenate([cases.grid_points(seed=3),
+                         rng.uniform(0, 1, (20000, 3)).astype(np.float32)])
+    inv = np.ascontiguousarray(1.0 / grid.aabb_extent, np.float32)
+    ref = ok.interp_full(xn, tables, grid.resolutions, na, inv)
+    got = pk.interp_full(xn, tables, grid.resolutions, na, inv)
+    assert_exact(got[2], ref[2], "corner indices")
+    for k, nm in ((0, "feats"), (1, "jac"), (3, "cw"), (4, "cdw")):
+        assert_close(got[k], ref[k], 1e-5, nm)
+    assert_close(pk.interp_features(xn, tables, grid.resolutions, na), ref[0], 1e-5, "features")
+    dfeat = rng.standard_normal((xn.shape[0], 2 * L)).astype(np.float32)
+    u = rng.standard_normal((xn.shape[0], 2 * L, 3)).astype(np.float32)
+    for fn_o, fn_p, w, d in ((ok.scatter_first, pk.scatter_first, ref[3], dfeat),
+                             (ok.scatter_second, pk.scatter_second, ref[4], u)):
+        g_o = np.zeros_like(tables)
+        g_p = np.zeros_like(tables)
+        fn_o(g_o, ref[2], w, d, na)
+        fn_p(g_p, ref[2], w, d, na)
+        assert_close(g_p, g_o, 1e-5, fn_o.__name__)
+
+
+def test_adam_step_bit_exact():
+    rng = np.random.default_rng(0)
+    for dt in (np.float32, np.float64):
+        p = rng.standard_normal(5000).astype(dt)
+        g = rng.standard_normal(5000).astype(dt)
+        m = (0.1 * rng.standard_normal(5000)).astype(dt)
+        v = np.abs(0.1 * rng.standard_normal(5000)).astype(dt)
+        po, mo, vo = p.copy(), m.copy(), v.copy()
+        ok.adam_step(po, g, mo, vo, 7, 1e-2, 0.9, 0.99, 1e-15)
+        pk.adam_step(p, g, m, v, 7, 1e-2, 0.9, 0.99, 1e-15)
+        assert_exact(m, mo, "m")
+        assert_exact(v, vo, "v")
+        assert_exact(p, po, "param")
+
+
+def _c1_state(level_init=8, seed=0):
+    cfg = otrain.TrainConfig(batch_size=1024, num_levels=8, table_size=2**14, seed=seed,
+                             level_init=level_init)
+    return otrain.TrainState.create(cfg)
+
+
+@pytest.fixture(scope="module")
+def sphere64():
+    return oscene.make_synthetic("sphere", views=8, seed=0, image_size=64)
+
+
+def test_march_bit_exact(sphere64):
+    ost = _c1_state()
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    b = oscene.sample_ray_batch(sphere64, 0, 4096, 0.9, np.random.default_rng(1))
+    # add rays that graze / miss / start inside the box and axis-parallel rays
+    extra_o = np.array([[0.0, 0.0, 0.0], [3.0, 0.2, 0.1], [0.5, 2.0, -0.3], [-0.99, -0.99, -0.99]])
+    extra_d = np.array([[1.0, 0.0, 0.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0], [0.0, 0.0, 1.0]])
+    o = np.concatenate([b.origins, extra_o])
+    d = np.concatenate([b.directions, extra_d])
+    ref = orender.march_rays(o, d, ost.occ)
+    pocc = prender.OccupancyGrid(128)
+    pocc.set_bits(ost.occ.bits)
+    got = prender.march_rays(o, d, pocc)
+    assert got.sample_count == ref.ray_ids.shape[0]
+    assert_exact(np_(got.ray_ids).astype(np.int64), ref.ray_ids, "ray ids")
+    assert_exact(np_(got.t), ref.t, "t")
+    assert_exact(np_(got.positions), ref.positions, "positions")
+    assert_exact(np_(got.positions32), ref.positions.astype(np.float32), "fp32 positions")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("lam", ["all", 3])
+def test_field_forward_backward(name, lam):
+    from test_oracle_golden import oracle_field_params
+
+    op = oracle_field_params(name)
+    pp = product_params_from_oracle(op)
+    lam = op.grid.num_levels if lam == "all" else lam
+    rng = np.random.default_rng(9)
+    x = cases.world_points(seed=5, n=4096)
+    v = rng.standard_normal((x.shape[0], 3))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    oc = ofield.eval_field(op, x, v, lam)
+    pc = pfield.eval_field(pp, x, v, lam)
+    assert_close(np_(pc.d), oc.d, TOL, "d")
+    assert_close(np_(pc.g), oc.g, TOL, "g")
+    assert_close(np_(pc.normals), oc.normals, TOL, "normals")
+    assert_close(np_(pc.colors), oc.colors, TOL, "colors")
+    assert_close(np_(pfield.field_sdf_only(pp, x, lam)), ofield.field_sdf_only(op, x, lam), TOL)
+    dl_dc = rng.standard_normal((x.shape[0], 3))
+    dl_dd = rng.standard_normal(x.shape[0])
+    dl_dn = rng.standard_normal((x.shape[0], 3)).astype(np.float32)
+    og = ofield.field_backward(op, oc, dl_dc=dl_dc, dl_dd=dl_dd, dl_dn=dl_dn)
+    pg = pfield.field_backward(pp, pc, dl_dc=dl_dc, dl_dd=dl_dd, dl_dn=dl_dn)
+    for i in range(2):
+        assert_close(np_(pg.sdf_layers[i]), og.sdf_layers[i], TOL, f"sdf{i}")
+    for i in range(3):
+        assert_close(np_(pg.color_layers[i]), og.color_layers[i], TOL, f"color{i}")
+    gt = np_(pg.tables)
+    for lv in range(op.grid.num_levels):
+        assert_close(gt[lv], og.tables[lv], TOL, f"tables level {lv}")
+
+
+def test_render_and_cotangents(sphere64):
+    ost = _c1_state()
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    ost.params.grid.tables[:] = cases.trained_tables(8, 2**14, scale=0.05)
+    pp = product_params_from_oracle(ost.params)
+    pocc = prender.OccupancyGrid(128)
+    pocc.set_bits(ost.occ.bits)
+    b = oscene.sample_ray_batch(sphere64, 0, 4096, 0.9, np.random.default_rng(2))
+    oc, orec = orender.render_rays(b, ost.params, ost.occ, 8)
+    pc, prec = prender.render_rays(b, pp, pocc, 8)
+    assert prec.sample_count == orec.sample_count
+    assert_exact(np_(prec.interval_first), orec.interval_first, "intervals")
+    assert_close(np_(pc), oc, TOL, "rendered")
+    assert_close(np_(prec.alphas), orec.alphas, TOL, "alphas")
+    assert_close(np_(prec.weights), orec.weights, TOL, "weights")
+    assert_close(np_(prec.transmittance), orec.transmittance, TOL, "residual T")
+    g = np.random.default_rng(3).standard_normal((4096, 3)) / 4096
+    od = orender.backward_cotangents(orec, g)
+    pd = prender.backward_cotangents(prec, g)
+    assert_close(np_(pd[0]), od[0], TOL, "dl_dc")
+    assert_close(np_(pd[1]), od[1], TOL, "dl_dsdf")
+    assert abs(pd[2] - od[2]) <= TOL * max(abs(od[2]), 1e-12)
+
+
+def test_occupancy_update():
+    ost = _c1_state()
+    pst = product_state_from_oracle(ost)
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    prender.update_occupancy(pst.occ, pst.params, 8)
+    pb = np_(pst.occ.bits).astype(bool)
+    flips = np.count_nonzero(pb != ost.occ.bits)
+    assert flips <= 1e-4 * pb.size, f"{flips} occupancy bits differ"
+    assert_close(np_(pst.occ.ema), ost.occ.ema, TOL, "ema")
+
+
+@pytest.mark.parametrize("level_init", [2, 8])
+def test_train_steps_match_oracle(sphere64, level_init):
+    """Three full steps from the same init and the same ray batches."""
+    cfg = otrain.TrainConfig(batch_size=2048, num_levels=8, table_size=2**14, seed=0,
+                             level_init=level_init)
+    ost = otrain.TrainState.create(cfg)
+    orender.update_occupancy(ost.occ, ost.params, otrain.level_schedule(0, cfg))
+    ost.step = 1  # steps 1..3: no occupancy refresh, so both sides march the same bits
+    pst = product_state_from_oracle(ost)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        b = oscene.sample_ray_batch(sphere64, 0, cfg.batch_size, cfg.fg_fraction, rng)
+        ro = otrain.train_step(ost, sphere64, batch=b)
+        rp = ptrain.train_step(pst, sphere64, batch=b)
+        assert rp.sample_count == ro.sample_count
+        assert rp.level == ro.level
+        for k in ("color", "eikonal", "total", "psnr"):
+            a, r = getattr(rp, k), getattr(ro, k)
+            assert abs(a - r) <= TOL * max(abs(r), 1e-9), f"{k}: {a} vs {r}"
+        pp = pst.params
+        for i in range(2):
+            assert_close(np_(pp.sdf_net.layers[i]), ost.params.sdf_net.layers[i], TOL, f"sdf{i}")
+        for i in range(3):
+            assert_close(np_(pp.color_net.layers[i]), ost.params.color_net.layers[i], TOL,
+                         f"color{i}")
+        assert_close(np_(pp.grid.tables), ost.params.grid.tables, TOL, "tables")
+        assert abs(pp.sharpness - ost.params.sharpness) <= 1e-6 * ost.params.sharpness
+
+
+def test_oracle_loop_on_gpu_kernels(sphere64, monkeypatch):
+    """Seam (1): the oracle's unmodified numpy loop with its compiled kernels swapped
+    for libns2b's array-level entry points gives the oracle's results."""
+    cfg = otrain.TrainConfig(batch_size=512, num_levels=8, table_size=2**14, seed=0, level_init=8)
+    a = otrain.TrainState.create(cfg)
+    b_ = otrain.TrainState.create(cfg)
+    rng = np.random.default_rng(6)
+    batch = oscene.sample_ray_batch(sphere64, 0, cfg.batch_size, cfg.fg_fraction, rng)
+    ra = otrain.train_step(a, sphere64, batch=batch)
+    for fn in ("interp_features", "interp_full", "scatter_first", "scatter_second", "adam_step"):
+        monkeypatch.setattr(ok, fn, getattr(pk, fn))
+    rb = otrain.train_step(b_, sphere64, batch=batch)
+    assert rb.sample_count == ra.sample_count
+    assert abs(rb.total - ra.total) <= TOL * abs(ra.total)
+    assert_close(b_.params.grid.tables, a.params.grid.tables, TOL, "tables")
+    assert_close(b_.params.sdf_net.layers[0], a.params.sdf_net.layers[0], TOL, "sdf0")
+
+
+def test_divergence_raises(sphere64):
+    cfg = otrain.TrainConfig(batch_size=256, num_levels=8, table_size=2**14, seed=0, level_init=8)
+    ost = otrain.TrainState.create(cfg)
+    pst = product_state_from_oracle(ost)
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    pst.occ.set_bits(ost.occ.bits)
+    pst.params.color_net.layers[1].fill_(float("nan"))
+    before = np_(pst.params.grid.tables).copy()
+    b = oscene.sample_ray_batch(sphere64, 0, 256, 0.9, np.random.default_rng(0))
+    pst.step = 1  # skip the occupancy refresh
+    with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for"):
+        ptrain.train_step(pst, sphere64, batch=b)
+    assert np.array_equal(np_(pst.params.grid.tables), before)
