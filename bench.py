@@ -1,0 +1,393 @@
+"""Benchmark: NeuS2 static training step, rays/s incl. the 2nd-order Eikonal backward.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1]
+
+Workload (BASELINE.json configs[1], "c2"): synthetic DTU-shaped static scene
+(two-spheres, 49 orbit views, 1600x1200), 2^18 rays/batch, 16-level 2^19 hash grid,
+64-wide SDF + colour MLPs, Eikonal weight 0.1, all 16 levels active (lambda fixed),
+occupancy frozen from the step-0 refresh of the SAL init.  Synthetic data, seeded.
+
+`value`  : whole-job rays/s with each step's ray batch already resident in HBM.
+`e2e`    : same metric through the public API (trainer.train_step) with the batch in
+           pinned host memory, copied H2D every step, and the loss report read back.
+`roofline`: the dominant kernel (per-kernel CUDA events on the launching stream over
+           the timed region) against the measured peaks; see DESIGN.md for the
+           algorithmic bytes/flops per sample.
+`cpu_baseline`: the CPU oracle (restatement of the reference, tests-pinned) timed on
+           this host on a bounded sample of the same workload.
+--impl reference: times that CPU implementation alone as the reference arm.
+
+Multi-GPU: launch with torchrun; each rank takes a contiguous slice of the SAME global
+batch (weak scaling: global batch = N x 2^18), NCCL all-reduce of P and gradients.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+RAYS = 1 << 18
+METRIC = "training rays/sec incl. 2nd-order Eikonal bwd; ms/iter at 1/2/4/8 B200"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback"
+    return d
+
+
+def workload(name):
+    if name == "c1":
+        return dict(workload="c1: sphere 8 views 64x64, 4096 rays, 8-level 2^14 grid", rays=4096,
+                    levels=8, table=2**14, scene=("sphere", 8, 64, 64, 64 * 1.4))
+    return dict(workload="c2: DTU-shaped two-spheres 49 views 1600x1200, 2^18 rays/batch, "
+                         "16-level 2^19 hash grid, 64-wide SDF+colour MLPs, Eikonal bwd",
+                rays=RAYS, levels=16, table=2**19, scene=("two-spheres", 49, 1600, 1200, 1.4 * 1200))
+
+
+def make_dataset(wl, device=None):
+    """DTU-shaped scene.  The per-pixel ray tracing of the 49 views is data preparation
+    (not the timed path) and runs on the GPU when one is available."""
+    from paper_2212_05231_b200 import scene_io
+
+    preset, views, w, h, focal = wl["scene"]
+    if device is None or w * h <= 64 * 64:
+        return scene_io.make_synthetic(preset, views=views, seed=0, width=w, height=h, focal=focal)
+    return _make_dataset_gpu(preset, views, w, h, focal, device)
+
+
+def _make_dataset_gpu(preset, views, w, h, focal, device):
+    import torch
+
+    from paper_2212_05231_b200 import scene_io
+
+    spheres, motion = scene_io.preset_scene(preset)
+    rng = np.random.default_rng(0)
+    elev = np.deg2rad(np.where(np.arange(views) % 2 == 0, 18.0, -12.0))
+    azim = 2 * np.pi * np.arange(views) / views + rng.uniform(0, 2 * np.pi / views)
+    light = torch.tensor(scene_io.LIGHT, dtype=torch.float64, device=device)
+    ys, xs = torch.meshgrid(torch.arange(h, device=device, dtype=torch.float64),
+                            torch.arange(w, device=device, dtype=torch.float64), indexing="ij")
+    frames = []
+    for v in range(views):
+        pose = scene_io.orbit_pose(azim[v], elev[v], 2.6)
+        R = torch.tensor(pose[:3, :3], device=device)
+        eye = torch.tensor(pose[:3, 3], device=device)
+        dc = torch.stack([(xs.reshape(-1) + 0.5 - w / 2.0) / focal,
+                          (ys.reshape(-1) + 0.5 - h / 2.0) / focal,
+                          torch.ones(h * w, device=device, dtype=torch.float64)], 1)
+        d = dc @ R.T
+        d = d / torch.linalg.norm(d, dim=1, keepdim=True)
+        best = torch.full((h * w,), float("inf"), device=device, dtype=torch.float64)
+        which = torch.full((h * w,), -1, device=device, dtype=torch.int64)
+        for si, (c, r, _) in enumerate(spheres):
+            oc = eye - torch.tensor(c, device=device)
+            b = d @ oc
+            disc = b * b - (oc @ oc - r * r)
+            t = torch.where(disc >= 0, -b - torch.sqrt(torch.clamp(disc, min=0.0)),
+                            torch.full_like(b, float("inf")))
+            t = torch.where(t > 1e-6, t, torch.full_like(t, float("inf")))
+            closer = t < best
+            best = torch.where(closer, t, best)
+            which = torch.where(closer, torch.full_like(which, si), which)
+        hit = torch.isfinite(best)
+        col = torch.zeros((h * w, 3), device=device, dtype=torch.float64)
+        for si, (c, r, albedo) in enumerate(spheres):
+            sel = hit & (which == si)
+            p = eye + best[sel, None] * d[sel]
+            nrm = (p - torch.tensor(c, device=device)) / r
+            lam = torch.clamp(nrm @ light, min=0.0)
+            col[sel] = torch.tensor(albedo, device=device) * (0.3 + 0.7 * lam)[:, None]
+        rgb8 = (col.clamp(0, 1) * 255).round().to(torch.uint8).reshape(h, w, 3).cpu().numpy()
+        fr = scene_io.CameraFrame(focal, focal, w / 2.0, h / 2.0, w, h, pose,
+                                  rgb8.astype(np.float64) / 255.0,
+                                  hit.reshape(h, w).to(torch.float64).cpu().numpy(), 0)
+        frames.append(fr)
+    return scene_io.MultiViewDataset(frames)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.gpu = gpu_index
+        self.path = Path(os.environ.get("NS2B_CLOCKS_CSV", f"/tmp/ns2b_clocks_{os.getpid()}.csv"))
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.fh.close()
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip() == "Active"})
+        load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU ---
+def cpu_oracle_rate(wl, rays_sample, steps=1, threads=None):
+    """Oracle train_step on this host: returns (rays/s, seconds, P, cores)."""
+    threads = threads or os.cpu_count()
+    os.environ["NS2B_ORACLE_THREADS"] = str(threads)
+    from oracle import kernels as ok
+
+    ok.NUM_THREADS = threads
+    from oracle import render as orender
+    from oracle import train as otrain
+    from paper_2212_05231_b200 import scene_io
+
+    cfg = otrain.TrainConfig(batch_size=rays_sample, num_levels=wl["levels"],
+                             table_size=wl["table"], seed=0, level_init=wl["levels"])
+    st = otrain.TrainState.create(cfg)
+    # occupancy from the SAL init (the frozen grid of the GPU run), computed on the CPU
+    orender.update_occupancy(st.occ, st.params, wl["levels"])
+    st.step = 1
+    ds = wl["_dataset"]
+    rng = np.random.default_rng(123)
+    times, counts = [], []
+    for _ in range(steps):
+        b = scene_io.sample_ray_batch(ds, 0, rays_sample, 0.9, rng)
+        t0 = time.perf_counter()
+        rep = otrain.train_step(st, ds, batch=b)
+        times.append(time.perf_counter() - t0)
+        counts.append(rep.sample_count)
+    med = statistics.median(times)
+    return rays_sample / med, med, int(np.median(counts)), threads
+
+
+def run_reference(args, wl):
+    from paper_2212_05231_b200.parallel import init_from_env
+
+    dp = init_from_env("gloo") if "RANK" in os.environ else None
+    if dp is not None and dp.rank != 0:
+        return
+    wl["_dataset"] = make_dataset(wl, device=None if args.config == "c1" else _maybe_gpu())
+    rays_sample = 2048 if args.config == "c2" else wl["rays"]
+    # warm-up (allocations, first-touch) then timed steps
+    cpu_oracle_rate(wl, rays_sample, steps=max(1, min(args.warmup, 1)))
+    rate, sec, P, cores = cpu_oracle_rate(wl, rays_sample, steps=max(1, args.steps))
+    line = {
+        "metric": METRIC, "value": rate, "unit": "rays/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3 * wl["rays"] / rays_sample,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32/fp64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": wl["workload"], "global_batch": wl["rays"], "levels": wl["levels"],
+                   "table_size": wl["table"], "parallelism": "cpu"},
+        "cpu_baseline": {"value": rate, "unit": "rays/s", "cores": cores, "kind": "port",
+                         "sample": f"{rays_sample}-ray sub-batch of the workload (P~{P} samples) per "
+                                   f"step, median of {args.steps} steps, extrapolated per ray"},
+        "e2e": {"value": rate, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _maybe_gpu():
+    try:
+        import torch
+
+        return torch.device("cuda", 0) if torch.cuda.is_available() else None
+    except Exception:  # pragma: no cover
+        return None
+
+
+# ------------------------------------------------------------------ GPU ---
+def l2_probes(dev, nbytes=64 << 20):
+    """Measured L2 read and random-RED bandwidth (GB/s) over a working-set-sized buffer."""
+    import torch
+
+    from paper_2212_05231_b200 import _lib
+
+    buf = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    st = _lib.stream_ptr()
+    iters = 20
+    for _ in range(2):
+        _lib.call("ns2b_bench_l2_read", _lib.ptr(buf), buf.numel(), 2, _lib.ptr(sink), st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _lib.call("ns2b_bench_l2_read", _lib.ptr(buf), buf.numel(), iters, _lib.ptr(sink), st)
+    e1.record()
+    torch.cuda.synchronize()
+    read_gbs = nbytes * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    nops = 1 << 27
+    _lib.call("ns2b_bench_red", _lib.ptr(buf), buf.numel() // 2, 1 << 20, 1, st)
+    e0.record()
+    _lib.call("ns2b_bench_red", _lib.ptr(buf), buf.numel() // 2, nops, 7, st)
+    e1.record()
+    torch.cuda.synchronize()
+    red_s = e0.elapsed_time(e1) * 1e-3
+    return {"l2_read_gbs": read_gbs, "red_f32x2_gops": nops / red_s / 1e9,
+            "red_f32x2_gbs": nops * 8 / red_s / 1e9, "buffer_mib": nbytes >> 20}
+
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2212_05231_b200 import _lib, renderer, trainer
+    from paper_2212_05231_b200.parallel import init_from_env
+    from paper_2212_05231_b200.scene_io import DeviceRaySource
+
+    dp = init_from_env()
+    rank, world = dp.rank, dp.world
+    dev = torch.device("cuda", torch.cuda.current_device())
+    torch.manual_seed(0)
+    ds = make_dataset(wl, dev)
+    m_global = wl["rays"] * world  # weak scaling: each GPU keeps 2^18 rays
+    cfg = trainer.TrainConfig(batch_size=m_global, num_levels=wl["levels"], table_size=wl["table"],
+                              seed=0, level_init=wl["levels"], total_steps=15000)
+    st = trainer.TrainState.create(cfg, dp=dp)
+    renderer.update_occupancy(st.occ, st.params, wl["levels"])  # step-0 refresh, then frozen
+    st.step = 1
+    nb = args.warmup + args.steps
+    src = DeviceRaySource(ds, m_global, nb, seed=1, device=dev)
+    from paper_2212_05231_b200.scene_io import RayBatch
+
+    def batch(i, host=False):
+        o, d, t = src.host[i] if host else src.dev[i]
+        return RayBatch(o, d, t, None)
+
+    def barrier():
+        if dp.active:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(host):
+        for i in range(args.warmup):
+            trainer.train_step(st, ds, batch=batch(i, host))
+        barrier()
+        n0 = _lib.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        reps = []
+        for i in range(args.warmup, nb):
+            reps.append(trainer.train_step(st, ds, batch=batch(i, host)))
+        e1.record()
+        barrier()
+        wall = time.perf_counter() - t0
+        ms = e0.elapsed_time(e1)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dp.max_(t)
+        return float(t.item()), _lib.launch_count() - n0, reps, wall
+
+    # kernel-resident leg (value) with per-kernel timers + clocks
+    clocks = ClockSampler(torch.cuda.current_device())
+    st.timers = {}
+    clocks.start()
+    ms_dev, launches, reps, wall = timed(host=False)
+    clk = clocks.stop()
+    timers = st.timers
+    st.timers = None
+    per_kernel = {k: statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:])
+                  for k, v in timers.items()}
+    # end-to-end leg through the public API with host batches
+    ms_e2e, _, _, _ = timed(host=True)
+    P_mean = statistics.mean(r.sample_count for r in reps)
+    value = m_global * args.steps / (ms_dev * 1e-3)
+    e2e = m_global * args.steps / (ms_e2e * 1e-3)
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    l2 = l2_probes(dev)
+    dom = max(per_kernel, key=per_kernel.get)
+    Pl = P_mean / world  # per-rank samples per launch
+    L = wl["levels"]
+    # algorithmic traffic of the field backward per sample: re-gather (8 corners x 2
+    # fp32 features x L) + fused first/second-order scatter (same rows, RED) + inputs
+    bytes_bwd = Pl * (8 * 2 * 4 * L * 2 + 32)
+    bytes_fwd = Pl * (8 * 2 * 4 * L + 28)
+    alg = {"field_backward": bytes_bwd, "field_forward": bytes_fwd}
+    ach_gbs = alg.get(dom, bytes_bwd) / (per_kernel[dom] * 1e-3) / 1e9
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": ach_gbs, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach_gbs / peaks["hbm_gbs"],
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['source']})",
+                "traffic": None,
+                "l2_frac": ach_gbs / l2["l2_read_gbs"], "l2_probe": l2,
+                "algorithmic_bytes_per_sample": alg.get(dom, bytes_bwd) / Pl,
+                "per_kernel_ms": per_kernel, "step_share": per_kernel[dom] / (ms_dev / args.steps)}
+    # CPU baseline on a bounded sample (the oracle, all host cores)
+    wl["_dataset"] = ds
+    cpu = None
+    if not args.no_cpu:
+        rays_sample = 1024 if args.config == "c2" else wl["rays"]
+        rate, sec, Pc, cores = cpu_oracle_rate(wl, rays_sample, steps=1)
+        cpu = {"value": rate, "unit": "rays/s", "cores": cores, "kind": "port",
+               "sample": f"1 oracle train_step on a {rays_sample}-ray sub-batch of the workload "
+                         f"(P={Pc}), {sec:.1f} s, extrapolated per ray"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (fp64 march/composite)",
+        "data": "synthetic",
+        "config": {"workload": wl["workload"], "global_batch": m_global, "rays_per_gpu": wl["rays"],
+                   "levels": L, "table_size": wl["table"], "parallelism": f"dp{world}",
+                   "samples_per_step": P_mean, "lambda": L, "occupancy": "frozen after step-0 refresh",
+                   "l2": "working set > L2 (per-sample buffers ~GBs per step), no flush needed"},
+        "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": m_global // world * 72,
+                "d2h_bytes_per_step": 4 + 64, "ms_per_step": ms_e2e / args.steps},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "loss": {"first": reps[0].total, "last": reps[-1].total},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    args = ap.parse_args()
+    wl = workload(args.config)
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -205,6 +205,13 @@ NS2B_API int ns2b_adam_scalar_f64(double *param, const double *raw_grad, double 
                          double *v, int64_t t, double lr, double beta1, double beta2, double eps,
                          const int32_t *flag, int32_t *flag_out, int32_t flag_bit, void *stream);
 
+/* ------------------------------------------------ in-run roofline probes -- */
+/* L2 read sweep: `iters` passes of 16-B ld.global.cg over buf (nfloats % 4 == 0). */
+NS2B_API int ns2b_bench_l2_read(const float *buf, int64_t nfloats, int32_t iters, float *sink,
+                                void *stream);
+/* nops random float2 REDs over nrows 8-B rows of buf (the scatter's access pattern). */
+NS2B_API int ns2b_bench_red(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,9 +56,12 @@ def interp_full(xn, tables, resolutions, n_active, inv_extent):
 def _scatter(name, grad, cidx, w, d, n_active):
     g = _dev(grad, np.float32)
     nlev, tsize, nfeat = grad.shape
-    _lib.call(name, _lib.ptr(g), nlev, tsize, nfeat, _lib.ptr(_dev(cidx, np.int64)),
-              _lib.ptr(_dev(w, np.float32)), _lib.ptr(_dev(d, np.float32)), cidx.shape[0],
-              int(n_active), _lib.stream_ptr())
+    # keep every device temporary referenced until the kernel has been enqueued and
+    # the result copied back (a dropped tensor's block can be reused by the next
+    # allocation on the stream)
+    ci, wd, dd = _dev(cidx, np.int64), _dev(w, np.float32), _dev(d, np.float32)
+    _lib.call(name, _lib.ptr(g), nlev, tsize, nfeat, _lib.ptr(ci), _lib.ptr(wd), _lib.ptr(dd),
+              cidx.shape[0], int(n_active), _lib.stream_ptr())
     grad[...] = g.cpu().numpy()
 
 

@@ -74,6 +74,8 @@ _SIGS = {
     "ns2b_adam_multi": (ctypes.c_int, [P, P, P, P, P, P, P, P, I32, F64, F64, F64, P, P]),
     "ns2b_adam_scalar_f64": (ctypes.c_int, [P, P, F64, P, P, I64, F64, F64, F64, F64, P, P, I32,
                                             P]),
+    "ns2b_bench_l2_read": (ctypes.c_int, [P, I64, I32, P, P]),
+    "ns2b_bench_red": (ctypes.c_int, [P, I64, I64, ctypes.c_uint32, P]),
 }
 
 _lib = None

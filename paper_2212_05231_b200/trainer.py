@@ -212,6 +212,26 @@ class TrainState:
         return cls(params, occ, config, rng, dp=dp)
 
 
+class _Timer:
+    """Optional per-kernel CUDA-event timing on the launching stream (bench.py)."""
+
+    def __init__(self, store, name, stream):
+        self.store, self.name, self.stream = store, name, stream
+
+    def __enter__(self):
+        if self.store is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record(self.stream)
+        return self
+
+    def __exit__(self, *exc):
+        if self.store is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(self.stream)
+            self.store.setdefault(self.name, []).append((self.e0, e1))
+        return False
+
+
 def _upload_batch(ws, batch, lo, hi, stream):
     """Copy rays [lo, hi) of the batch into the workspace (pinned, async)."""
     for dst, src in ((ws.o, batch.origins), (ws.d, batch.directions), (ws.tgt, batch.target_colors)):
@@ -244,30 +264,36 @@ def train_step(state, dataset, time_index=0, batch=None):
     ws.rays(m)
     _upload_batch(ws, batch, lo, hi, st)
 
+    timers = getattr(state, "timers", None)
     # K1: march (count, scan) -> P -> fill
-    renderer.march_count_and_scan(ws.o, ws.d, occ, ws.counts, ws.offsets, st)
+    with _Timer(timers, "march_count_scan", st):
+        renderer.march_count_and_scan(ws.o, ws.d, occ, ws.counts, ws.offsets, st)
     ws.p_host.copy_(ws.offsets[m:m + 1], non_blocking=True)
     st.synchronize()
     P = int(ws.p_host[0])
     P_glob = dp.allreduce_count(P, ws.dev)
     ws.samples(max(P, 1))
     o = occ.struct()
-    _lib.call("ns2b_march_fill", _lib.ptr(ws.o), _lib.ptr(ws.d), m, ctypes.byref(o),
-              _lib.ptr(ws.offsets), _lib.ptr(ws.ray_ids), None, None, _lib.ptr(ws.pos32), sp)
+    with _Timer(timers, "march_fill", st):
+        _lib.call("ns2b_march_fill", _lib.ptr(ws.o), _lib.ptr(ws.d), m, ctypes.byref(o),
+                  _lib.ptr(ws.offsets), _lib.ptr(ws.ray_ids), None, None, _lib.ptr(ws.pos32), sp)
     count = ws.offsets[m:m + 1]
     ws.sums.zero_()
     s = params.sharpness
     na = enc.active_level_count(params.grid, level)
     f = params.field_struct(na)
     # K2: field forward (+ Eikonal sum)
-    _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
-              _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf), _lib.ptr(ws.colors), None,
-              None, _lib.ptr(ws.sums[3:4]), sp)
+    with _Timer(timers, "field_forward", st):
+        _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
+                  _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf), _lib.ptr(ws.colors), None,
+                  None, _lib.ptr(ws.sums[3:4]), sp)
     # K3/K4: composite + Huber + compositing backward
-    _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf), _lib.ptr(ws.colors),
-              s, _lib.ptr(ws.tgt), cfg.huber_delta, float(m_total), _lib.ptr(ws.rendered),
-              _lib.ptr(ws.resid), _lib.ptr(ws.alphas), _lib.ptr(ws.weights), _lib.ptr(ws.tb),
-              _lib.ptr(ws.dl_dc), _lib.ptr(ws.dl_dsdf), _lib.ptr(ws.sums), sp)
+    with _Timer(timers, "composite", st):
+        _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf),
+                  _lib.ptr(ws.colors), s, _lib.ptr(ws.tgt), cfg.huber_delta, float(m_total),
+                  _lib.ptr(ws.rendered), _lib.ptr(ws.resid), _lib.ptr(ws.alphas),
+                  _lib.ptr(ws.weights), _lib.ptr(ws.tb), _lib.ptr(ws.dl_dc), _lib.ptr(ws.dl_dsdf),
+                  _lib.ptr(ws.sums), sp)
     lay = params.layout
     end = lay.active_end(na)
     ws.flag.zero_()
@@ -276,14 +302,17 @@ def train_step(state, dataset, time_index=0, batch=None):
         ws.count64.fill_(P_glob)
         # K5: field backward with the fused Eikonal cotangent
         sdf_g, col_g, tab_g = lay.views(ws.grads)
-        _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
-                  _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.dl_dc), _lib.ptr(ws.dl_dsdf),
-                  None, cfg.eikonal_weight, _lib.ptr(ws.count64), _lib.ptr(sdf_g[0]),
-                  _lib.ptr(col_g[0]), _lib.ptr(tab_g), sp)
+        with _Timer(timers, "field_backward", st):
+            _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(ws.pos32),
+                      _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.dl_dc),
+                      _lib.ptr(ws.dl_dsdf), None, cfg.eikonal_weight, _lib.ptr(ws.count64),
+                      _lib.ptr(sdf_g[0]), _lib.ptr(col_g[0]), _lib.ptr(tab_g), sp)
         if dp.active:
-            dp.allreduce_(ws.grads[:end])
-            dp.allreduce_(ws.sums[:4])
-        _apply_gradients(state, na, s)
+            with _Timer(timers, "allreduce", st):
+                dp.allreduce_(ws.grads[:end])
+                dp.allreduce_(ws.sums[:4])
+        with _Timer(timers, "adam", st):
+            _apply_gradients(state, na, s)
     elif dp.active:
         dp.allreduce_(ws.sums[:4])
     # one D2H: [huber sum, dslog, sq err, eik sum, flag, slog]
