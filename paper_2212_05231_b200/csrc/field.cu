@@ -777,7 +777,6 @@ field_backward_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *
         warp_rank32(gacc + G_H1, EP, H, EP, stage, 0, 64, lane);
         __syncwarp();
         // slot A <- s1 = H2[0] . m1 ; slot B <- mvec ; dH1 += S1^T MV  (Theorem 1, l = 1)
-        // pvec = (H1 mvec) . m1 -> slot C (cols 100..)?  computed below into registers
 #pragma unroll
         for (int j = 0; j < H; ++j) my[j] = mask_bit(mlo, mhi, j) ? sw[OFF_H2 + j] : 0.f;
 #pragma unroll
@@ -785,40 +784,49 @@ field_backward_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *
         __syncwarp();
         warp_rank32(gacc + G_H1, EP, H, EP, stage, 0, 64, lane);
         __syncwarp();
-        // slot A <- dl_dy (16) ; slot B <- a1 (recomputed from e) ; dH2 += DLY^T A1
-        //   plus Theorem-1 row 0: dH2[0] += pvec, folded in as an extra rank-1 term by
-        //   staging pvec with dl_dy-row [1,0,..] in the second half of the chunk below.
+        // slot A <- dl_dy (16) ; slot B <- a1 (recomputed from e_aug) ; dH2 += DLY^T A1
+        float e2[EP];
+#pragma unroll
+        for (int i = 0; i < EP; ++i) e2[i] = et[i * BWD_BLOCK];
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) my[o] = dly[o];
 #pragma unroll 2
         for (int j = 0; j < H; ++j) {
             const float *h1 = sw + OFF_H1 + j * EP;
-            float z = 0.f, zp = 0.f;
+            float z = 0.f;
 #pragma unroll
             for (int i = 0; i < EP; i += 4) {
                 const float4 w = lds4(h1 + i);
-                z = fmaf(w.x, e[i], z);
-                z = fmaf(w.y, e[i + 1], z);
-                z = fmaf(w.z, e[i + 2], z);
-                z = fmaf(w.w, e[i + 3], z);
+                z = fmaf(w.x, e2[i], z);
+                z = fmaf(w.y, e2[i + 1], z);
+                z = fmaf(w.z, e2[i + 2], z);
+                z = fmaf(w.w, e2[i + 3], z);
+            }
+            my[64 + j] = mask_bit(mlo, mhi, j) ? z : 0.f;
+        }
+        __syncwarp();
+        warp_rank32(gacc + G_H2, H, NOUT, H, stage, 0, 64, lane);
+        __syncwarp();
+        // Theorem 1, layer 2 (row 0 only): dH2[0] += pvec = (H1 mvec) . m1,
+        // staged against the one-hot row e_0
+        my[0] = 1.f;
+        my[1] = my[2] = my[3] = 0.f;
+#pragma unroll 2
+        for (int j = 0; j < H; ++j) {
+            const float *h1 = sw + OFF_H1 + j * EP;
+            float zp = 0.f;
+#pragma unroll
+            for (int i = 0; i < EP; i += 4) {
+                const float4 w = lds4(h1 + i);
                 zp = fmaf(w.x, mv[i], zp);
                 zp = fmaf(w.y, mv[i + 1], zp);
                 zp = fmaf(w.z, mv[i + 2], zp);
                 zp = fmaf(w.w, mv[i + 3], zp);
             }
-            const bool on = mask_bit(mlo, mhi, j);
-            my[64 + j] = on ? z : 0.f;  // a1
-            my[16 + j] = on ? zp : 0.f;  // pvec (slot A cols 16..79)
+            my[64 + j] = mask_bit(mlo, mhi, j) ? zp : 0.f;
         }
         __syncwarp();
-        warp_rank32(gacc + G_H2, H, NOUT, H, stage, 0, 64, lane);
-        // dH2[0][j] += sum_s pvec[s][j]
-        for (int j = lane; j < H; j += 32) {
-            float s = 0.f;
-#pragma unroll 8
-            for (int r = 0; r < 32; ++r) s += stage[r * SROW + 16 + j];
-            if (s != 0.f) atomicAdd(gacc + G_H2 + j, s);
-        }
+        warp_rank32(gacc + G_H2, H, 4, H, stage, 0, 64, lane);
         __syncwarp();
     }
     __syncthreads();
