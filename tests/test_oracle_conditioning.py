@@ -1,8 +1,14 @@
-"""Documents the conditioning of the training step that the GPU parity bars rely on:
-perturbing the oracle's own MLP weights at fp32 rounding level (1e-7 relative) moves
-its table gradients by up to ~1e-3 relL2 and ~1e-2 max-abs (ReLU-mask and alpha-clamp
-flips), so multi-step GPU-vs-oracle gradient checks use the measured sensitivity as
-their bar (tests/test_gpu_parity.py::oracle_sensitivity).  CPU only."""
+"""Documents the conditioning of the training step that the GPU parity bars rely on.
+
+The reference clamps alpha at 0 and passes zero gradient there (`renderer.py:342-352`),
+but just above the clamp dalpha/df_i = (c_j/c_i^2) s c_i (1-c_i) is O(s).  Intervals
+with raw alpha ~ 0 (SDF nearly flat along the ray) therefore switch between a zero and
+an O(s) gradient under a 1-ulp change of the SDF.  Perturbing the oracle's own MLP
+weights by 1e-7 relative moves dL/dsdf by several % relL2 and table gradients by up to
+~3e-2 relL2 / ~0.3 max-abs, while a 1e-8 perturbation (below fp32 resolution) moves
+them by ~1e-7.  Multi-step GPU-vs-oracle gradient checks therefore use the measured
+self-sensitivity as their bar (tests/test_gpu_parity.py::oracle_sensitivity); single
+field passes are held to 1e-3.  CPU only."""
 
 import numpy as np
 
@@ -29,7 +35,6 @@ def test_step_gradient_sensitivity_to_ulp_perturbation():
     otrain.train_step(b, ds, batch=batch, trace=tb)
     rels = [rel_err(tb["grads"].tables[lv], ta["grads"].tables[lv]) for lv in range(8)]
     maxs = [max_err(tb["grads"].tables[lv], ta["grads"].tables[lv]) for lv in range(8)]
-    # the effect is real (not zero) but bounded: these are the magnitudes the GPU bar
-    # scales with
-    assert max(rels) > 1e-5 and max(maxs) > 1e-4
-    assert max(rels) < 1e-2 and max(maxs) < 1e-1
+    # a 1-ulp perturbation moves the step's table gradients far beyond 1 ulp
+    assert max(rels) > 1e-4 and max(maxs) > 1e-3
+    assert max(rels) < 1e-1 and max(maxs) < 1.0
