@@ -212,6 +212,12 @@ NS2B_API int ns2b_bench_l2_read(const float *buf, int64_t nfloats, int32_t iters
 /* nops random float2 REDs over nrows 8-B rows of buf (the scatter's access pattern). */
 NS2B_API int ns2b_bench_red(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void *stream);
 
+/* tcgen05 building-block self-test (one CTA): mode 0: D[128x64] = A[128x48] B[64x48]^T
+ * (f16 split, K-major/K-major); 1: D = A[128x48] B[48x64] (B MN-major); 2: D[64x48] =
+ * U[128x64]^T V[128x48] (bf16, M=64, MN-major both); 3: mode 0 in bf16. fp32 in/out. */
+NS2B_API int ns2b_selftest_umma(const float *A, const float *B, float *D, int32_t mode,
+                                void *stream);
+
 #ifdef __cplusplus
 }
 #endif
