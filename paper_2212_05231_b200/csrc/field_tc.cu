@@ -14,8 +14,8 @@
 //     fp32 shared-memory accumulator (one global RED per element per CTA at exit).
 //
 // Cotangents span many binades (dL/dc ~ 1/m), so every cotangent tile is staged
-// scaled by an exact per-tile power of two 2^-G (G = exponent of the tile's max) and
-// the GEMM results are multiplied back by 2^G: exact, keeps fp16 in range.
+// scaled by an exact per-tile power of two (the tile max lands in [2^13, 2^14)) and
+// the GEMM results are multiplied back: exact, keeps fp16 hi/lo parts normal.
 //
 // Algorithm per tile (field.py:208-331, relu_mlp.py:94-216):
 //   P0 gather features + d feature/dx (J -> TMEM);  Z1 = E H1^T
@@ -69,6 +69,11 @@ constexpr uint32_t TM_DC2 = 0, TM_DC1 = 64, TM_DC3 = 96, TM_DH2 = 112, TM_DH1 = 
 constexpr uint32_t TM_J = 176, TM_Z1 = 272, TM_JD = 336, TM_SA = 384, TM_SB = 448;
 
 // instruction descriptors
+// Cotangent tiles are staged as v * 2^(kHead - G), G = exponent of the tile max, so the
+// largest element lands in [2^13, 2^14) (< 65504) and small elements keep normal fp16
+// hi/lo parts; results are multiplied back by 2^(G - kHead).
+constexpr int kHead = 14;
+
 constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
 constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
@@ -458,7 +463,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int i = 3; i < 16; ++i) dlog[i] = 0.f;
             G1 = tile_exponent(absmax<3>(dlog), red);
-            const float sc = pow2i(-G1);
+            const float sc = pow2i(kHead - G1);
 #pragma unroll
             for (int i = 0; i < 3; ++i) dlog[i] *= sc;
             stage<16>(S, TD, TDB, t, dlog);
@@ -477,17 +482,17 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::tmem_ld<16>(my + TM_DC3, d);
             if (lane < 16) {
                 const int j = warp * 16 + lane;
-                const float sc = pow2i(G1);
+                const float sc = pow2i(G1 - kHead);
 #pragma unroll
                 for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + j] += d[o] * sc;
             }
             float u[64];
             umma::tmem_ld<64>(my + TM_SA, u);
-            const float sc1 = pow2i(G1);
+            const float sc1 = pow2i(G1 - kHead);
 #pragma unroll
             for (int k = 0; k < 64; ++k) u[k] = mask_bit(c2lo, c2hi, k) ? u[k] * sc1 : 0.f;
             G2 = tile_exponent(absmax<64>(u), red);
-            const float sc = pow2i(-G2);
+            const float sc = pow2i(kHead - G2);
 #pragma unroll
             for (int k = 0; k < 64; ++k) u[k] *= sc;
             stage<64>(S, TY, T64B, t, u);
@@ -504,11 +509,11 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         {
             float u[64];
             umma::tmem_ld<64>(my + TM_SB, u);
-            const float sc2 = pow2i(G2);
+            const float sc2 = pow2i(G2 - kHead);
 #pragma unroll
             for (int j = 0; j < 64; ++j) u[j] = mask_bit(c1lo, c1hi, j) ? u[j] * sc2 : 0.f;
             G3 = tile_exponent(absmax<64>(u), red);
-            const float sc = pow2i(-G3);
+            const float sc = pow2i(kHead - G3);
 #pragma unroll
             for (int j = 0; j < 64; ++j) u[j] *= sc;
             stage<64>(S, TX, T64B, t, u);
@@ -526,7 +531,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         {
             float dcin[32];
             umma::tmem_ld<32>(my + TM_SA, dcin);
-            const float sc3 = pow2i(G3);
+            const float sc3 = pow2i(G3 - kHead);
             q0 = gn0 + dcin[3] * sc3;  // field.py:308-312
             q1 = gn1 + dcin[4] * sc3;
             q2 = gn2 + dcin[5] * sc3;
@@ -535,7 +540,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int o = 1; o < 16; ++o) dly[o] = dcin[9 + o] * sc3;
             G4 = tile_exponent(absmax<16>(dly), red);
-            const float sc = pow2i(-G4);
+            const float sc = pow2i(kHead - G4);
 #pragma unroll
             for (int o = 0; o < 16; ++o) dly[o] *= sc;
             stage<16>(S, TD, TDB, t, dly);
@@ -557,7 +562,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         {
             float u[64];
             umma::tmem_ld<64>(my + TM_SB, u);
-            const float sc4 = pow2i(G4);
+            const float sc4 = pow2i(G4 - kHead);
 #pragma unroll
             for (int j = 0; j < 64; ++j) u[j] = mask_bit(mlo, mhi, j) ? u[j] * sc4 : 0.f;
             float J[96];
@@ -572,7 +577,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int i = 35; i < 48; ++i) mv[i] = 0.f;
             G56 = tile_exponent(fmaxf(absmax<64>(u), absmax<48>(mv)), red);
-            const float sc = pow2i(-G56);
+            const float sc = pow2i(kHead - G56);
 #pragma unroll
             for (int j = 0; j < 64; ++j) u[j] *= sc;
 #pragma unroll
@@ -598,7 +603,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         float de[48], jd[48];
         {
             umma::tmem_ld<48>(my + TM_SA, de);
-            const float sc56 = pow2i(G56);
+            const float sc56 = pow2i(G56 - kHead);
 #pragma unroll
             for (int i = 0; i < 48; ++i) de[i] *= sc56;
             float pv[64];
@@ -606,7 +611,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int j = 0; j < 64; ++j) pv[j] = mask_bit(mlo, mhi, j) ? pv[j] * sc56 : 0.f;
             G7 = tile_exponent(absmax<64>(pv), red);
-            const float sc = pow2i(-G7);
+            const float sc = pow2i(kHead - G7);
 #pragma unroll
             for (int j = 0; j < 64; ++j) pv[j] *= sc;
             stage<64>(S, TX, T64B, t, pv);
@@ -662,13 +667,13 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             float d[64];
             umma::tmem_ld<64>(my + TM_DC2, d);
             if (lane < 16) {
-                const float sc = pow2i(G2);
+                const float sc = pow2i(G2 - kHead);
 #pragma unroll
                 for (int c = 0; c < 64; ++c) gacc[G_C2r + j * H + c] += d[c] * sc;
             }
             umma::tmem_ld<32>(my + TM_DC1, d);
             if (lane < 16) {
-                const float sc = pow2i(G3);
+                const float sc = pow2i(G3 - kHead);
 #pragma unroll
                 for (int c = 0; c < CIN; ++c) gacc[G_C1r + j * CIN + c] += d[c] * sc;
             }
@@ -676,14 +681,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             float dp[16];
             umma::tmem_ld<16>(my + TM_DC3, dp);
             if (lane < 16) {
-                const float sc = pow2i(G4);
+                const float sc = pow2i(G4 - kHead);
 #pragma unroll
                 for (int o = 0; o < 16; ++o) gacc[G_H2r + o * H + j] += d[o] * sc;
-                gacc[G_H2r + j] += dp[0] * pow2i(G7);
+                gacc[G_H2r + j] += dp[0] * pow2i(G7 - kHead);
             }
             umma::tmem_ld<48>(my + TM_DH1, d);
             if (lane < 16) {
-                const float sc = pow2i(G56);
+                const float sc = pow2i(G56 - kHead);
 #pragma unroll
                 for (int c = 0; c < EP; ++c) {
                     const int dst = c < E ? c : (c == EC ? E : -1);
