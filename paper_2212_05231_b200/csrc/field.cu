@@ -585,14 +585,20 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
                       const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
                       float *grad_color, float *grad_tables, cudaStream_t st);
 
-// NS2B_FIELD_IMPL=simt selects the round-1 SIMT kernels (A/B comparison); default tcgen05.
-static bool use_simt() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("NS2B_FIELD_IMPL");
-        v = (e && strcmp(e, "simt") == 0) ? 1 : 0;
+// NS2B_FIELD_IMPL=simt selects the round-1 SIMT kernels for both passes (A/B
+// comparison; default tcgen05); NS2B_FIELD_FWD / NS2B_FIELD_BWD override per pass.
+static bool env_is_simt(const char *name) {
+    const char *e = getenv(name);
+    return e && strcmp(e, "simt") == 0;
+}
+static bool use_simt(bool bwd) {
+    static int v[2] = {-1, -1};
+    if (v[bwd] < 0) {
+        const char *specific = bwd ? "NS2B_FIELD_BWD" : "NS2B_FIELD_FWD";
+        const char *e = getenv(specific);
+        v[bwd] = e ? (strcmp(e, "simt") == 0) : env_is_simt("NS2B_FIELD_IMPL");
     }
-    return v == 1;
+    return v[bwd] == 1;
 }
 }  // namespace ns2b
 
@@ -604,7 +610,7 @@ int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int3
                        const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
                        float *colors, float *normals, float *geo, double *eik_sum,
                        void *stream) {
-    if (!use_simt())
+    if (!use_simt(false))
         return field_forward_tc(field, pos32, ray_ids, dirs, count, capacity, sdf, colors, normals, geo, eik_sum,
                                 as_stream(stream));
     FieldDev f;
@@ -650,7 +656,7 @@ int ns2b_field_backward(const ns2b_field_t *field, const float *pos32, const int
                         const float *dl_dc, const float *dl_dsdf, const float *dl_dn_extra,
                         double eik_weight, const int64_t *eik_count, float *grad_sdf,
                         float *grad_color, float *grad_tables, void *stream) {
-    if (!use_simt())
+    if (!use_simt(true))
         return field_backward_tc(field, pos32, ray_ids, dirs, count, capacity, dl_dc, dl_dsdf, dl_dn_extra,
                                  eik_weight, eik_count, grad_sdf, grad_color, grad_tables, as_stream(stream));
     FieldDev f;

@@ -5,20 +5,24 @@
 // masks, normals, sigmoid, losses, scatter) is plain per-thread code on the rows that
 // tcgen05.ld returns.  Every dense contraction is a UMMA issued by thread 0:
 //
-//   chain GEMMs (M = 128 samples):  operand tiles [sample][feature] (K-major A) x the
-//     weights (K-major for W^T, MN-major view of the same tile for W), fp16 with the
-//     three-term hi/lo split (A_hi B_hi + A_lo B_hi + A_hi B_lo, fp32 accumulation
-//     in TMEM) -> fp32-level accuracy.
-//   weight-gradient GEMMs (M = 64 weight rows, K = the 128 samples): MN-major views
-//     of the same per-sample tiles; accumulated per tile in TMEM and folded into an
-//     fp32 shared-memory accumulator (one global RED per element per CTA at exit).
+//   chain GEMMs (M = 128 samples): operand tiles [sample][feature] (K-major A) x the
+//     weights (K-major view for W^T, MN-major view of the same tile for W);
+//   weight-gradient GEMMs (M = 64 weight rows, K = the 128 samples of the tile):
+//     MN-major views of the same per-sample tiles; each finished per-tile accumulator
+//     is folded into an fp32 shared-memory sum (one global RED per element per CTA).
 //
-// Cotangents span many binades (dL/dc ~ 1/m), so every cotangent tile is staged
-// scaled by an exact per-tile power of two (the tile max lands in [2^13, 2^14)) and
-// the GEMM results are multiplied back: exact, keeps fp16 hi/lo parts normal.
+// Precision: every operand is fp16 with the three-term hi/lo split (A_hi B_hi +
+// A_lo B_hi + A_hi B_lo, fp32 accumulation in TMEM).  The split is fp32-accurate only
+// while the lo parts stay normal, so every staged tile (per tile) and every weight
+// matrix (per CTA) is scaled by an exact power of two putting its max in
+// [2^13, 2^14); GEMM results are multiplied back by 2^-(eA+eB).  This also keeps the
+// cotangents (dL/dc ~ 1/m) in range.
+//
+// Encoding column order inside the tiles: [features 0..31 | x y z | 1 | 0 x 12] (48),
+// so a level's feature pair is 4-byte aligned; H1 / dH1 are permuted accordingly.
 //
 // Algorithm per tile (field.py:208-331, relu_mlp.py:94-216):
-//   P0 gather features + d feature/dx (J -> TMEM);  Z1 = E H1^T
+//   P0 gather features + dfeature/dx (J -> TMEM);  Z1 = E H1^T
 //   P1 a1 = relu(Z1), s1 = H2[0].m1;  Y = A1 H2^T,  JD = S1 H1          (j_d)
 //   P2 n = j_d J; cin = [x,n,v,y];  Zc1 = CIN C1^T
 //   P3 Zc2 = A1c C2^T;  P4 LOG = A2c C3^T;  P5 c = sigmoid  (forward ends here)
@@ -26,9 +30,8 @@
 //   P6 u2 -> U1 = U2 C2,         dC2 += U2^T A1c
 //   P7 u1 -> DCIN = U1 C1,       dC1 += U1^T CIN
 //   P8 q, dly -> U = DLY H2,     dH2 += A1^T DLY
-//   P9 u, mvec=[q,Jq,0] -> DE = U H1, PV = MV H1^T,  dH1 += U^T E + S1^T MV  (Thm 1)
+//   P9 u, mvec=[Jq,q] -> DE = U H1, PV = MV H1^T,  dH1 += U^T E + S1^T MV  (Thm 1)
 //   P10 dH2[0] += sum pv (PV^T ONES);  fused first+second-order table scatter (Eq. 9)
-//   P11 fold the per-tile weight gradients into shared fp32
 #include "field_common.cuh"
 #include "umma.cuh"
 
@@ -36,9 +39,10 @@ namespace ns2b {
 namespace tc {
 
 constexpr int TILE = 128;
+constexpr int kHead = 14;  // staged maxima land in [2^13, 2^14)
 
 // shared memory map (bytes); every tile is hi part then lo part
-constexpr uint32_t WH1 = 0;                          // 64 x 48 f16
+constexpr uint32_t WH1 = 0;                          // 64 x 48
 constexpr uint32_t WH1B = 64 * 48 * 2;
 constexpr uint32_t WH2 = WH1 + 2 * WH1B;              // 16 x 64
 constexpr uint32_t WH2B = 16 * 64 * 2;
@@ -60,19 +64,20 @@ constexpr uint32_t TD = TC + 2 * TCB;                 // 128 x 16
 constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
 constexpr uint32_t GACC = TEND;                       // fp32 gradient accumulator (bwd)
-constexpr int GACC_FLOATS = 9216;                     // 64*36 + 16*64 + 64*25 + 64*64 + 3*64
+constexpr int GACC_FLOATS = 9216;
 constexpr uint32_t SMEM_FWD = TEND;
 constexpr uint32_t SMEM_BWD = GACC + GACC_FLOATS * 4;
 
 // TMEM columns (512 allocated)
-constexpr uint32_t TM_DC2 = 0, TM_DC1 = 64, TM_DC3 = 96, TM_DH2 = 112, TM_DH1 = 128;
-constexpr uint32_t TM_J = 176, TM_Z1 = 272, TM_JD = 336, TM_SA = 384, TM_SB = 448;
-
-// instruction descriptors
-// Cotangent tiles are staged as v * 2^(kHead - G), G = exponent of the tile max, so the
-// largest element lands in [2^13, 2^14) (< 65504) and small elements keep normal fp16
-// hi/lo parts; results are multiplied back by 2^(G - kHead).
-constexpr int kHead = 14;
+constexpr uint32_t TM_DC2 = 0;    // 64: dC2 acc; later mvec scratch (32) and dH1b acc (48)
+constexpr uint32_t TM_DC1 = 64;   // 32
+constexpr uint32_t TM_DC3 = 96;   // 16: dC3^T acc; later dPV acc
+constexpr uint32_t TM_DH2 = 112;  // 16
+constexpr uint32_t TM_DH1 = 128;  // 48: dH1a acc
+constexpr uint32_t TM_J = 176;    // 16 levels x 8: [dfeat/dx (6) | j_d feature pair (2)]
+constexpr uint32_t TM_Z1 = 304;   // 64
+constexpr uint32_t TM_SA = 368;   // 64 chain slot A (P0: raw feature scratch)
+constexpr uint32_t TM_SB = 432;   // 64 chain slot B
 
 constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
@@ -81,6 +86,14 @@ constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
 __device__ __forceinline__ float pow2i(int e) {
     e = e < -120 ? -120 : (e > 120 ? 120 : e);
     return __int_as_float((127 + e) << 23);
+}
+
+// tile column -> column of the real H1 (64, E+1) layout, -1 for padding
+__device__ __forceinline__ int h1_col(int c, int E) {
+    if (c < 32) return (3 + c < E) ? 3 + c : -1;
+    if (c < 35) return c - 32;
+    if (c == 35) return E;
+    return -1;
 }
 
 struct Smem {
@@ -94,90 +107,96 @@ struct Smem {
     }
 };
 
+// stage row r of a tile with values v * 2^e
 template <int C>
-__device__ __forceinline__ void stage(const Smem &s, uint32_t off, uint32_t part, int r, const float *v) {
-    umma::stage_row<0, C>(s.p(off), s.p(off + part), r, v);
+__device__ __forceinline__ void stage(const Smem &s, uint32_t off, uint32_t part, int r, const float *v, int e) {
+    const float sc = pow2i(e);
+    float w[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) w[i] = v[i] * sc;
+    umma::stage_row<0, C>(s.p(off), s.p(off + part), r, w);
 }
 
-// weights -> fp16 hi/lo tiles in the padded 36-wide encoding layout (see field.cu)
-__device__ void load_weight_tiles(const Smem &s, const FieldDev &f) {
-    const int E = 3 + 2 * f.L;
-    for (int r = threadIdx.x; r < 64 + 16 + 64 + 64 + 16; r += blockDim.x) {
-        float row[64];
-        if (r < 64) {
-            for (int c = 0; c < 48; ++c) {
-                int src = c < E ? c : (c == EC ? E : -1);
-                row[c] = (c < EP && src >= 0) ? f.sdf_w[r * (E + 1) + src] : 0.f;
-            }
-            stage<48>(s, WH1, WH1B, r, row);
-        } else if (r < 80) {
-            const int o = r - 64;
-            for (int c = 0; c < 64; ++c) row[c] = f.sdf_w[H * (E + 1) + o * H + c];
-            stage<64>(s, WH2, WH2B, o, row);
-        } else if (r < 144) {
-            const int j = r - 80;
-            for (int c = 0; c < 32; ++c) row[c] = c < CIN ? f.color_w[j * CIN + c] : 0.f;
-            stage<32>(s, WC1, WC1B, j, row);
-        } else if (r < 208) {
-            const int k = r - 144;
-            for (int c = 0; c < 64; ++c) row[c] = f.color_w[H * CIN + k * H + c];
-            stage<64>(s, WC2, WC2B, k, row);
-        } else {
-            const int o = r - 208;
-            for (int c = 0; c < 64; ++c) row[c] = o < 3 ? f.color_w[H * CIN + H * H + o * H + c] : 0.f;
-            stage<64>(s, WC3, WC3B, o, row);
+__device__ __forceinline__ int exp_for(float m) {
+    if (!(m > 0.f) || !(m < INFINITY)) return 0;
+    int G;
+    frexpf(m, &G);
+    return kHead - G;
+}
+
+// block-wide max of up to two values -> their staging exponents (one barrier)
+struct Reducer {
+    uint32_t (*red)[2][4];
+    int parity;
+    __device__ void two(float a, float b, int &ea, int &eb) {
+        const int warp = threadIdx.x >> 5;
+        const uint32_t ra = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(a)));
+        const uint32_t rb = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(b)));
+        if ((threadIdx.x & 31) == 0) {
+            red[parity][0][warp] = ra;
+            red[parity][1][warp] = rb;
         }
+        __syncthreads();
+        uint32_t ma = 0, mb = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            ma = max(ma, red[parity][0][w]);
+            mb = max(mb, red[parity][1][w]);
+        }
+        parity ^= 1;
+        ea = exp_for(__uint_as_float(ma));
+        eb = exp_for(__uint_as_float(mb));
     }
+    __device__ int one(float a) {
+        int ea, eb;
+        two(a, 0.f, ea, eb);
+        return ea;
+    }
+};
+
+template <int N>
+__device__ __forceinline__ float absmax(const float *v) {
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) m = fmaxf(m, fabsf(v[i]));
+    return m;
 }
 
-// gather (features into e, jacobian rows into J[96])
-__device__ __forceinline__ void gather_regs(const FieldDev &f, float x0, float x1, float x2, float (&e)[EP],
-                                            float (&J)[96]) {
-    const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
-    const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
-    const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
-#pragma unroll
-    for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
-        float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
-        if (l < f.n_active) {
-            const LevelInfo lv = f.lv[l];
-            int cx, cy, cz;
-            float fx, fy, fz;
-            cell_frac(u0, lv.n, cx, fx);
-            cell_frac(u1, lv.n, cy, fy);
-            cell_frac(u2, lv.n, cz, fz);
-            const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
-            float2 v[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
-            const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-                const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                const float w = wx * wy * wz;
-                const float dwx = (ox ? sx : -sx) * (wy * wz);
-                const float dwy = (oy ? sy : -sy) * (wx * wz);
-                const float dwz = (oz ? sz : -sz) * (wx * wy);
-                f0 = fmaf(w, v[c].x, f0);
-                f1 = fmaf(w, v[c].y, f1);
-                j00 = fmaf(dwx, v[c].x, j00);
-                j01 = fmaf(dwy, v[c].x, j01);
-                j02 = fmaf(dwz, v[c].x, j02);
-                j10 = fmaf(dwx, v[c].y, j10);
-                j11 = fmaf(dwy, v[c].y, j11);
-                j12 = fmaf(dwz, v[c].y, j12);
-            }
+// weights -> fp16 hi/lo tiles, each matrix scaled by its own power of two
+__device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wmax, int *wexp) {
+    const int E = 3 + 2 * f.L;
+    auto fetch = [&](int r, int c) -> float {  // row r of the stacked [H1|H2|C1|C2|C3] tiles
+        if (r < 64) {
+            const int rc = h1_col(c, E);
+            return (c < 48 && rc >= 0) ? f.sdf_w[r * (E + 1) + rc] : 0.f;
         }
-        e[3 + 2 * l] = f0;
-        e[4 + 2 * l] = f1;
-        J[6 * l + 0] = j00;
-        J[6 * l + 1] = j01;
-        J[6 * l + 2] = j02;
-        J[6 * l + 3] = j10;
-        J[6 * l + 4] = j11;
-        J[6 * l + 5] = j12;
+        if (r < 80) return f.sdf_w[H * (E + 1) + (r - 64) * H + c];
+        if (r < 144) return c < CIN ? f.color_w[(r - 80) * CIN + c] : 0.f;
+        if (r < 208) return f.color_w[H * CIN + (r - 144) * H + c];
+        return (r - 208) < 3 ? f.color_w[H * CIN + H * H + (r - 208) * H + c] : 0.f;
+    };
+    auto mat = [](int r) { return r < 64 ? 0 : r < 80 ? 1 : r < 144 ? 2 : r < 208 ? 3 : 4; };
+    const int cols[5] = {48, 64, 32, 64, 64};
+    if (threadIdx.x < 5) wmax[threadIdx.x] = 0u;
+    __syncthreads();
+    for (int r = threadIdx.x; r < 224; r += blockDim.x) {
+        float m = 0.f;
+        for (int c = 0; c < cols[mat(r)]; ++c) m = fmaxf(m, fabsf(fetch(r, c)));
+        atomicMax(&wmax[mat(r)], __float_as_uint(m));
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) wexp[threadIdx.x] = exp_for(__uint_as_float(wmax[threadIdx.x]));
+    __syncthreads();
+    for (int r = threadIdx.x; r < 224; r += blockDim.x) {
+        float row[64];
+        const int k = mat(r);
+        for (int c = 0; c < 64; ++c) row[c] = c < cols[k] ? fetch(r, c) : 0.f;
+        const int e = wexp[k];
+        if (k == 0) stage<48>(s, WH1, WH1B, r, row, e);
+        else if (k == 1) stage<64>(s, WH2, WH2B, r - 64, row, e);
+        else if (k == 2) stage<32>(s, WC1, WC1B, r - 80, row, e);
+        else if (k == 3) stage<64>(s, WC2, WC2B, r - 144, row, e);
+        else stage<64>(s, WC3, WC3B, r - 208, row, e);
     }
 }
 
@@ -187,7 +206,6 @@ __device__ __forceinline__ void block_sync_tc() {
     umma::fence_after_sync();
 }
 
-// make this thread's staged smem visible to the tensor core and rendezvous
 __device__ __forceinline__ void publish() {
     umma::fence_async_smem();
     block_sync_tc();
@@ -199,27 +217,11 @@ __device__ __forceinline__ void wait_mma(uint64_t *mbar, uint32_t &phase) {
     umma::fence_after_sync();
 }
 
-// exponent G of the tile-wide max |v| (max in [2^(G-1), 2^G)); all threads call it
-__device__ __forceinline__ int tile_exponent(float rowmax, uint32_t *red) {
-    uint32_t b = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(rowmax)));
-    const int warp = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) red[warp] = b;
-    __syncthreads();
-    uint32_t m = max(max(red[0], red[1]), max(red[2], red[3]));
-    __syncthreads();
-    float mv = __uint_as_float(m);
-    int e = 0;
-    if (mv > 0.f && mv < INFINITY) frexpf(mv, &e);
-    return e;
-}
-
-template <int N>
-__device__ __forceinline__ float absmax(const float *v) {
-    float m = 0.f;
-#pragma unroll
-    for (int i = 0; i < N; ++i) m = fmaxf(m, fabsf(v[i]));
-    return m;
-}
+struct LevelSm {
+    LevelInfo lv;
+    float sx, sy, sz;
+    float pad;
+};
 
 template <bool kBwd>
 __global__ void __launch_bounds__(TILE, 1)
@@ -233,14 +235,25 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_s;
-    __shared__ uint32_t red[4];
+    __shared__ uint32_t red[2][2][4];
+    __shared__ uint32_t wmax[5];
+    __shared__ int wexp_s[5];
     __shared__ float h2row0[H];
+    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int E = 3 + 2 * f.L;
+    const int NA = f.n_active;
 
-    load_weight_tiles(S, f);
+    if (t < NS2B_MAX_LEVELS) {
+        lvs[t].lv = f.lv[t];
+        lvs[t].sx = f.sx[t];
+        lvs[t].sy = f.sy[t];
+        lvs[t].sz = f.sz[t];
+    }
     if (t < H) h2row0[t] = f.sdf_w[H * (E + 1) + t];
+    load_weight_tiles(S, f, wmax, wexp_s);
+    const int eH1 = wexp_s[0], eH2 = wexp_s[1], eC1 = wexp_s[2], eC2 = wexp_s[3], eC3 = wexp_s[4];
     float *gacc = reinterpret_cast<float *>(S.p(GACC));
     if (kBwd)
         for (int i = t; i < GACC_FLOATS; i += TILE) gacc[i] = 0.f;
@@ -251,13 +264,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     if (warp == 0) umma::tmem_alloc(&tmem_base_s, 512);
     publish();
     const uint32_t tb = tmem_base_s;
-    const uint32_t my = tb + (static_cast<uint32_t>(warp * 32) << 16);  // this warp's lane quadrant
+    const uint32_t my = tb + (static_cast<uint32_t>(warp * 32) << 16);
     uint32_t phase = 0;
+    Reducer R{red, 0};
     const int P = *count;
     const float Pf = (kBwd && eik_count) ? static_cast<float>(*eik_count) : 1.f;
-    // gradient layout offsets inside gacc (= the flat parameter layout's MLP prefix)
     const int G_H1r = 0, G_H2r = H * (E + 1), G_C1r = G_H2r + NOUT * H, G_C2r = G_C1r + H * CIN,
               G_C3r = G_C2r + H * H;
+    const int jrow = warp * 16 + lane;  // weight row held by lanes 0..15 in M=64 accumulators
     float eik = 0.f;
 
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
@@ -274,21 +288,77 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             v1 = static_cast<float>(dirs[3 * r + 1]);
             v2 = static_cast<float>(dirs[3 * r + 2]);
         }
-        // ------------------------------------------------ P0: gather, Z1
+        const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+        const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+        const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+        // ------------------------------------------------ P0: gather (4 levels / batch), Z1
+        int eE;
         {
-            float e[EP], J[96];
-            gather_regs(f, x0, x1, x2, e, J);
-            e[0] = x0;
-            e[1] = x1;
-            e[2] = x2;
-            e[EC] = 1.f;
-            float row[48];
+            float fmax_ = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), 1.f));
+#pragma unroll 1
+            for (int g = 0; g < NS2B_MAX_LEVELS; g += 4) {
+                if (g >= NA) break;
+                float2 v[4][8];
+                float fr[4][3];
 #pragma unroll
-            for (int i = 0; i < 48; ++i) row[i] = i < EP ? e[i] : 0.f;
-            stage<48>(S, TE, TEB, t, row);
+                for (int i = 0; i < 4; ++i) {
+                    const int l = g + i;
+                    if (l < NA) {
+                        const LevelInfo lv = lvs[l].lv;
+                        int cx, cy, cz;
+                        cell_frac(un0, lv.n, cx, fr[i][0]);
+                        cell_frac(un1, lv.n, cy, fr[i][1]);
+                        cell_frac(un2, lv.n, cz, fr[i][2]);
+                        const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
 #pragma unroll
-            for (int c = 0; c < 96; c += 16) umma::tmem_st16(my + TM_J + c, J + c);
+                        for (int c = 0; c < 8; ++c)
+                            v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int l = g + i;
+                    if (l < NA) {
+                        const float fx = fr[i][0], fy = fr[i][1], fz = fr[i][2];
+                        const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
+                        float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                            const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                            const float w = wx * wy * wz;
+                            const float dwx = (ox ? sx : -sx) * (wy * wz);
+                            const float dwy = (oy ? sy : -sy) * (wx * wz);
+                            const float dwz = (oz ? sz : -sz) * (wx * wy);
+                            f0 = fmaf(w, v[i][c].x, f0);
+                            f1 = fmaf(w, v[i][c].y, f1);
+                            j00 = fmaf(dwx, v[i][c].x, j00);
+                            j01 = fmaf(dwy, v[i][c].x, j01);
+                            j02 = fmaf(dwz, v[i][c].x, j02);
+                            j10 = fmaf(dwx, v[i][c].y, j10);
+                            j11 = fmaf(dwy, v[i][c].y, j11);
+                            j12 = fmaf(dwz, v[i][c].y, j12);
+                        }
+                        fmax_ = fmaxf(fmax_, fmaxf(fabsf(f0), fabsf(f1)));
+                        umma::tmem_st2(my + TM_SA + 2 * l, f0, f1);
+                        umma::tmem_st4(my + TM_J + 8 * l, j00, j01, j02, j10);
+                        umma::tmem_st2(my + TM_J + 8 * l + 4, j11, j12);
+                    }
+                }
+            }
             umma::tmem_st_wait();
+            eE = R.one(fmax_);
+            float row[48];
+            umma::tmem_ld<32>(my + TM_SA, row);
+#pragma unroll
+            for (int a = 0; a < 32; ++a) row[a] = (a < 2 * NA) ? row[a] : 0.f;
+            row[32] = x0;
+            row[33] = x1;
+            row[34] = x2;
+            row[35] = 1.f;
+#pragma unroll
+            for (int i = 36; i < 48; ++i) row[i] = 0.f;
+            stage<48>(S, TE, TEB, t, row, eE);
         }
         publish();
         if (t == 0) {
@@ -298,10 +368,12 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         wait_mma(&mbar, phase);
         // ------------------------------------------------ P1: a1, s1 -> Y, JD
         uint32_t mlo = 0u, mhi = 0u;
+        int eA1, eS1;
         {
             float z[64];
             umma::tmem_ld<64>(my + TM_Z1, z);
-            float a[64], s1[64];
+            const float sc = pow2i(-(eE + eH1));
+            float s1[64], ma = 0.f, ms = 0.f;
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
                 const bool on = z[j] > 0.f;
@@ -309,38 +381,51 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     if (j < 32) mlo |= 1u << j;
                     else mhi |= 1u << (j - 32);
                 }
-                a[j] = on ? z[j] : 0.f;
+                z[j] = on ? z[j] * sc : 0.f;
                 s1[j] = on ? h2row0[j] : 0.f;
+                ma = fmaxf(ma, z[j]);
+                ms = fmaxf(ms, fabsf(s1[j]));
             }
-            stage<64>(S, TX, T64B, t, a);
-            stage<64>(S, TY, T64B, t, s1);
+            R.two(ma, ms, eA1, eS1);
+            stage<64>(S, TX, T64B, t, z, eA1);
+            stage<64>(S, TY, T64B, t, s1, eS1);
         }
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), 4, ID_KK(16), false);
-            umma::gemm3(tb + TM_JD, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
+            umma::gemm3(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
         // ------------------------------------------------ P2: normal, cin -> Zc1
         float y[16], n0, n1, n2;
         float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
+        int eCin;
         {
             umma::tmem_ld<16>(my + TM_SB, y);
-            float jd[48], J[96];
-            umma::tmem_ld<48>(my + TM_JD, jd);
-            umma::tmem_ld<96>(my + TM_J, J);
-            n0 = jd[0];
-            n1 = jd[1];
-            n2 = jd[2];
+            const float scy = pow2i(-(eA1 + eH2));
 #pragma unroll
-            for (int a = 0; a < 2 * NS2B_MAX_LEVELS; ++a) {
-                if (a < 2 * f.n_active) {
-                    n0 = fmaf(jd[3 + a], J[3 * a], n0);
-                    n1 = fmaf(jd[3 + a], J[3 * a + 1], n1);
-                    n2 = fmaf(jd[3 + a], J[3 * a + 2], n2);
-                }
+            for (int o = 0; o < 16; ++o) y[o] *= scy;
+            const float scd = pow2i(-(eS1 + eH1));
+            float jx[4];
+            umma::tmem_ld4(my + TM_SA + 32, jx);  // j_d for x, y, z (tile cols 32..34)
+            n0 = jx[0] * scd;
+            n1 = jx[1] * scd;
+            n2 = jx[2] * scd;
+#pragma unroll 1
+            for (int l = 0; l < NA; ++l) {
+                float d0, d1;
+                umma::tmem_ld2(my + TM_SA + 2 * l, d0, d1);
+                d0 *= scd;
+                d1 *= scd;
+                umma::tmem_st2(my + TM_J + 8 * l + 6, d0, d1);  // keep j_d pair for the scatter
+                float jl[8];
+                umma::tmem_ld8(my + TM_J + 8 * l, jl);
+                n0 = fmaf(d0, jl[0], fmaf(d1, jl[3], n0));
+                n1 = fmaf(d0, jl[1], fmaf(d1, jl[4], n1));
+                n2 = fmaf(d0, jl[2], fmaf(d1, jl[5], n2));
             }
+            umma::tmem_st_wait();
             const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
             if (valid) eik += (nn - 1.f) * (nn - 1.f);
             if (kBwd && valid) {
@@ -370,7 +455,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             for (int o = 0; o < 16; ++o) cin[9 + o] = y[o];
 #pragma unroll
             for (int i = 25; i < 32; ++i) cin[i] = 0.f;
-            stage<32>(S, TC, TCB, t, cin);
+            eCin = R.one(absmax<25>(cin));
+            stage<32>(S, TC, TCB, t, cin, eCin);
         }
         publish();
         if (t == 0) {
@@ -380,9 +466,12 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         wait_mma(&mbar, phase);
         // ------------------------------------------------ P3: a1c -> Zc2
         uint32_t c1lo = 0u, c1hi = 0u, c2lo = 0u, c2hi = 0u;
+        int eA1c, eA2c;
         {
             float z[64];
             umma::tmem_ld<64>(my + TM_SA, z);
+            const float sc = pow2i(-(eCin + eC1));
+            float m = 0.f;
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
                 const bool on = z[j] > 0.f;
@@ -390,9 +479,11 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     if (j < 32) c1lo |= 1u << j;
                     else c1hi |= 1u << (j - 32);
                 }
-                z[j] = on ? z[j] : 0.f;
+                z[j] = on ? z[j] * sc : 0.f;
+                m = fmaxf(m, z[j]);
             }
-            stage<64>(S, TZ, T64B, t, z);
+            eA1c = R.one(m);
+            stage<64>(S, TZ, T64B, t, z, eA1c);
         }
         publish();
         if (t == 0) {
@@ -404,6 +495,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         {
             float z[64];
             umma::tmem_ld<64>(my + TM_SB, z);
+            const float sc = pow2i(-(eA1c + eC2));
+            float m = 0.f;
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
                 const bool on = z[j] > 0.f;
@@ -411,9 +504,11 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     if (j < 32) c2lo |= 1u << j;
                     else c2hi |= 1u << (j - 32);
                 }
-                z[j] = on ? z[j] : 0.f;
+                z[j] = on ? z[j] * sc : 0.f;
+                m = fmaxf(m, z[j]);
             }
-            stage<64>(S, TX, T64B, t, z);
+            eA2c = R.one(m);
+            stage<64>(S, TX, T64B, t, z, eA2c);
         }
         publish();
         if (t == 0) {
@@ -424,11 +519,12 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         // ------------------------------------------------ P5: colours (+ backward start)
         float cc0, cc1, cc2;
         {
-            float lg[16];
-            umma::tmem_ld<16>(my + TM_SA, lg);
-            cc0 = sigmoid_f(lg[0]);
-            cc1 = sigmoid_f(lg[1]);
-            cc2 = sigmoid_f(lg[2]);
+            float lg[4];
+            umma::tmem_ld4(my + TM_SA, lg);
+            const float sc = pow2i(-(eA2c + eC3));
+            cc0 = sigmoid_f(lg[0] * sc);
+            cc1 = sigmoid_f(lg[1] * sc);
+            cc2 = sigmoid_f(lg[2] * sc);
         }
         if (!kBwd) {
             if (valid) {
@@ -454,7 +550,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             gc2 = dl_dc[3 * p + 2];
             gd = dl_dsdf[p];
         }
-        int G1;
+        int eD;
         {
             float dlog[16];
             dlog[0] = gc0 * cc0 * (1.f - cc0);  // field.py:304
@@ -462,11 +558,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             dlog[2] = gc2 * cc2 * (1.f - cc2);
 #pragma unroll
             for (int i = 3; i < 16; ++i) dlog[i] = 0.f;
-            G1 = tile_exponent(absmax<3>(dlog), red);
-            const float sc = pow2i(kHead - G1);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) dlog[i] *= sc;
-            stage<16>(S, TD, TDB, t, dlog);
+            eD = R.one(absmax<3>(dlog));
+            stage<16>(S, TD, TDB, t, dlog, eD);
         }
         publish();
         if (t == 0) {
@@ -475,27 +568,27 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P6: u2 -> U1, dC2 (+ flush dC3)
-        int G2;
+        // ------------------------------------------------ P6: dC3 fold; u2 -> U1, dC2
+        int eU2;
         {
             float d[16];
             umma::tmem_ld<16>(my + TM_DC3, d);
             if (lane < 16) {
-                const int j = warp * 16 + lane;
-                const float sc = pow2i(G1 - kHead);
+                const float sc = pow2i(-(eA2c + eD));
 #pragma unroll
-                for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + j] += d[o] * sc;
+                for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sc;
             }
             float u[64];
             umma::tmem_ld<64>(my + TM_SA, u);
-            const float sc1 = pow2i(G1 - kHead);
+            const float sc = pow2i(-(eD + eC3));
+            float m = 0.f;
 #pragma unroll
-            for (int k = 0; k < 64; ++k) u[k] = mask_bit(c2lo, c2hi, k) ? u[k] * sc1 : 0.f;
-            G2 = tile_exponent(absmax<64>(u), red);
-            const float sc = pow2i(kHead - G2);
-#pragma unroll
-            for (int k = 0; k < 64; ++k) u[k] *= sc;
-            stage<64>(S, TY, T64B, t, u);
+            for (int k = 0; k < 64; ++k) {
+                u[k] = mask_bit(c2lo, c2hi, k) ? u[k] * sc : 0.f;
+                m = fmaxf(m, fabsf(u[k]));
+            }
+            eU2 = R.one(m);
+            stage<64>(S, TY, T64B, t, u, eU2);
         }
         publish();
         if (t == 0) {
@@ -504,19 +597,27 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P7: u1 -> DCIN, dC1
-        int G3;
+        // ------------------------------------------------ P7: dC2 fold; u1 -> DCIN, dC1
+        int eU1;
         {
+            float d[64];
+            umma::tmem_ld<64>(my + TM_DC2, d);
+            if (lane < 16) {
+                const float sc = pow2i(-(eU2 + eA1c));
+#pragma unroll
+                for (int c = 0; c < 64; ++c) gacc[G_C2r + jrow * H + c] += d[c] * sc;
+            }
             float u[64];
             umma::tmem_ld<64>(my + TM_SB, u);
-            const float sc2 = pow2i(G2 - kHead);
+            const float sc = pow2i(-(eU2 + eC2));
+            float m = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) u[j] = mask_bit(c1lo, c1hi, j) ? u[j] * sc2 : 0.f;
-            G3 = tile_exponent(absmax<64>(u), red);
-            const float sc = pow2i(kHead - G3);
-#pragma unroll
-            for (int j = 0; j < 64; ++j) u[j] *= sc;
-            stage<64>(S, TX, T64B, t, u);
+            for (int j = 0; j < 64; ++j) {
+                u[j] = mask_bit(c1lo, c1hi, j) ? u[j] * sc : 0.f;
+                m = fmaxf(m, fabsf(u[j]));
+            }
+            eU1 = R.one(m);
+            stage<64>(S, TX, T64B, t, u, eU1);
         }
         publish();
         if (t == 0) {
@@ -525,13 +626,20 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P8: q, dly -> U, dH2
+        // ------------------------------------------------ P8: dC1 fold; q, dly -> U, dH2
         float q0, q1, q2;
-        int G4;
+        int eDLY;
         {
+            float d[32];
+            umma::tmem_ld<32>(my + TM_DC1, d);
+            if (lane < 16) {
+                const float sc = pow2i(-(eU1 + eCin));
+#pragma unroll
+                for (int c = 0; c < CIN; ++c) gacc[G_C1r + jrow * CIN + c] += d[c] * sc;
+            }
             float dcin[32];
             umma::tmem_ld<32>(my + TM_SA, dcin);
-            const float sc3 = pow2i(G3 - kHead);
+            const float sc3 = pow2i(-(eU1 + eC1));
             q0 = gn0 + dcin[3] * sc3;  // field.py:308-312
             q1 = gn1 + dcin[4] * sc3;
             q2 = gn2 + dcin[5] * sc3;
@@ -539,16 +647,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             dly[0] = gd + dcin[9] * sc3;
 #pragma unroll
             for (int o = 1; o < 16; ++o) dly[o] = dcin[9 + o] * sc3;
-            G4 = tile_exponent(absmax<16>(dly), red);
-            const float sc = pow2i(kHead - G4);
-#pragma unroll
-            for (int o = 0; o < 16; ++o) dly[o] *= sc;
-            stage<16>(S, TD, TDB, t, dly);
+            eDLY = R.one(absmax<16>(dly));
+            stage<16>(S, TD, TDB, t, dly, eDLY);
             float z[64];
             umma::tmem_ld<64>(my + TM_Z1, z);
+            const float sz = pow2i(-(eE + eH1));
 #pragma unroll
-            for (int j = 0; j < 64; ++j) z[j] = z[j] > 0.f ? z[j] : 0.f;
-            stage<64>(S, TY, T64B, t, z);
+            for (int j = 0; j < 64; ++j) z[j] = z[j] > 0.f ? z[j] * sz : 0.f;
+            stage<64>(S, TY, T64B, t, z, eA1);
         }
         publish();
         if (t == 0) {
@@ -557,93 +663,118 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P9: u, mvec -> DE, PV, dH1
-        int G56;
+        // ------------------------------------------------ P9: dH2 fold; u, mvec -> DE, PV, dH1
+        int eU, eMV;
         {
+            float d[16];
+            umma::tmem_ld<16>(my + TM_DH2, d);
+            if (lane < 16) {
+                const float sc = pow2i(-(eA1 + eDLY));
+#pragma unroll
+                for (int o = 0; o < 16; ++o) gacc[G_H2r + o * H + jrow] += d[o] * sc;
+            }
             float u[64];
             umma::tmem_ld<64>(my + TM_SB, u);
-            const float sc4 = pow2i(G4 - kHead);
+            const float sc4 = pow2i(-(eDLY + eH2));
+            float mu = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) u[j] = mask_bit(mlo, mhi, j) ? u[j] * sc4 : 0.f;
-            float J[96];
-            umma::tmem_ld<96>(my + TM_J, J);
+            for (int j = 0; j < 64; ++j) {
+                u[j] = mask_bit(mlo, mhi, j) ? u[j] * sc4 : 0.f;
+                mu = fmaxf(mu, fabsf(u[j]));
+            }
+            // mvec feature rows J q (field.py:326-327) -> scratch TM_DC2[0..32)
+            float mm = fmaxf(fmaxf(fabsf(q0), fabsf(q1)), fabsf(q2));
+#pragma unroll 1
+            for (int l = 0; l < NA; ++l) {
+                float jl[8];
+                umma::tmem_ld8(my + TM_J + 8 * l, jl);
+                const float a0 = jl[0] * q0 + jl[1] * q1 + jl[2] * q2;
+                const float a1 = jl[3] * q0 + jl[4] * q1 + jl[5] * q2;
+                mm = fmaxf(mm, fmaxf(fabsf(a0), fabsf(a1)));
+                umma::tmem_st2(my + TM_DC2 + 2 * l, a0, a1);
+            }
+            umma::tmem_st_wait();
+            R.two(mu, mm, eU, eMV);
+            stage<64>(S, TX, T64B, t, u, eU);
             float mv[48];
-            mv[0] = q0;
-            mv[1] = q1;
-            mv[2] = q2;
+            umma::tmem_ld<32>(my + TM_DC2, mv);
 #pragma unroll
-            for (int a = 0; a < 32; ++a)
-                mv[3 + a] = (a < 2 * f.n_active) ? (J[3 * a] * q0 + J[3 * a + 1] * q1 + J[3 * a + 2] * q2) : 0.f;
+            for (int a = 0; a < 32; ++a) mv[a] = (a < 2 * NA) ? mv[a] : 0.f;
+            mv[32] = q0;
+            mv[33] = q1;
+            mv[34] = q2;
 #pragma unroll
             for (int i = 35; i < 48; ++i) mv[i] = 0.f;
-            G56 = tile_exponent(fmaxf(absmax<64>(u), absmax<48>(mv)), red);
-            const float sc = pow2i(kHead - G56);
-#pragma unroll
-            for (int j = 0; j < 64; ++j) u[j] *= sc;
-#pragma unroll
-            for (int i = 0; i < 48; ++i) mv[i] *= sc;
-            stage<64>(S, TX, T64B, t, u);
-            stage<48>(S, TZ, T64B, t, mv);
+            stage<48>(S, TZ, T64B, t, mv, eMV);
             float s1[64];
 #pragma unroll
             for (int j = 0; j < 64; ++j) s1[j] = mask_bit(mlo, mhi, j) ? h2row0[j] : 0.f;
-            stage<64>(S, TY, T64B, t, s1);
+            stage<64>(S, TY, T64B, t, s1, eS1);
         }
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
             umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
             umma::gemm3(tb + TM_DH1, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), 8, ID_WG(48), false);
-            umma::gemm3(tb + TM_DH1, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), true);
+            umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P10: pvec, scatter
-        int G7;
-        float de[48], jd[48];
+        // ------------------------------------------------ P10: dH1 fold; pvec, scatter
+        int ePV;
         {
-            umma::tmem_ld<48>(my + TM_SA, de);
-            const float sc56 = pow2i(G56 - kHead);
+            float da[48], db[48];
+            umma::tmem_ld<48>(my + TM_DH1, da);
+            umma::tmem_ld<48>(my + TM_DC2, db);
+            if (lane < 16) {
+                const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
 #pragma unroll
-            for (int i = 0; i < 48; ++i) de[i] *= sc56;
+                for (int c = 0; c < 36; ++c) {
+                    const int rc = h1_col(c, E);
+                    if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[c] * sa + db[c] * sb;
+                }
+            }
             float pv[64];
             umma::tmem_ld<64>(my + TM_SB, pv);
+            const float sc = pow2i(-(eMV + eH1));
+            float m = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) pv[j] = mask_bit(mlo, mhi, j) ? pv[j] * sc56 : 0.f;
-            G7 = tile_exponent(absmax<64>(pv), red);
-            const float sc = pow2i(kHead - G7);
-#pragma unroll
-            for (int j = 0; j < 64; ++j) pv[j] *= sc;
-            stage<64>(S, TX, T64B, t, pv);
+            for (int j = 0; j < 64; ++j) {
+                pv[j] = mask_bit(mlo, mhi, j) ? pv[j] * sc : 0.f;
+                m = fmaxf(m, fabsf(pv[j]));
+            }
+            ePV = R.one(m);
+            stage<64>(S, TX, T64B, t, pv, ePV);
             float ones[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) ones[i] = i == 0 ? 1.f : 0.f;
-            stage<16>(S, TD, TDB, t, ones);
-            umma::tmem_ld<48>(my + TM_JD, jd);
+            stage<16>(S, TD, TDB, t, ones, 0);
         }
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbar);
         }
-        // fused first + second order table scatter while the last MMA runs (Eq. 9):
-        // grad += w * dL/dfeat + j_d[feat] * (q . dw)   (one float2 RED per corner)
-        if (valid) {
-            const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
-            const float uu1 = normalize_coord(x1, f.lo[1], f.ext[1]);
-            const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
-#pragma unroll
-            for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
-                if (l < f.n_active) {
-                    const LevelInfo lv = f.lv[l];
+        // fused first + second order table scatter while that MMA runs (Eq. 9):
+        //   grad += w * dL/dfeat + j_d[feat] * (q . dw)  -- one float2 RED per corner
+        {
+            const float sde = pow2i(-(eU + eH1));
+#pragma unroll 1
+            for (int l = 0; l < NA; ++l) {
+                float de0, de1, jl[8];
+                umma::tmem_ld2(my + TM_SA + 2 * l, de0, de1);
+                umma::tmem_ld8(my + TM_J + 8 * l, jl);
+                if (valid) {
+                    de0 *= sde;
+                    de1 *= sde;
+                    const float jd0 = jl[6], jd1 = jl[7];
+                    const LevelInfo lv = lvs[l].lv;
+                    const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
                     int cx, cy, cz;
                     float fx, fy, fz;
-                    cell_frac(u0, lv.n, cx, fx);
-                    cell_frac(uu1, lv.n, cy, fy);
-                    cell_frac(u2, lv.n, cz, fz);
-                    const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
-                    const float de0 = de[3 + 2 * l], de1 = de[4 + 2 * l];
-                    const float jd0 = jd[3 + 2 * l], jd1 = jd[4 + 2 * l];
+                    cell_frac(un0, lv.n, cx, fx);
+                    cell_frac(un1, lv.n, cy, fy);
+                    cell_frac(un2, lv.n, cz, fz);
                     float *gt = g_tab + l * f.T * 2;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
@@ -661,40 +792,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P11: fold weight gradients
-        {
-            const int j = warp * 16 + lane;  // weight row held by lanes 0..15 (M=64 layout)
-            float d[64];
-            umma::tmem_ld<64>(my + TM_DC2, d);
-            if (lane < 16) {
-                const float sc = pow2i(G2 - kHead);
-#pragma unroll
-                for (int c = 0; c < 64; ++c) gacc[G_C2r + j * H + c] += d[c] * sc;
-            }
-            umma::tmem_ld<32>(my + TM_DC1, d);
-            if (lane < 16) {
-                const float sc = pow2i(G3 - kHead);
-#pragma unroll
-                for (int c = 0; c < CIN; ++c) gacc[G_C1r + j * CIN + c] += d[c] * sc;
-            }
-            umma::tmem_ld<16>(my + TM_DH2, d);
-            float dp[16];
-            umma::tmem_ld<16>(my + TM_DC3, dp);
-            if (lane < 16) {
-                const float sc = pow2i(G4 - kHead);
-#pragma unroll
-                for (int o = 0; o < 16; ++o) gacc[G_H2r + o * H + j] += d[o] * sc;
-                gacc[G_H2r + j] += dp[0] * pow2i(G7 - kHead);
-            }
-            umma::tmem_ld<48>(my + TM_DH1, d);
-            if (lane < 16) {
-                const float sc = pow2i(G56 - kHead);
-#pragma unroll
-                for (int c = 0; c < EP; ++c) {
-                    const int dst = c < E ? c : (c == EC ? E : -1);
-                    if (dst >= 0) gacc[G_H1r + j * (E + 1) + dst] += d[c] * sc;
-                }
-            }
+        {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
+            float d[16];
+            umma::tmem_ld<16>(my + TM_DC3, d);
+            if (lane < 16) gacc[G_H2r + jrow] += d[0] * pow2i(-ePV);
         }
     }
     if (eik_sum) {
@@ -707,11 +808,9 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         const int nsdf = H * (E + 1) + NOUT * H;
         for (int i = t; i < GACC_FLOATS; i += TILE) {
             const float v = gacc[i];
-            if (i < nsdf) {
-                if (v != 0.f) atomicAdd(g_sdf + i, v);
-            } else if (i < G_C3r + 3 * H) {
-                if (v != 0.f) atomicAdd(g_color + (i - nsdf), v);
-            }
+            if (v == 0.f) continue;
+            if (i < nsdf) atomicAdd(g_sdf + i, v);
+            else if (i < G_C3r + 3 * H) atomicAdd(g_color + (i - nsdf), v);
         }
     }
     if (warp == 0) umma::tmem_dealloc(tb, 512);
