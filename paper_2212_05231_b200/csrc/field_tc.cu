@@ -369,6 +369,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         // ------------------------------------------------ P1: a1, s1 -> Y, JD
         uint32_t mlo = 0u, mhi = 0u;
         int eA1, eS1;
+        float d_sdf = 0.f;  // SDF value: exact-fp32 dot product (see below)
         {
             float z[64];
             umma::tmem_ld<64>(my + TM_Z1, z);
@@ -385,6 +386,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 s1[j] = on ? h2row0[j] : 0.f;
                 ma = fmaxf(ma, z[j]);
                 ms = fmaxf(ms, fabsf(s1[j]));
+                // d = H2[0] a1 is a cancelling sum (~|x| - r at init) and alpha takes
+                // differences of sigmoid(s d) along a ray, so it is computed with fp32
+                // FMAs instead of the tensor core, whose fp32 accumulator truncates.
+                d_sdf = fmaf(h2row0[j], z[j], d_sdf);
             }
             R.two(ma, ms, eA1, eS1);
             stage<64>(S, TX, T64B, t, z, eA1);
@@ -406,6 +411,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             const float scy = pow2i(-(eA1 + eH2));
 #pragma unroll
             for (int o = 0; o < 16; ++o) y[o] *= scy;
+            y[0] = d_sdf;
             const float scd = pow2i(-(eS1 + eH1));
             float jx[4];
             umma::tmem_ld4(my + TM_SA + 32, jx);  // j_d for x, y, z (tile cols 32..34)

@@ -39,3 +39,21 @@ for i in range(2):
     print(f"  sdf{i}: err {rel_err(np_(sdf_g[i]), og.sdf_layers[i]):.2e}  sens {sens[f'sdf{i}'][0]:.2e}")
 for i in range(3):
     print(f"  color{i}: err {rel_err(np_(col_g[i]), og.color_layers[i]):.2e}  sens {sens[f'color{i}'][0]:.2e}")
+
+# ---- intermediates of the same step
+ws = pst.ws
+P = rp.sample_count
+rec = tr["records"]
+def cmp(name, a, r):
+    a = np.asarray(a, np.float64).reshape(r.shape); r = np.asarray(r, np.float64)
+    d = np.abs(a - r)
+    print(f"  {name}: relL2 {rel_err(a, r):.2e} maxabs {d.max():.2e} argmax {np.unravel_index(d.argmax(), d.shape)} n>1e-3rel {(d > 1e-3*np.abs(r).max()).sum()}")
+cmp("sdf", np_(ws.sdf[:P]), rec.sdf)
+cmp("colors", np_(ws.colors[:P]), rec.sample_colors)
+cmp("dl_dsdf", np_(ws.dl_dsdf[:P]), tr["dl_dsdf"])
+cmp("dl_dc", np_(ws.dl_dc[:P]), tr["dl_dc"])
+ii = rec.interval_first
+a_p = np_(ws.alphas[:P])[ii]
+print("  alpha clamp-at-0 count (prod/oracle):", int((a_p == 0).sum()), int((rec.alphas == 0).sum()),
+      " mismatched zero-status:", int(((a_p == 0) != (rec.alphas == 0)).sum()))
+cmp("alphas", a_p, rec.alphas)
