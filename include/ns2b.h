@@ -134,8 +134,13 @@ NS2B_API int ns2b_march_fill(const double *origins, const double *dirs, int64_t 
  * sum_p (||n_p|| - 1)^2 (trainer.py:227-229); may be NULL.  count is a device int32. */
 NS2B_API int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
                        const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
-                       float *colors, float *normals, float *geo, double *eik_sum,
+                       float *colors, float *normals, float *geo, double *eik_sum, void *workspace,
                        void *stream);
+
+/* Device workspace (bytes) the field kernels need for `capacity` samples: the gather
+ * pass's pre-staged encoding tiles and d feature/dx, and the backward's scatter inputs.
+ * ns2b_field_backward must get the workspace its matching ns2b_field_forward filled. */
+NS2B_API int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes);
 
 /* Lean SDF-only query (renderer.py:131-142) on fp32 positions; d (P). */
 NS2B_API int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,
@@ -182,7 +187,7 @@ NS2B_API int ns2b_field_backward(const ns2b_field_t *field, const float *pos32, 
                         const double *dirs, const int32_t *count, int64_t capacity,
                         const float *dl_dc, const float *dl_dsdf, const float *dl_dn_extra,
                         double eik_weight, const int64_t *eik_count, float *grad_sdf,
-                        float *grad_color, float *grad_tables, void *stream);
+                        float *grad_color, float *grad_tables, void *workspace, void *stream);
 
 /* Finite check over flat fp32 segments: flag |= 1<<seg for non-finite gradients
  * (trainer.py:158-159).  seg_off/seg_len are HOST arrays of nseg entries. */

@@ -62,14 +62,15 @@ _SIGS = {
     "ns2b_scan_offsets": (ctypes.c_int, [P, I64, P, P, ctypes.POINTER(SZ), P]),
     "ns2b_march_fill": (ctypes.c_int, [P, P, I64, ctypes.POINTER(OccT), P, P, P, P, P, P]),
     "ns2b_field_forward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
-                                          P]),
+                                          P, P]),
+    "ns2b_field_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),
     "ns2b_field_sdf": (ctypes.c_int, [ctypes.POINTER(FieldT), P, I64, P, P]),
     "ns2b_occupancy_update": (ctypes.c_int, [ctypes.POINTER(FieldT), ctypes.POINTER(OccT), F64,
                                              F64, P, P, P]),
     "ns2b_composite": (ctypes.c_int, [P, I64, P, P, F64, P, F64, F64, P, P, P, P, P, P, P, P, P]),
     "ns2b_composite_backward": (ctypes.c_int, [P, I64, P, P, F64, P, P, P, P, P, P, P, P]),
     "ns2b_field_backward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, F64,
-                                           P, P, P, P, P]),
+                                           P, P, P, P, P, P]),
     "ns2b_check_finite": (ctypes.c_int, [P, P, P, I32, P, P]),
     "ns2b_adam_multi": (ctypes.c_int, [P, P, P, P, P, P, P, P, I32, F64, F64, F64, P, P]),
     "ns2b_adam_scalar_f64": (ctypes.c_int, [P, P, F64, P, P, I64, F64, F64, F64, F64, P, P, I32,
@@ -135,6 +136,15 @@ def ptr(t):
 def stream_ptr(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def field_workspace(capacity, device, cache=None):
+    """Device workspace tensor for `capacity` samples (reused from `cache` if large enough)."""
+    n = ctypes.c_size_t(0)
+    call("ns2b_field_workspace_bytes", int(max(capacity, 1)), ctypes.byref(n))
+    if cache is not None and cache.numel() >= n.value:
+        return cache
+    return torch.empty(int(n.value), dtype=torch.uint8, device=device)
 
 
 def launch_count() -> int:

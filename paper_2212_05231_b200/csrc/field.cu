@@ -577,13 +577,14 @@ static int ensure_attrs() {
 }  // namespace ns2b
 
 namespace ns2b {
+int field_workspace_bytes(int64_t capacity, size_t *bytes);
 int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                      const int32_t *count, int64_t capacity, float *sdf, float *colors, float *normals, float *geo,
-                     double *eik_sum, cudaStream_t st);
+                     double *eik_sum, void *workspace, cudaStream_t st);
 int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                       const int32_t *count, int64_t capacity, const float *dl_dc, const float *dl_dsdf,
                       const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
-                      float *grad_color, float *grad_tables, cudaStream_t st);
+                      float *grad_color, float *grad_tables, void *workspace, cudaStream_t st);
 
 // NS2B_FIELD_IMPL=simt selects the round-1 SIMT kernels for both passes (A/B
 // comparison; default tcgen05); NS2B_FIELD_FWD / NS2B_FIELD_BWD override per pass.
@@ -608,11 +609,11 @@ extern "C" {
 
 int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
                        const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
-                       float *colors, float *normals, float *geo, double *eik_sum,
+                       float *colors, float *normals, float *geo, double *eik_sum, void *workspace,
                        void *stream) {
     if (!use_simt(false))
         return field_forward_tc(field, pos32, ray_ids, dirs, count, capacity, sdf, colors, normals, geo, eik_sum,
-                                as_stream(stream));
+                                workspace, as_stream(stream));
     FieldDev f;
     int rc = make_field_dev(field, f);
     if (rc) return rc;
@@ -622,6 +623,10 @@ int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int3
     field_forward_kernel<<<blocks, FWD_BLOCK, FWD_SMEM, as_stream(stream)>>>(
         f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum);
     return check_launch("field_forward");
+}
+
+int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes) {
+    return field_workspace_bytes(capacity, bytes);
 }
 
 int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,
@@ -655,10 +660,11 @@ int ns2b_field_backward(const ns2b_field_t *field, const float *pos32, const int
                         const double *dirs, const int32_t *count, int64_t capacity,
                         const float *dl_dc, const float *dl_dsdf, const float *dl_dn_extra,
                         double eik_weight, const int64_t *eik_count, float *grad_sdf,
-                        float *grad_color, float *grad_tables, void *stream) {
+                        float *grad_color, float *grad_tables, void *workspace, void *stream) {
     if (!use_simt(true))
         return field_backward_tc(field, pos32, ray_ids, dirs, count, capacity, dl_dc, dl_dsdf, dl_dn_extra,
-                                 eik_weight, eik_count, grad_sdf, grad_color, grad_tables, as_stream(stream));
+                                 eik_weight, eik_count, grad_sdf, grad_color, grad_tables, workspace,
+                                 as_stream(stream));
     FieldDev f;
     int rc = make_field_dev(field, f);
     if (rc) return rc;

@@ -223,6 +223,33 @@ struct LevelSm {
     float pad;
 };
 
+// Per-tile workspace written by the gather kernel and the backward MLP kernel
+// (see ns2b_field_workspace_bytes): pre-staged E tiles (fp16 hi | lo, tile layout),
+// their staging exponent, d feature/dx value-major [tile][96][128] fp32, and the
+// scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d feature rows (32) | q (3).
+constexpr int JROWS = 96, SBROWS = 68;
+struct Workspace {
+    uint8_t *e_tiles;
+    int *e_exp;
+    float *jac;
+    float *sb;
+};
+__host__ __device__ inline size_t ws_tile_bytes() {
+    return 2 * static_cast<size_t>(TEB) + sizeof(int) + (JROWS + SBROWS) * TILE * sizeof(float);
+}
+__host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
+    uint8_t *b = static_cast<uint8_t *>(base);
+    Workspace w;
+    w.e_tiles = b;
+    b += ntiles * 2 * static_cast<size_t>(TEB);
+    w.jac = reinterpret_cast<float *>(b);
+    b += ntiles * JROWS * TILE * sizeof(float);
+    w.sb = reinterpret_cast<float *>(b);
+    b += ntiles * SBROWS * TILE * sizeof(float);
+    w.e_exp = reinterpret_cast<int *>(b);
+    return w;
+}
+
 template <bool kBwd>
 __global__ void __launch_bounds__(TILE, 1)
 field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
@@ -231,7 +258,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 float *__restrict__ geo_out, double *__restrict__ eik_sum,
                 const float *__restrict__ dl_dc, const float *__restrict__ dl_dsdf,
                 const float *__restrict__ dl_dn_extra, float eik_w, const int64_t *__restrict__ eik_count,
-                float *__restrict__ g_sdf, float *__restrict__ g_color, float *__restrict__ g_tab) {
+                float *__restrict__ g_sdf, float *__restrict__ g_color, Workspace ws) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_s;
@@ -288,77 +315,26 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             v1 = static_cast<float>(dirs[3 * r + 1]);
             v2 = static_cast<float>(dirs[3 * r + 2]);
         }
-        const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
-        const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
-        const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
-        // ------------------------------------------------ P0: gather (4 levels / batch), Z1
+        // ------------------------------------------------ P0: pre-staged E tile, J, Z1
+        const int64_t tile = base / TILE;
+        const float *Jt = ws.jac + tile * JROWS * TILE;
+        float *SBt = ws.sb + tile * SBROWS * TILE;
         int eE;
         {
-            float fmax_ = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), 1.f));
+            const uint4 *src = reinterpret_cast<const uint4 *>(ws.e_tiles + tile * 2 * TEB);
+            uint4 *dst = reinterpret_cast<uint4 *>(S.p(TE));
+#pragma unroll 4
+            for (int i = t; i < static_cast<int>(2 * TEB / 16); i += TILE) dst[i] = src[i];
+            eE = ws.e_exp[tile];
+            if (kBwd) {
 #pragma unroll 1
-            for (int g = 0; g < NS2B_MAX_LEVELS; g += 4) {
-                if (g >= NA) break;
-                float2 v[4][8];
-                float fr[4][3];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int l = g + i;
-                    if (l < NA) {
-                        const LevelInfo lv = lvs[l].lv;
-                        int cx, cy, cz;
-                        cell_frac(un0, lv.n, cx, fr[i][0]);
-                        cell_frac(un1, lv.n, cy, fr[i][1]);
-                        cell_frac(un2, lv.n, cz, fr[i][2]);
-                        const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
-#pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
-                    }
+                for (int l = 0; l < NA; ++l) {
+                    const float *jr = Jt + 6 * l * TILE + t;
+                    umma::tmem_st4(my + TM_J + 8 * l, jr[0], jr[TILE], jr[2 * TILE], jr[3 * TILE]);
+                    umma::tmem_st2(my + TM_J + 8 * l + 4, jr[4 * TILE], jr[5 * TILE]);
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int l = g + i;
-                    if (l < NA) {
-                        const float fx = fr[i][0], fy = fr[i][1], fz = fr[i][2];
-                        const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
-                        float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-                            const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                            const float w = wx * wy * wz;
-                            const float dwx = (ox ? sx : -sx) * (wy * wz);
-                            const float dwy = (oy ? sy : -sy) * (wx * wz);
-                            const float dwz = (oz ? sz : -sz) * (wx * wy);
-                            f0 = fmaf(w, v[i][c].x, f0);
-                            f1 = fmaf(w, v[i][c].y, f1);
-                            j00 = fmaf(dwx, v[i][c].x, j00);
-                            j01 = fmaf(dwy, v[i][c].x, j01);
-                            j02 = fmaf(dwz, v[i][c].x, j02);
-                            j10 = fmaf(dwx, v[i][c].y, j10);
-                            j11 = fmaf(dwy, v[i][c].y, j11);
-                            j12 = fmaf(dwz, v[i][c].y, j12);
-                        }
-                        fmax_ = fmaxf(fmax_, fmaxf(fabsf(f0), fabsf(f1)));
-                        umma::tmem_st2(my + TM_SA + 2 * l, f0, f1);
-                        umma::tmem_st4(my + TM_J + 8 * l, j00, j01, j02, j10);
-                        umma::tmem_st2(my + TM_J + 8 * l + 4, j11, j12);
-                    }
-                }
+                umma::tmem_st_wait();
             }
-            umma::tmem_st_wait();
-            eE = R.one(fmax_);
-            float row[48];
-            umma::tmem_ld<32>(my + TM_SA, row);
-#pragma unroll
-            for (int a = 0; a < 32; ++a) row[a] = (a < 2 * NA) ? row[a] : 0.f;
-            row[32] = x0;
-            row[33] = x1;
-            row[34] = x2;
-            row[35] = 1.f;
-#pragma unroll
-            for (int i = 36; i < 48; ++i) row[i] = 0.f;
-            stage<48>(S, TE, TEB, t, row, eE);
         }
         publish();
         if (t == 0) {
@@ -424,14 +400,18 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 umma::tmem_ld2(my + TM_SA + 2 * l, d0, d1);
                 d0 *= scd;
                 d1 *= scd;
-                umma::tmem_st2(my + TM_J + 8 * l + 6, d0, d1);  // keep j_d pair for the scatter
-                float jl[8];
-                umma::tmem_ld8(my + TM_J + 8 * l, jl);
+                const float *jr = Jt + 6 * l * TILE + t;
+                float jl[6];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) jl[k] = jr[k * TILE];
+                if (kBwd) {  // j_d feature pair for the scatter kernel
+                    SBt[(32 + 2 * l) * TILE + t] = d0;
+                    SBt[(33 + 2 * l) * TILE + t] = d1;
+                }
                 n0 = fmaf(d0, jl[0], fmaf(d1, jl[3], n0));
                 n1 = fmaf(d0, jl[1], fmaf(d1, jl[4], n1));
                 n2 = fmaf(d0, jl[2], fmaf(d1, jl[5], n2));
             }
-            umma::tmem_st_wait();
             const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
             if (valid) eik += (nn - 1.f) * (nn - 1.f);
             if (kBwd && valid) {
@@ -761,41 +741,19 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbar);
         }
-        // fused first + second order table scatter while that MMA runs (Eq. 9):
-        //   grad += w * dL/dfeat + j_d[feat] * (q . dw)  -- one float2 RED per corner
+        // inputs of the table scatter (Eq. 9), consumed by field_scatter_kernel
         {
             const float sde = pow2i(-(eU + eH1));
 #pragma unroll 1
             for (int l = 0; l < NA; ++l) {
-                float de0, de1, jl[8];
+                float de0, de1;
                 umma::tmem_ld2(my + TM_SA + 2 * l, de0, de1);
-                umma::tmem_ld8(my + TM_J + 8 * l, jl);
-                if (valid) {
-                    de0 *= sde;
-                    de1 *= sde;
-                    const float jd0 = jl[6], jd1 = jl[7];
-                    const LevelInfo lv = lvs[l].lv;
-                    const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
-                    int cx, cy, cz;
-                    float fx, fy, fz;
-                    cell_frac(un0, lv.n, cx, fx);
-                    cell_frac(un1, lv.n, cy, fy);
-                    cell_frac(un2, lv.n, cz, fz);
-                    float *gt = g_tab + l * f.T * 2;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-                        const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                        const float w = wx * wy * wz;
-                        const float dwx = (ox ? sx : -sx) * (wy * wz);
-                        const float dwy = (oy ? sy : -sy) * (wx * wz);
-                        const float dwz = (oz ? sz : -sz) * (wx * wy);
-                        const float qd = dwx * q0 + dwy * q1 + dwz * q2;
-                        const uint32_t row = corner_row(lv, cx + ox, cy + oy, cz + oz);
-                        red_add_f32x2(gt + 2 * row, fmaf(w, de0, jd0 * qd), fmaf(w, de1, jd1 * qd));
-                    }
-                }
+                SBt[(2 * l) * TILE + t] = de0 * sde;
+                SBt[(2 * l + 1) * TILE + t] = de1 * sde;
             }
+            SBt[64 * TILE + t] = q0;
+            SBt[65 * TILE + t] = q1;
+            SBt[66 * TILE + t] = q2;
         }
         wait_mma(&mbar, phase);
         {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
@@ -822,6 +780,209 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     if (warp == 0) umma::tmem_dealloc(tb, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Gather kernel (one pass per step): per 128-sample tile, trilinear features and
+// d feature/dx for the active levels (_kernels.py:67-119 without corner records),
+// 4 levels (32 float2 loads) in flight per thread.  Features are staged straight into
+// the fp16 hi/lo E-tile layout the MLP kernels DMA into shared memory.
+constexpr int GATHER_BLOCK = TILE;
+
+__global__ void __launch_bounds__(GATHER_BLOCK)
+field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count, Workspace ws) {
+    __shared__ float raw[32][TILE + 1];
+    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
+    __shared__ uint32_t red[2][2][4];
+    const int t = threadIdx.x;
+    if (t < NS2B_MAX_LEVELS) {
+        lvs[t].lv = f.lv[t];
+        lvs[t].sx = f.sx[t];
+        lvs[t].sy = f.sy[t];
+        lvs[t].sz = f.sz[t];
+    }
+    __syncthreads();
+    Reducer R{red, 0};
+    const int NA = f.n_active;
+    const int P = *count;
+    const int64_t ntiles = (static_cast<int64_t>(P) + TILE - 1) / TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p = tile * TILE + t;
+        const bool valid = p < P;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+        if (valid) {
+            x0 = pos[3 * p];
+            x1 = pos[3 * p + 1];
+            x2 = pos[3 * p + 2];
+        }
+        const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+        const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+        const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+        float *Jt = ws.jac + tile * JROWS * TILE;
+        float fmax_ = fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), 1.f));
+#pragma unroll 1
+        for (int g = 0; g < NS2B_MAX_LEVELS; g += 4) {
+            if (g >= NA) break;
+            float2 v[4][8];
+            float fr[4][3];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < NA) {
+                    const LevelInfo lv = lvs[l].lv;
+                    int cx, cy, cz;
+                    cell_frac(un0, lv.n, cx, fr[i][0]);
+                    cell_frac(un1, lv.n, cy, fr[i][1]);
+                    cell_frac(un2, lv.n, cz, fr[i][2]);
+                    const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < NA) {
+                    const float fx = fr[i][0], fy = fr[i][1], fz = fr[i][2];
+                    const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
+                    float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                        const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                        const float w = wx * wy * wz;
+                        const float dwx = (ox ? sx : -sx) * (wy * wz);
+                        const float dwy = (oy ? sy : -sy) * (wx * wz);
+                        const float dwz = (oz ? sz : -sz) * (wx * wy);
+                        f0 = fmaf(w, v[i][c].x, f0);
+                        f1 = fmaf(w, v[i][c].y, f1);
+                        j00 = fmaf(dwx, v[i][c].x, j00);
+                        j01 = fmaf(dwy, v[i][c].x, j01);
+                        j02 = fmaf(dwz, v[i][c].x, j02);
+                        j10 = fmaf(dwx, v[i][c].y, j10);
+                        j11 = fmaf(dwy, v[i][c].y, j11);
+                        j12 = fmaf(dwz, v[i][c].y, j12);
+                    }
+                    fmax_ = fmaxf(fmax_, fmaxf(fabsf(f0), fabsf(f1)));
+                    raw[2 * l][t] = f0;
+                    raw[2 * l + 1][t] = f1;
+                    float *jr = Jt + 6 * l * TILE + t;
+                    jr[0] = j00;
+                    jr[TILE] = j01;
+                    jr[2 * TILE] = j02;
+                    jr[3 * TILE] = j10;
+                    jr[4 * TILE] = j11;
+                    jr[5 * TILE] = j12;
+                }
+            }
+        }
+        const int eE = R.one(fmax_);
+        float row[48];
+#pragma unroll
+        for (int a = 0; a < 32; ++a) row[a] = (a < 2 * NA) ? raw[a][t] : 0.f;
+        row[32] = x0;
+        row[33] = x1;
+        row[34] = x2;
+        row[35] = 1.f;
+#pragma unroll
+        for (int i = 36; i < 48; ++i) row[i] = 0.f;
+        const float sc = pow2i(eE);
+#pragma unroll
+        for (int i = 0; i < 48; ++i) row[i] *= sc;
+        uint8_t *et = ws.e_tiles + tile * 2 * TEB;
+        umma::stage_row<0, 48>(et, et + TEB, t, row);
+        if (t == 0) ws.e_exp[tile] = eE;
+        __syncthreads();  // raw[] reuse
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Table-gradient scatter (Eq. 9 + first order, field.py:317-324): block = one tile at
+// one level, thread = sample, 8 float2 REDs:  grad += w dL/dfeat + j_d (q . dw).
+// Consecutive lanes are consecutive samples of a ray; on the coarse levels they often
+// hit the same corner row, so runs of equal rows are pre-summed with a segmented
+// shuffle reduction and only the run's last lane issues the RED.
+constexpr int kAggLevels = 9;
+
+__device__ __forceinline__ void seg_red(float *gt, uint32_t row, float a, float b, int lane) {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
+    const uint32_t next = __shfl_down_sync(0xffffffffu, row, 1);
+    const bool head = lane == 0 || prev != row;
+    const bool tail = lane == 31 || next != row;
+    const uint32_t heads = __ballot_sync(0xffffffffu, head);
+    const int seg_start = 31 - __clz(heads & ((2u << lane) - 1u));  // last head at or before lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan
+        const float pa = __shfl_up_sync(0xffffffffu, a, o);
+        const float pb = __shfl_up_sync(0xffffffffu, b, o);
+        if (lane - o >= seg_start) {
+            a += pa;
+            b += pb;
+        }
+    }
+    if (tail) red_add_f32x2(gt + 2 * row, a, b);
+}
+
+__global__ void __launch_bounds__(TILE)
+field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count,
+                     const Workspace ws, float *__restrict__ g_tab) {
+    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
+    const int t = threadIdx.x, lane = t & 31;
+    if (t < NS2B_MAX_LEVELS) {
+        lvs[t].lv = f.lv[t];
+        lvs[t].sx = f.sx[t];
+        lvs[t].sy = f.sy[t];
+        lvs[t].sz = f.sz[t];
+    }
+    __syncthreads();
+    const int NA = f.n_active;
+    const int P = *count;
+    const int64_t ntiles = (static_cast<int64_t>(P) + TILE - 1) / TILE;
+    for (int64_t item = blockIdx.x; item < ntiles * NA; item += gridDim.x) {
+        const int64_t tile = item / NA;
+        const int l = static_cast<int>(item - tile * NA);
+        const int64_t p = tile * TILE + t;
+        const bool valid = p < P;
+        const float *SBt = ws.sb + tile * SBROWS * TILE + t;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, de0 = 0.f, de1 = 0.f, jd0 = 0.f, jd1 = 0.f, q0 = 0.f, q1 = 0.f, q2 = 0.f;
+        if (valid) {
+            x0 = pos[3 * p];
+            x1 = pos[3 * p + 1];
+            x2 = pos[3 * p + 2];
+            de0 = SBt[(2 * l) * TILE];
+            de1 = SBt[(2 * l + 1) * TILE];
+            jd0 = SBt[(32 + 2 * l) * TILE];
+            jd1 = SBt[(33 + 2 * l) * TILE];
+            q0 = SBt[64 * TILE];
+            q1 = SBt[65 * TILE];
+            q2 = SBt[66 * TILE];
+        }
+        const LevelInfo lv = lvs[l].lv;
+        const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
+        int cx, cy, cz;
+        float fx, fy, fz;
+        cell_frac(normalize_coord(x0, f.lo[0], f.ext[0]), lv.n, cx, fx);
+        cell_frac(normalize_coord(x1, f.lo[1], f.ext[1]), lv.n, cy, fy);
+        cell_frac(normalize_coord(x2, f.lo[2], f.ext[2]), lv.n, cz, fz);
+        float *gt = g_tab + l * f.T * 2;
+        const bool agg = l < kAggLevels;  // block-uniform
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+            const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+            const float w = wx * wy * wz;
+            const float dwx = (ox ? sx : -sx) * (wy * wz);
+            const float dwy = (oy ? sy : -sy) * (wx * wz);
+            const float dwz = (oz ? sz : -sz) * (wx * wy);
+            const float qd = dwx * q0 + dwy * q1 + dwz * q2;
+            const float a = valid ? fmaf(w, de0, jd0 * qd) : 0.f;
+            const float b = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
+            const uint32_t row = corner_row(lv, cx + ox, cy + oy, cz + oz);
+            if (agg) seg_red(gt, row, a, b, lane);
+            else if (valid) red_add_f32x2(gt + 2 * row, a, b);
+        }
+    }
+}
+
 static int g_tc_attr = 0;
 static int ensure_tc_attrs() {
     if (g_tc_attr) return NS2B_OK;
@@ -837,36 +998,52 @@ static int ensure_tc_attrs() {
 
 }  // namespace tc
 
+int field_workspace_bytes(int64_t capacity, size_t *bytes) {
+    NS2B_REQUIRE(bytes != nullptr && capacity >= 0, "workspace query");
+    const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
+    *bytes = static_cast<size_t>(ntiles) * tc::ws_tile_bytes() + 256;
+    return NS2B_OK;
+}
+
 int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                      const int32_t *count, int64_t capacity, float *sdf, float *colors, float *normals, float *geo,
-                     double *eik_sum, cudaStream_t st) {
+                     double *eik_sum, void *workspace, cudaStream_t st) {
     FieldDev f;
     int rc = make_field_dev(field, f);
     if (rc) return rc;
     if ((rc = tc::ensure_tc_attrs())) return rc;
+    NS2B_REQUIRE(workspace != nullptr, "field_forward: workspace required (ns2b_field_workspace_bytes)");
     if (capacity <= 0) return NS2B_OK;
-    const int blocks = grid_for(capacity, tc::TILE, kNumSMs);
-    tc::field_tc_kernel<false><<<blocks, tc::TILE, tc::SMEM_FWD, st>>>(
+    const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
+    const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
+    tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, count, ws);
+    if ((rc = check_launch("field_gather"))) return rc;
+    tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::TILE, tc::SMEM_FWD, st>>>(
         f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,
-        nullptr, nullptr, nullptr, nullptr);
+        nullptr, nullptr, nullptr, ws);
     return check_launch("field_forward_tc");
 }
 
 int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                       const int32_t *count, int64_t capacity, const float *dl_dc, const float *dl_dsdf,
                       const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
-                      float *grad_color, float *grad_tables, cudaStream_t st) {
+                      float *grad_color, float *grad_tables, void *workspace, cudaStream_t st) {
     FieldDev f;
     int rc = make_field_dev(field, f);
     if (rc) return rc;
     if ((rc = tc::ensure_tc_attrs())) return rc;
     NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
+    NS2B_REQUIRE(workspace != nullptr, "field_backward: workspace of the matching forward required");
     if (capacity <= 0) return NS2B_OK;
-    const int blocks = grid_for(capacity, tc::TILE, kNumSMs);
-    tc::field_tc_kernel<true><<<blocks, tc::TILE, tc::SMEM_BWD, st>>>(
+    const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
+    const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
+    tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::TILE, tc::SMEM_BWD, st>>>(
         f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf, dl_dn_extra,
-        static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, grad_tables);
-    return check_launch("field_backward_tc");
+        static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+    if ((rc = check_launch("field_backward_tc"))) return rc;
+    tc::field_scatter_kernel<<<grid_for(ntiles * f.n_active, 1, kNumSMs * 16), tc::TILE, 0, st>>>(
+        f, pos32, count, ws, grad_tables);
+    return check_launch("field_scatter");
 }
 
 }  // namespace ns2b

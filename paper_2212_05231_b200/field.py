@@ -230,6 +230,7 @@ class FieldCache:
     colors: torch.Tensor | None = None
     geo: torch.Tensor | None = None
     has_color: bool = True
+    workspace: torch.Tensor | None = None  # gather results the backward reuses
 
     @property
     def d(self):
@@ -286,11 +287,12 @@ def eval_field(params, x, view_dirs=None, max_level=None, need_color=True):
     normals = torch.empty((npts, 3), dtype=torch.float32, device=xb.device)
     geo = torch.empty((npts, GEO_FEATURE_DIM), dtype=torch.float32, device=xb.device)
     f = params.field_struct(na)
+    ws = _lib.field_workspace(npts, xb.device)
     _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(xb), _lib.ptr(ray_ids), _lib.ptr(v),
               _lib.ptr(count), npts, _lib.ptr(sdf), _lib.ptr(colors), _lib.ptr(normals),
-              _lib.ptr(geo), None, _lib.stream_ptr())
+              _lib.ptr(geo), None, _lib.ptr(ws), _lib.stream_ptr())
     return FieldCache(xb, max_level, na, ray_ids, v, count, sdf, normals,
-                      colors if need_color else None, geo, need_color)
+                      colors if need_color else None, geo, need_color, ws)
 
 
 def eval_sdf(params, x, max_level=None):
@@ -340,5 +342,6 @@ def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input
     _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.ray_ids),
               _lib.ptr(cache.dirs), _lib.ptr(cache.count), npts, _lib.ptr(gc), _lib.ptr(gd),
               _lib.ptr(gn), 0.0, None, _lib.ptr(grads.sdf_layers[0]),
-              _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.tables), _lib.stream_ptr())
+              _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.tables), _lib.ptr(cache.workspace),
+              _lib.stream_ptr())
     return grads

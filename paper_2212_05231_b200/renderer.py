@@ -257,11 +257,13 @@ def render_rays(batch, params, occ, max_level, point_transform=None, dir_transfo
         normals = torch.empty((P, 3), dtype=torch.float32, device=o.device)
         geo = torch.empty((P, fieldmod.GEO_FEATURE_DIM), dtype=torch.float32, device=o.device)
         f = params.field_struct(na)
+        ws = _lib.field_workspace(P, o.device)
         _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(mr.positions32),
                   _lib.ptr(mr.ray_ids), _lib.ptr(d), _lib.ptr(mr.count), P, _lib.ptr(sdf),
-                  _lib.ptr(cols), _lib.ptr(normals), _lib.ptr(geo), None, _lib.stream_ptr())
+                  _lib.ptr(cols), _lib.ptr(normals), _lib.ptr(geo), None, _lib.ptr(ws),
+                  _lib.stream_ptr())
         cache = fieldmod.FieldCache(mr.positions32, max_level, na, mr.ray_ids, d, mr.count, sdf,
-                                    normals, cols, geo, True)
+                                    normals, cols, geo, True, ws)
     rendered = torch.empty((m, 3), dtype=torch.float64, device=o.device)
     resid = torch.empty(m, dtype=torch.float64, device=o.device)
     a = torch.zeros(P, dtype=torch.float64, device=o.device)

@@ -175,6 +175,7 @@ class StepWorkspace:
             self.tb = torch.empty(cap, dtype=torch.float64, device=d)
             self.dl_dc = torch.empty((cap, 3), dtype=torch.float32, device=d)
             self.dl_dsdf = torch.empty(cap, dtype=torch.float32, device=d)
+            self.field_ws = _lib.field_workspace(cap, d)
             self.cap = cap
 
 
@@ -286,7 +287,7 @@ def train_step(state, dataset, time_index=0, batch=None):
     with _Timer(timers, "field_forward", st):
         _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
                   _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf), _lib.ptr(ws.colors), None,
-                  None, _lib.ptr(ws.sums[3:4]), sp)
+                  None, _lib.ptr(ws.sums[3:4]), _lib.ptr(ws.field_ws), sp)
     # K3/K4: composite + Huber + compositing backward
     with _Timer(timers, "composite", st):
         _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf),
@@ -306,7 +307,8 @@ def train_step(state, dataset, time_index=0, batch=None):
             _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(ws.pos32),
                       _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.dl_dc),
                       _lib.ptr(ws.dl_dsdf), None, cfg.eikonal_weight, _lib.ptr(ws.count64),
-                      _lib.ptr(sdf_g[0]), _lib.ptr(col_g[0]), _lib.ptr(tab_g), sp)
+                      _lib.ptr(sdf_g[0]), _lib.ptr(col_g[0]), _lib.ptr(tab_g),
+                      _lib.ptr(ws.field_ws), sp)
         if dp.active:
             with _Timer(timers, "allreduce", st):
                 dp.allreduce_(ws.grads[:end])
