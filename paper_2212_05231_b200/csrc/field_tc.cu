@@ -250,8 +250,60 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     return w;
 }
 
+// ---------------------------------------------------------------------------
+// MLP kernel: 512 threads per 128-sample tile.  Warp w reads TMEM lane quadrant w%4,
+// so thread (quarter k = w/4, row r = 32*(w%4) + lane) co-owns sample r with three
+// other threads; every per-row epilogue is split by 8-column blocks: the thread of
+// quarter k owns blocks k and k+4 of a tile.  Row scalars (the SDF value, the normal)
+// are combined through shared memory.  One elected thread issues all MMAs.
+constexpr int MLP_THREADS = 512;
+constexpr int NWARP = MLP_THREADS / 32;
+
+struct Reducer16 {
+    uint32_t (*red)[2][NWARP];
+    int parity;
+    __device__ void two(float a, float b, int &ea, int &eb) {
+        const int warp = threadIdx.x >> 5;
+        const uint32_t ra = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(a)));
+        const uint32_t rb = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(b)));
+        if ((threadIdx.x & 31) == 0) {
+            red[parity][0][warp] = ra;
+            red[parity][1][warp] = rb;
+        }
+        __syncthreads();
+        uint32_t ma = 0, mb = 0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) {
+            ma = max(ma, red[parity][0][w]);
+            mb = max(mb, red[parity][1][w]);
+        }
+        parity ^= 1;
+        ea = exp_for(__uint_as_float(ma));
+        eb = exp_for(__uint_as_float(mb));
+    }
+    __device__ int one(float a) {
+        int ea, eb;
+        two(a, 0.f, ea, eb);
+        return ea;
+    }
+};
+
+// stage one 8-column block of row r (values * sc) into a C-column tile
+template <int C>
+__device__ __forceinline__ void stage_blk(const Smem &s, uint32_t off, uint32_t part, int r, int b, const float *v,
+                                          float sc) {
+    uint4 h, l;
+    umma::split2<0>(v[0] * sc, v[1] * sc, h.x, l.x);
+    umma::split2<0>(v[2] * sc, v[3] * sc, h.y, l.y);
+    umma::split2<0>(v[4] * sc, v[5] * sc, h.z, l.z);
+    umma::split2<0>(v[6] * sc, v[7] * sc, h.w, l.w);
+    const uint32_t o = umma::tile_off(r, 8 * b, C);
+    *reinterpret_cast<uint4 *>(s.p(off) + o) = h;
+    *reinterpret_cast<uint4 *>(s.p(off + part) + o) = l;
+}
+
 template <bool kBwd>
-__global__ void __launch_bounds__(TILE, 1)
+__global__ void __launch_bounds__(MLP_THREADS, 1)
 field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
                 const double *__restrict__ dirs, const int32_t *__restrict__ count,
                 float *__restrict__ sdf_out, float *__restrict__ col_out, float *__restrict__ nrm_out,
@@ -262,28 +314,23 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_s;
-    __shared__ uint32_t red[2][2][4];
+    __shared__ uint32_t red[2][2][NWARP];
     __shared__ uint32_t wmax[5];
     __shared__ int wexp_s[5];
     __shared__ float h2row0[H];
-    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int qd = warp & 3, qt = warp >> 2;        // TMEM lane quadrant, column quarter
+    const int r = 32 * qd + lane;                    // sample row in the tile
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
 
-    if (t < NS2B_MAX_LEVELS) {
-        lvs[t].lv = f.lv[t];
-        lvs[t].sx = f.sx[t];
-        lvs[t].sy = f.sy[t];
-        lvs[t].sz = f.sz[t];
-    }
     if (t < H) h2row0[t] = f.sdf_w[H * (E + 1) + t];
     load_weight_tiles(S, f, wmax, wexp_s);
     const int eH1 = wexp_s[0], eH2 = wexp_s[1], eC1 = wexp_s[2], eC2 = wexp_s[3], eC3 = wexp_s[4];
     float *gacc = reinterpret_cast<float *>(S.p(GACC));
     if (kBwd)
-        for (int i = t; i < GACC_FLOATS; i += TILE) gacc[i] = 0.f;
+        for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) gacc[i] = 0.f;
     if (t == 0) {
         umma::mbar_init(&mbar, 1);
         umma::fence_barrier_init();
@@ -291,45 +338,36 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     if (warp == 0) umma::tmem_alloc(&tmem_base_s, 512);
     publish();
     const uint32_t tb = tmem_base_s;
-    const uint32_t my = tb + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    float *xch = reinterpret_cast<float *>(S.p(TZ));  // row-scalar exchange scratch (P1-P2)
     uint32_t phase = 0;
-    Reducer R{red, 0};
+    Reducer16 R{red, 0};
     const int P = *count;
     const float Pf = (kBwd && eik_count) ? static_cast<float>(*eik_count) : 1.f;
     const int G_H1r = 0, G_H2r = H * (E + 1), G_C1r = G_H2r + NOUT * H, G_C2r = G_C1r + H * CIN,
               G_C3r = G_C2r + H * H;
-    const int jrow = warp * 16 + lane;  // weight row held by lanes 0..15 in M=64 accumulators
+    const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
+    const int b0 = qt, b1 = qt + 4;   // my column blocks of 64-wide tiles
     float eik = 0.f;
 
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
-        const int64_t p = base + t;
+        const int64_t p = base + r;
         const bool valid = p < P;
-        float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
-        if (valid) {
-            x0 = pos[3 * p];
-            x1 = pos[3 * p + 1];
-            x2 = pos[3 * p + 2];
-            const int r = ray_ids[p];
-            v0 = static_cast<float>(dirs[3 * r]);
-            v1 = static_cast<float>(dirs[3 * r + 1]);
-            v2 = static_cast<float>(dirs[3 * r + 2]);
-        }
-        // ------------------------------------------------ P0: pre-staged E tile, J, Z1
         const int64_t tile = base / TILE;
         const float *Jt = ws.jac + tile * JROWS * TILE;
         float *SBt = ws.sb + tile * SBROWS * TILE;
-        int eE;
+        // ------------------------------------------------ P0: E tile, J, Z1
+        const int eE = ws.e_exp[tile];
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(ws.e_tiles + tile * 2 * TEB);
             uint4 *dst = reinterpret_cast<uint4 *>(S.p(TE));
-#pragma unroll 4
-            for (int i = t; i < static_cast<int>(2 * TEB / 16); i += TILE) dst[i] = src[i];
-            eE = ws.e_exp[tile];
+#pragma unroll
+            for (int i = t; i < static_cast<int>(2 * TEB / 16); i += MLP_THREADS) dst[i] = src[i];
             if (kBwd) {
 #pragma unroll 1
-                for (int l = 0; l < NA; ++l) {
-                    const float *jr = Jt + 6 * l * TILE + t;
+                for (int l = 4 * qt; l < min(NA, 4 * qt + 4); ++l) {
+                    const float *jr = Jt + 6 * l * TILE + r;
                     umma::tmem_st4(my + TM_J + 8 * l, jr[0], jr[TILE], jr[2 * TILE], jr[3 * TILE]);
                     umma::tmem_st2(my + TM_J + 8 * l + 4, jr[4 * TILE], jr[5 * TILE]);
                 }
@@ -342,35 +380,40 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P1: a1, s1 -> Y, JD
-        uint32_t mlo = 0u, mhi = 0u;
+        // ------------------------------------------------ P1: a1, s1 -> Y, JD; SDF value
+        uint32_t m1 = 0u;  // my 16 hidden-unit mask bits (blocks b0, b1)
         int eA1, eS1;
-        float d_sdf = 0.f;  // SDF value: exact-fp32 dot product (see below)
         {
-            float z[64];
-            umma::tmem_ld<64>(my + TM_Z1, z);
+            float z[2][8], s1[2][8], ma = 0.f, ms = 0.f, dpart = 0.f;
             const float sc = pow2i(-(eE + eH1));
-            float s1[64], ma = 0.f, ms = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const bool on = z[j] > 0.f;
-                if (on) {
-                    if (j < 32) mlo |= 1u << j;
-                    else mhi |= 1u << (j - 32);
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                umma::tmem_ld8(my + TM_Z1 + 8 * b, z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    m1 |= on ? (1u << (8 * i + k)) : 0u;
+                    const float a = on ? z[i][k] * sc : 0.f;
+                    z[i][k] = a;
+                    s1[i][k] = on ? h2row0[8 * b + k] : 0.f;
+                    ma = fmaxf(ma, a);
+                    ms = fmaxf(ms, fabsf(s1[i][k]));
+                    // d = H2[0] a1 in fp32 FMAs: a cancelling sum the NeuS alpha
+                    // differentiates along the ray (the MMA accumulator truncates)
+                    dpart = fmaf(h2row0[8 * b + k], a, dpart);
                 }
-                z[j] = on ? z[j] * sc : 0.f;
-                s1[j] = on ? h2row0[j] : 0.f;
-                ma = fmaxf(ma, z[j]);
-                ms = fmaxf(ms, fabsf(s1[j]));
-                // d = H2[0] a1 is a cancelling sum (~|x| - r at init) and alpha takes
-                // differences of sigmoid(s d) along a ray, so it is computed with fp32
-                // FMAs instead of the tensor core, whose fp32 accumulator truncates.
-                d_sdf = fmaf(h2row0[j], z[j], d_sdf);
             }
+            xch[qt * TILE + r] = dpart;
             R.two(ma, ms, eA1, eS1);
-            stage<64>(S, TX, T64B, t, z, eA1);
-            stage<64>(S, TY, T64B, t, s1, eS1);
+            const float sa = pow2i(eA1), ss = pow2i(eS1);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], sa);
+                stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
+            }
         }
+        const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), 4, ID_KK(16), false);
@@ -379,41 +422,50 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         }
         wait_mma(&mbar, phase);
         // ------------------------------------------------ P2: normal, cin -> Zc1
-        float y[16], n0, n1, n2;
-        float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
+        float y[16], n0, n1, n2, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
         int eCin;
         {
-            umma::tmem_ld<16>(my + TM_SB, y);
+            umma::tmem_ld8(my + TM_SB, *reinterpret_cast<float(*)[8]>(y));
+            umma::tmem_ld8(my + TM_SB + 8, *reinterpret_cast<float(*)[8]>(y + 8));
             const float scy = pow2i(-(eA1 + eH2));
 #pragma unroll
             for (int o = 0; o < 16; ++o) y[o] *= scy;
             y[0] = d_sdf;
+            // normal: my quarter's levels (+ the x rows for quarter 0), summed via smem
             const float scd = pow2i(-(eS1 + eH1));
-            float jx[4];
-            umma::tmem_ld4(my + TM_SA + 32, jx);  // j_d for x, y, z (tile cols 32..34)
-            n0 = jx[0] * scd;
-            n1 = jx[1] * scd;
-            n2 = jx[2] * scd;
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+            if (qt == 0) {
+                float jx[4];
+                umma::tmem_ld4(my + TM_SA + 32, jx);
+                p0 = jx[0] * scd;
+                p1 = jx[1] * scd;
+                p2 = jx[2] * scd;
+            }
 #pragma unroll 1
-            for (int l = 0; l < NA; ++l) {
+            for (int l = 4 * qt; l < min(NA, 4 * qt + 4); ++l) {
                 float d0, d1;
                 umma::tmem_ld2(my + TM_SA + 2 * l, d0, d1);
                 d0 *= scd;
                 d1 *= scd;
-                const float *jr = Jt + 6 * l * TILE + t;
-                float jl[6];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) jl[k] = jr[k * TILE];
-                if (kBwd) {  // j_d feature pair for the scatter kernel
-                    SBt[(32 + 2 * l) * TILE + t] = d0;
-                    SBt[(33 + 2 * l) * TILE + t] = d1;
+                const float *jr = Jt + 6 * l * TILE + r;
+                if (kBwd) {
+                    SBt[(32 + 2 * l) * TILE + r] = d0;
+                    SBt[(33 + 2 * l) * TILE + r] = d1;
                 }
-                n0 = fmaf(d0, jl[0], fmaf(d1, jl[3], n0));
-                n1 = fmaf(d0, jl[1], fmaf(d1, jl[4], n1));
-                n2 = fmaf(d0, jl[2], fmaf(d1, jl[5], n2));
+                p0 = fmaf(d0, jr[0], fmaf(d1, jr[3 * TILE], p0));
+                p1 = fmaf(d0, jr[TILE], fmaf(d1, jr[4 * TILE], p1));
+                p2 = fmaf(d0, jr[2 * TILE], fmaf(d1, jr[5 * TILE], p2));
             }
+            __syncthreads();  // xch reads of P1 are done
+            xch[(3 * qt + 0) * TILE + r] = p0;
+            xch[(3 * qt + 1) * TILE + r] = p1;
+            xch[(3 * qt + 2) * TILE + r] = p2;
+            __syncthreads();
+            n0 = xch[r] + xch[3 * TILE + r] + xch[6 * TILE + r] + xch[9 * TILE + r];
+            n1 = xch[TILE + r] + xch[4 * TILE + r] + xch[7 * TILE + r] + xch[10 * TILE + r];
+            n2 = xch[2 * TILE + r] + xch[5 * TILE + r] + xch[8 * TILE + r] + xch[11 * TILE + r];
             const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
-            if (valid) eik += (nn - 1.f) * (nn - 1.f);
+            if (valid && qt == 0) eik += (nn - 1.f) * (nn - 1.f);
             if (kBwd && valid) {
                 if (dl_dn_extra) {
                     gn0 = dl_dn_extra[3 * p];
@@ -427,97 +479,40 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     gn2 += coef * n2 / Pf;
                 }
             }
-            float cin[32];
-            cin[0] = x0;
-            cin[1] = x1;
-            cin[2] = x2;
-            cin[3] = n0;
-            cin[4] = n1;
-            cin[5] = n2;
-            cin[6] = v0;
-            cin[7] = v1;
-            cin[8] = v2;
-#pragma unroll
-            for (int o = 0; o < 16; ++o) cin[9 + o] = y[o];
-#pragma unroll
-            for (int i = 25; i < 32; ++i) cin[i] = 0.f;
-            eCin = R.one(absmax<25>(cin));
-            stage<32>(S, TC, TCB, t, cin, eCin);
-        }
-        publish();
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), 2, ID_KK(64), false);
-            umma::commit(&mbar);
-        }
-        wait_mma(&mbar, phase);
-        // ------------------------------------------------ P3: a1c -> Zc2
-        uint32_t c1lo = 0u, c1hi = 0u, c2lo = 0u, c2hi = 0u;
-        int eA1c, eA2c;
-        {
-            float z[64];
-            umma::tmem_ld<64>(my + TM_SA, z);
-            const float sc = pow2i(-(eCin + eC1));
-            float m = 0.f;
-#pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const bool on = z[j] > 0.f;
-                if (on) {
-                    if (j < 32) c1lo |= 1u << j;
-                    else c1hi |= 1u << (j - 32);
-                }
-                z[j] = on ? z[j] * sc : 0.f;
-                m = fmaxf(m, z[j]);
-            }
-            eA1c = R.one(m);
-            stage<64>(S, TZ, T64B, t, z, eA1c);
-        }
-        publish();
-        if (t == 0) {
-            umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), 4, ID_KK(64), false);
-            umma::commit(&mbar);
-        }
-        wait_mma(&mbar, phase);
-        // ------------------------------------------------ P4: a2c -> LOG
-        {
-            float z[64];
-            umma::tmem_ld<64>(my + TM_SB, z);
-            const float sc = pow2i(-(eA1c + eC2));
-            float m = 0.f;
-#pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const bool on = z[j] > 0.f;
-                if (on) {
-                    if (j < 32) c2lo |= 1u << j;
-                    else c2hi |= 1u << (j - 32);
-                }
-                z[j] = on ? z[j] * sc : 0.f;
-                m = fmaxf(m, z[j]);
-            }
-            eA2c = R.one(m);
-            stage<64>(S, TX, T64B, t, z, eA2c);
-        }
-        publish();
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), 4, ID_KK(16), false);
-            umma::commit(&mbar);
-        }
-        wait_mma(&mbar, phase);
-        // ------------------------------------------------ P5: colours (+ backward start)
-        float cc0, cc1, cc2;
-        {
-            float lg[4];
-            umma::tmem_ld4(my + TM_SA, lg);
-            const float sc = pow2i(-(eA2c + eC3));
-            cc0 = sigmoid_f(lg[0] * sc);
-            cc1 = sigmoid_f(lg[1] * sc);
-            cc2 = sigmoid_f(lg[2] * sc);
-        }
-        if (!kBwd) {
+            float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
             if (valid) {
-                sdf_out[p] = y[0];
-                col_out[3 * p] = cc0;
-                col_out[3 * p + 1] = cc1;
-                col_out[3 * p + 2] = cc2;
+                x0 = pos[3 * p];
+                x1 = pos[3 * p + 1];
+                x2 = pos[3 * p + 2];
+                const int rr = ray_ids[p];
+                v0 = static_cast<float>(dirs[3 * rr]);
+                v1 = static_cast<float>(dirs[3 * rr + 1]);
+                v2 = static_cast<float>(dirs[3 * rr + 2]);
+            }
+            // cin = [x, n, v, y] (field.py:237-239); quarter k stages block k of the 32
+            float blk[8];
+            float mc = 0.f;
+            if (qt == 0) {
+                blk[0] = x0; blk[1] = x1; blk[2] = x2; blk[3] = n0;
+                blk[4] = n1; blk[5] = n2; blk[6] = v0; blk[7] = v1;
+            } else if (qt == 1) {
+                blk[0] = v2;
+#pragma unroll
+                for (int k = 1; k < 8; ++k) blk[k] = y[k - 1];
+            } else if (qt == 2) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) blk[k] = y[7 + k];
+            } else {
+                blk[0] = y[15];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) blk[k] = 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mc = fmaxf(mc, fabsf(blk[k]));
+            eCin = R.one(mc);
+            stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
+            if (!kBwd && valid && qt == 0) {
+                sdf_out[p] = d_sdf;
                 if (nrm_out) {
                     nrm_out[3 * p] = n0;
                     nrm_out[3 * p + 1] = n1;
@@ -527,25 +522,100 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
                     for (int o = 1; o < 16; ++o) geo_out[15 * p + o - 1] = y[o];
             }
-            continue;
         }
-        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f;
-        if (valid) {
-            gc0 = dl_dc[3 * p];
-            gc1 = dl_dc[3 * p + 1];
-            gc2 = dl_dc[3 * p + 2];
-            gd = dl_dsdf[p];
+        publish();
+        if (t == 0) {
+            umma::gemm3(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), 2, ID_KK(64), false);
+            umma::commit(&mbar);
+        }
+        wait_mma(&mbar, phase);
+        // ------------------------------------------------ P3: a1c -> Zc2
+        uint32_t mc1 = 0u, mc2 = 0u;
+        int eA1c, eA2c;
+        {
+            float z[2][8], m = 0.f;
+            const float sc = pow2i(-(eCin + eC1));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SA + 8 * (i ? b1 : b0), z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    mc1 |= on ? (1u << (8 * i + k)) : 0u;
+                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    m = fmaxf(m, z[i][k]);
+                }
+            }
+            eA1c = R.one(m);
+            const float s = pow2i(eA1c);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
+        }
+        publish();
+        if (t == 0) {
+            umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), 4, ID_KK(64), false);
+            umma::commit(&mbar);
+        }
+        wait_mma(&mbar, phase);
+        // ------------------------------------------------ P4: a2c -> LOG
+        {
+            float z[2][8], m = 0.f;
+            const float sc = pow2i(-(eA1c + eC2));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    mc2 |= on ? (1u << (8 * i + k)) : 0u;
+                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    m = fmaxf(m, z[i][k]);
+                }
+            }
+            eA2c = R.one(m);
+            const float s = pow2i(eA2c);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], s);
+        }
+        publish();
+        if (t == 0) {
+            umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), 4, ID_KK(16), false);
+            umma::commit(&mbar);
+        }
+        wait_mma(&mbar, phase);
+        // ------------------------------------------------ P5: colours (+ backward start)
+        float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;
+        if (qt == 0) {
+            float lg[4];
+            umma::tmem_ld4(my + TM_SA, lg);
+            const float sc = pow2i(-(eA2c + eC3));
+            cc0 = sigmoid_f(lg[0] * sc);
+            cc1 = sigmoid_f(lg[1] * sc);
+            cc2 = sigmoid_f(lg[2] * sc);
+        } else {
+            float lg[4];
+            umma::tmem_ld4(my + TM_SA, lg);  // keep the warp-collective load uniform
+        }
+        if (!kBwd) {
+            if (valid && qt == 0) {
+                col_out[3 * p] = cc0;
+                col_out[3 * p + 1] = cc1;
+                col_out[3 * p + 2] = cc2;
+            }
+            continue;
         }
         int eD;
         {
-            float dlog[16];
-            dlog[0] = gc0 * cc0 * (1.f - cc0);  // field.py:304
-            dlog[1] = gc1 * cc1 * (1.f - cc1);
-            dlog[2] = gc2 * cc2 * (1.f - cc2);
+            float dlog[8];
 #pragma unroll
-            for (int i = 3; i < 16; ++i) dlog[i] = 0.f;
-            eD = R.one(absmax<3>(dlog));
-            stage<16>(S, TD, TDB, t, dlog, eD);
+            for (int k = 0; k < 8; ++k) dlog[k] = 0.f;
+            if (valid && qt == 0) {  // field.py:304
+                dlog[0] = dl_dc[3 * p] * cc0 * (1.f - cc0);
+                dlog[1] = dl_dc[3 * p + 1] * cc1 * (1.f - cc1);
+                dlog[2] = dl_dc[3 * p + 2] * cc2 * (1.f - cc2);
+            }
+            eD = R.one(fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
+            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
         }
         publish();
         if (t == 0) {
@@ -557,24 +627,28 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         // ------------------------------------------------ P6: dC3 fold; u2 -> U1, dC2
         int eU2;
         {
-            float d[16];
-            umma::tmem_ld<16>(my + TM_DC3, d);
-            if (lane < 16) {
+            float d[8];
+            umma::tmem_ld8(my + TM_DC3, d);
+            if (lane < 16 && qt == 0) {
                 const float sc = pow2i(-(eA2c + eD));
 #pragma unroll
                 for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sc;
             }
-            float u[64];
-            umma::tmem_ld<64>(my + TM_SA, u);
+            float u[2][8], m = 0.f;
             const float sc = pow2i(-(eD + eC3));
-            float m = 0.f;
 #pragma unroll
-            for (int k = 0; k < 64; ++k) {
-                u[k] = mask_bit(c2lo, c2hi, k) ? u[k] * sc : 0.f;
-                m = fmaxf(m, fabsf(u[k]));
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SA + 8 * (i ? b1 : b0), u[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[i][k] = ((mc2 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                    m = fmaxf(m, fabsf(u[i][k]));
+                }
             }
             eU2 = R.one(m);
-            stage<64>(S, TY, T64B, t, u, eU2);
+            const float s = pow2i(eU2);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
         }
         publish();
         if (t == 0) {
@@ -586,24 +660,31 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         // ------------------------------------------------ P7: dC2 fold; u1 -> DCIN, dC1
         int eU1;
         {
-            float d[64];
-            umma::tmem_ld<64>(my + TM_DC2, d);
+            float d[2][8];
+            umma::tmem_ld8(my + TM_DC2 + 8 * b0, d[0]);
+            umma::tmem_ld8(my + TM_DC2 + 8 * b1, d[1]);
             if (lane < 16) {
                 const float sc = pow2i(-(eU2 + eA1c));
 #pragma unroll
-                for (int c = 0; c < 64; ++c) gacc[G_C2r + jrow * H + c] += d[c] * sc;
-            }
-            float u[64];
-            umma::tmem_ld<64>(my + TM_SB, u);
-            const float sc = pow2i(-(eU2 + eC2));
-            float m = 0.f;
+                for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                u[j] = mask_bit(c1lo, c1hi, j) ? u[j] * sc : 0.f;
-                m = fmaxf(m, fabsf(u[j]));
+                    for (int k = 0; k < 8; ++k) gacc[G_C2r + jrow * H + 8 * (i ? b1 : b0) + k] += d[i][k] * sc;
+            }
+            float u[2][8], m = 0.f;
+            const float sc = pow2i(-(eU2 + eC2));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), u[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                    m = fmaxf(m, fabsf(u[i][k]));
+                }
             }
             eU1 = R.one(m);
-            stage<64>(S, TX, T64B, t, u, eU1);
+            const float s = pow2i(eU1);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
         }
         publish();
         if (t == 0) {
@@ -616,31 +697,56 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         float q0, q1, q2;
         int eDLY;
         {
-            float d[32];
-            umma::tmem_ld<32>(my + TM_DC1, d);
+            float d[8];
+            umma::tmem_ld8(my + TM_DC1 + 8 * qt, d);
             if (lane < 16) {
                 const float sc = pow2i(-(eU1 + eCin));
 #pragma unroll
-                for (int c = 0; c < CIN; ++c) gacc[G_C1r + jrow * CIN + c] += d[c] * sc;
+                for (int k = 0; k < 8; ++k)
+                    if (8 * qt + k < CIN) gacc[G_C1r + jrow * CIN + 8 * qt + k] += d[k] * sc;
             }
-            float dcin[32];
-            umma::tmem_ld<32>(my + TM_SA, dcin);
             const float sc3 = pow2i(-(eU1 + eC1));
-            q0 = gn0 + dcin[3] * sc3;  // field.py:308-312
-            q1 = gn1 + dcin[4] * sc3;
-            q2 = gn2 + dcin[5] * sc3;
-            float dly[16];
-            dly[0] = gd + dcin[9] * sc3;
+            float c0[8], c1[8], c2[8];
+            umma::tmem_ld8(my + TM_SA, c0);
+            umma::tmem_ld8(my + TM_SA + 8, c1);
+            umma::tmem_ld8(my + TM_SA + 16, c2);
+            float c3[8];
+            umma::tmem_ld8(my + TM_SA + 24, c3);
+            q0 = gn0 + c0[3] * sc3;  // field.py:308-312
+            q1 = gn1 + c0[4] * sc3;
+            q2 = gn2 + c0[5] * sc3;
+            // dly = [dd + dcin[9], dcin[10..24]]: block 0 (quarter 0), block 1 (quarter 1)
+            float blk[8];
+            if (qt == 0) {
+                blk[0] = (valid ? dl_dsdf[p] : 0.f) + c1[1] * sc3;
 #pragma unroll
-            for (int o = 1; o < 16; ++o) dly[o] = dcin[9 + o] * sc3;
-            eDLY = R.one(absmax<16>(dly));
-            stage<16>(S, TD, TDB, t, dly, eDLY);
-            float z[64];
-            umma::tmem_ld<64>(my + TM_Z1, z);
+                for (int k = 1; k < 7; ++k) blk[k] = c1[1 + k] * sc3;
+                blk[7] = c2[0] * sc3;
+            } else if (qt == 1) {
+#pragma unroll
+                for (int k = 0; k < 7; ++k) blk[k] = c2[1 + k] * sc3;
+                blk[7] = c3[0] * sc3;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) blk[k] = 0.f;
+            }
+            float m = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(blk[k]));
+            // A1 restage (ReLU of Z1) for dH2 += A1^T DLY
+            float z[2][8];
             const float sz = pow2i(-(eE + eH1));
 #pragma unroll
-            for (int j = 0; j < 64; ++j) z[j] = z[j] > 0.f ? z[j] * sz : 0.f;
-            stage<64>(S, TY, T64B, t, z, eA1);
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_Z1 + 8 * (i ? b1 : b0), z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) z[i][k] = z[i][k] > 0.f ? z[i][k] * sz : 0.f;
+            }
+            eDLY = R.one(m);
+            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
+            const float sa = pow2i(eA1);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, z[i], sa);
         }
         publish();
         if (t == 0) {
@@ -652,50 +758,68 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         // ------------------------------------------------ P9: dH2 fold; u, mvec -> DE, PV, dH1
         int eU, eMV;
         {
-            float d[16];
-            umma::tmem_ld<16>(my + TM_DH2, d);
-            if (lane < 16) {
-                const float sc = pow2i(-(eA1 + eDLY));
+            if (qt < 2) {
+                float d[8];
+                umma::tmem_ld8(my + TM_DH2 + 8 * qt, d);
+                if (lane < 16) {
+                    const float sc = pow2i(-(eA1 + eDLY));
 #pragma unroll
-                for (int o = 0; o < 16; ++o) gacc[G_H2r + o * H + jrow] += d[o] * sc;
+                    for (int k = 0; k < 8; ++k) gacc[G_H2r + (8 * qt + k) * H + jrow] += d[k] * sc;
+                }
+            } else {
+                float d[8];
+                umma::tmem_ld8(my + TM_DH2, d);
             }
-            float u[64];
-            umma::tmem_ld<64>(my + TM_SB, u);
+            float u[2][8], mu = 0.f;
             const float sc4 = pow2i(-(eDLY + eH2));
-            float mu = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                u[j] = mask_bit(mlo, mhi, j) ? u[j] * sc4 : 0.f;
-                mu = fmaxf(mu, fabsf(u[j]));
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), u[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
+                    mu = fmaxf(mu, fabsf(u[i][k]));
+                }
             }
-            // mvec feature rows J q (field.py:326-327) -> scratch TM_DC2[0..32)
-            float mm = fmaxf(fmaxf(fabsf(q0), fabsf(q1)), fabsf(q2));
-#pragma unroll 1
-            for (int l = 0; l < NA; ++l) {
+            // mvec = [J q (features), q, 0] (field.py:326-327); quarter k: block k
+            // (levels 4k..4k+3) and block k+4 (block 4 holds q)
+            float mv[2][8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                mv[0][k] = 0.f;
+                mv[1][k] = 0.f;
+            }
+            float mm = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = 4 * qt + i;
                 float jl[8];
                 umma::tmem_ld8(my + TM_J + 8 * l, jl);
-                const float a0 = jl[0] * q0 + jl[1] * q1 + jl[2] * q2;
-                const float a1 = jl[3] * q0 + jl[4] * q1 + jl[5] * q2;
-                mm = fmaxf(mm, fmaxf(fabsf(a0), fabsf(a1)));
-                umma::tmem_st2(my + TM_DC2 + 2 * l, a0, a1);
+                if (l < NA) {
+                    mv[0][2 * i] = jl[0] * q0 + jl[1] * q1 + jl[2] * q2;
+                    mv[0][2 * i + 1] = jl[3] * q0 + jl[4] * q1 + jl[5] * q2;
+                }
             }
-            umma::tmem_st_wait();
+            if (qt == 0) {
+                mv[1][0] = q0;
+                mv[1][1] = q1;
+                mv[1][2] = q2;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
             R.two(mu, mm, eU, eMV);
-            stage<64>(S, TX, T64B, t, u, eU);
-            float mv[48];
-            umma::tmem_ld<32>(my + TM_DC2, mv);
+            const float su = pow2i(eU), sm = pow2i(eMV), ss = pow2i(eS1);
+            float s1[8];
 #pragma unroll
-            for (int a = 0; a < 32; ++a) mv[a] = (a < 2 * NA) ? mv[a] : 0.f;
-            mv[32] = q0;
-            mv[33] = q1;
-            mv[34] = q2;
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                stage_blk<64>(S, TX, T64B, r, b, u[i], su);
 #pragma unroll
-            for (int i = 35; i < 48; ++i) mv[i] = 0.f;
-            stage<48>(S, TZ, T64B, t, mv, eMV);
-            float s1[64];
-#pragma unroll
-            for (int j = 0; j < 64; ++j) s1[j] = mask_bit(mlo, mhi, j) ? h2row0[j] : 0.f;
-            stage<64>(S, TY, T64B, t, s1, eS1);
+                for (int k = 0; k < 8; ++k) s1[k] = ((m1 >> (8 * i + k)) & 1u) ? h2row0[8 * b + k] : 0.f;
+                stage_blk<64>(S, TY, T64B, r, b, s1, ss);
+            }
+            stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
+            if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
         }
         publish();
         if (t == 0) {
@@ -706,60 +830,68 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P10: dH1 fold; pvec, scatter
+        // ------------------------------------------------ P10: dH1 fold; pvec; scatter inputs
         int ePV;
         {
-            float da[48], db[48];
-            umma::tmem_ld<48>(my + TM_DH1, da);
-            umma::tmem_ld<48>(my + TM_DC2, db);
-            if (lane < 16) {
-                const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
+            const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
 #pragma unroll
-                for (int c = 0; c < 36; ++c) {
-                    const int rc = h1_col(c, E);
-                    if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[c] * sa + db[c] * sb;
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                float da[8], db[8];
+                umma::tmem_ld8(my + TM_DH1 + 8 * (b < 6 ? b : 0), da);
+                umma::tmem_ld8(my + TM_DC2 + 8 * (b < 6 ? b : 0), db);
+                if (lane < 16 && b < 6) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int rc = h1_col(8 * b + k, E);
+                        if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[k] * sa + db[k] * sb;
+                    }
                 }
             }
-            float pv[64];
-            umma::tmem_ld<64>(my + TM_SB, pv);
+            float pv[2][8], m = 0.f;
             const float sc = pow2i(-(eMV + eH1));
-            float m = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                pv[j] = mask_bit(mlo, mhi, j) ? pv[j] * sc : 0.f;
-                m = fmaxf(m, fabsf(pv[j]));
+            for (int i = 0; i < 2; ++i) {
+                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), pv[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    pv[i][k] = ((m1 >> (8 * i + k)) & 1u) ? pv[i][k] * sc : 0.f;
+                    m = fmaxf(m, fabsf(pv[i][k]));
+                }
+            }
+            // dL/dfeature pairs (DE) and q for the scatter kernel
+            const float sde = pow2i(-(eU + eH1));
+            float de[8];
+            umma::tmem_ld8(my + TM_SA + 8 * qt, de);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (8 * qt + k < 2 * NA) SBt[(8 * qt + k) * TILE + r] = de[k] * sde;
+            if (qt == 0) {
+                SBt[64 * TILE + r] = q0;
+                SBt[65 * TILE + r] = q1;
+                SBt[66 * TILE + r] = q2;
             }
             ePV = R.one(m);
-            stage<64>(S, TX, T64B, t, pv, ePV);
-            float ones[16];
+            const float s = pow2i(ePV);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) ones[i] = i == 0 ? 1.f : 0.f;
-            stage<16>(S, TD, TDB, t, ones, 0);
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
+            if (qt < 2) {
+                float ones[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) ones[k] = (qt == 0 && k == 0) ? 1.f : 0.f;
+                stage_blk<16>(S, TD, TDB, r, qt, ones, 1.f);
+            }
         }
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbar);
         }
-        // inputs of the table scatter (Eq. 9), consumed by field_scatter_kernel
-        {
-            const float sde = pow2i(-(eU + eH1));
-#pragma unroll 1
-            for (int l = 0; l < NA; ++l) {
-                float de0, de1;
-                umma::tmem_ld2(my + TM_SA + 2 * l, de0, de1);
-                SBt[(2 * l) * TILE + t] = de0 * sde;
-                SBt[(2 * l + 1) * TILE + t] = de1 * sde;
-            }
-            SBt[64 * TILE + t] = q0;
-            SBt[65 * TILE + t] = q1;
-            SBt[66 * TILE + t] = q2;
-        }
         wait_mma(&mbar, phase);
         {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
-            float d[16];
-            umma::tmem_ld<16>(my + TM_DC3, d);
-            if (lane < 16) gacc[G_H2r + jrow] += d[0] * pow2i(-ePV);
+            float d[8];
+            umma::tmem_ld8(my + TM_DC3, d);
+            if (lane < 16 && qt == 0) gacc[G_H2r + jrow] += d[0] * pow2i(-ePV);
         }
     }
     if (eik_sum) {
@@ -770,7 +902,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     __syncthreads();
     if (kBwd) {
         const int nsdf = H * (E + 1) + NOUT * H;
-        for (int i = t; i < GACC_FLOATS; i += TILE) {
+        for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) {
             const float v = gacc[i];
             if (v == 0.f) continue;
             if (i < nsdf) atomicAdd(g_sdf + i, v);
@@ -1018,7 +1150,7 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
     tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, count, ws);
     if ((rc = check_launch("field_gather"))) return rc;
-    tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::TILE, tc::SMEM_FWD, st>>>(
+    tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
         f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,
         nullptr, nullptr, nullptr, ws);
     return check_launch("field_forward_tc");
@@ -1037,7 +1169,7 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
-    tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::TILE, tc::SMEM_BWD, st>>>(
+    tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
         f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf, dl_dn_extra,
         static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
     if ((rc = check_launch("field_backward_tc"))) return rc;
