@@ -142,6 +142,28 @@ NS2B_API int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, c
  * ns2b_field_backward must get the workspace its matching ns2b_field_forward filled. */
 NS2B_API int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes);
 
+/* The four kernels ns2b_field_forward / ns2b_field_backward chain, as separate entry
+ * points (same arguments): gather (features + d feature/dx -> workspace), the tcgen05
+ * MLP forward, the tcgen05 MLP backward (weight gradients + per-sample scatter inputs
+ * -> workspace) and the table-gradient scatter (Eq. 9, warp-aggregated float2 REDs). */
+NS2B_API int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *count,
+                               int64_t capacity, void *workspace, void *stream);
+NS2B_API int ns2b_field_mlp_forward(const ns2b_field_t *field, const float *pos32,
+                                    const int32_t *ray_ids, const double *dirs,
+                                    const int32_t *count, int64_t capacity, float *sdf,
+                                    float *colors, float *normals, float *geo, double *eik_sum,
+                                    void *workspace, void *stream);
+NS2B_API int ns2b_field_mlp_backward(const ns2b_field_t *field, const float *pos32,
+                                     const int32_t *ray_ids, const double *dirs,
+                                     const int32_t *count, int64_t capacity, const float *dl_dc,
+                                     const float *dl_dsdf, const float *dl_dn_extra,
+                                     double eik_weight, const int64_t *eik_count,
+                                     float *grad_sdf, float *grad_color, void *workspace,
+                                     void *stream);
+NS2B_API int ns2b_field_scatter(const ns2b_field_t *field, const float *pos32, const int32_t *count,
+                                int64_t capacity, float *grad_tables, void *workspace,
+                                void *stream);
+
 /* Lean SDF-only query (renderer.py:131-142) on fp32 positions; d (P). */
 NS2B_API int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,
                    void *stream);

@@ -578,6 +578,11 @@ static int ensure_attrs() {
 
 namespace ns2b {
 int field_workspace_bytes(int64_t capacity, size_t *bytes);
+int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                   const double *dirs, const int32_t *count, int64_t capacity, float *sdf, float *colors,
+                   float *normals, float *geo, double *eik_sum, const float *dl_dc, const float *dl_dsdf,
+                   const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
+                   float *grad_color, float *grad_tables, void *workspace, cudaStream_t st);
 int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                      const int32_t *count, int64_t capacity, float *sdf, float *colors, float *normals, float *geo,
                      double *eik_sum, void *workspace, cudaStream_t st);
@@ -627,6 +632,39 @@ int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, const int3
 
 int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes) {
     return field_workspace_bytes(capacity, bytes);
+}
+
+int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *count, int64_t capacity,
+                      void *workspace, void *stream) {
+    return field_stage_tc(0, field, pos32, nullptr, nullptr, count, capacity, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, workspace,
+                          as_stream(stream));
+}
+
+int ns2b_field_mlp_forward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                           const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
+                           float *colors, float *normals, float *geo, double *eik_sum, void *workspace,
+                           void *stream) {
+    return field_stage_tc(1, field, pos32, ray_ids, dirs, count, capacity, sdf, colors, normals, geo, eik_sum,
+                          nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, workspace,
+                          as_stream(stream));
+}
+
+int ns2b_field_mlp_backward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                            const double *dirs, const int32_t *count, int64_t capacity, const float *dl_dc,
+                            const float *dl_dsdf, const float *dl_dn_extra, double eik_weight,
+                            const int64_t *eik_count, float *grad_sdf, float *grad_color, void *workspace,
+                            void *stream) {
+    return field_stage_tc(2, field, pos32, ray_ids, dirs, count, capacity, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, dl_dc, dl_dsdf, dl_dn_extra, eik_weight, eik_count, grad_sdf, grad_color,
+                          nullptr, workspace, as_stream(stream));
+}
+
+int ns2b_field_scatter(const ns2b_field_t *field, const float *pos32, const int32_t *count, int64_t capacity,
+                       float *grad_tables, void *workspace, void *stream) {
+    return field_stage_tc(3, field, pos32, nullptr, nullptr, count, capacity, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, grad_tables,
+                          workspace, as_stream(stream));
 }
 
 int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,

@@ -1137,6 +1137,42 @@ int field_workspace_bytes(int64_t capacity, size_t *bytes) {
     return NS2B_OK;
 }
 
+// split entry points (the trainer times each kernel; field_forward/backward chain them)
+int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                   const double *dirs, const int32_t *count, int64_t capacity, float *sdf, float *colors,
+                   float *normals, float *geo, double *eik_sum, const float *dl_dc, const float *dl_dsdf,
+                   const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
+                   float *grad_color, float *grad_tables, void *workspace, cudaStream_t st) {
+    FieldDev f;
+    int rc = make_field_dev(field, f);
+    if (rc) return rc;
+    if ((rc = tc::ensure_tc_attrs())) return rc;
+    NS2B_REQUIRE(workspace != nullptr, "field kernels need the workspace (ns2b_field_workspace_bytes)");
+    if (capacity <= 0) return NS2B_OK;
+    const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
+    const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
+    switch (which) {
+    case 0:
+        tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, count, ws);
+        return check_launch("field_gather");
+    case 1:
+        tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
+            f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,
+            nullptr, nullptr, nullptr, ws);
+        return check_launch("field_mlp_forward");
+    case 2:
+        NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
+        tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
+            f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf,
+            dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+        return check_launch("field_mlp_backward");
+    default:
+        tc::field_scatter_kernel<<<grid_for(ntiles * f.n_active, 1, kNumSMs * 16), tc::TILE, 0, st>>>(
+            f, pos32, count, ws, grad_tables);
+        return check_launch("field_scatter");
+    }
+}
+
 int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                      const int32_t *count, int64_t capacity, float *sdf, float *colors, float *normals, float *geo,
                      double *eik_sum, void *workspace, cudaStream_t st) {

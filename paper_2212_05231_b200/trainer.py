@@ -283,11 +283,14 @@ def train_step(state, dataset, time_index=0, batch=None):
     s = params.sharpness
     na = enc.active_level_count(params.grid, level)
     f = params.field_struct(na)
-    # K2: field forward (+ Eikonal sum)
-    with _Timer(timers, "field_forward", st):
-        _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
-                  _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf), _lib.ptr(ws.colors), None,
-                  None, _lib.ptr(ws.sums[3:4]), _lib.ptr(ws.field_ws), sp)
+    # K2: gather (features + d feature/dx -> workspace), tcgen05 MLP forward (+ Eikonal sum)
+    with _Timer(timers, "field_gather", st):
+        _lib.call("ns2b_field_gather", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(count), P,
+                  _lib.ptr(ws.field_ws), sp)
+    with _Timer(timers, "field_mlp_forward", st):
+        _lib.call("ns2b_field_mlp_forward", ctypes.byref(f), _lib.ptr(ws.pos32),
+                  _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf),
+                  _lib.ptr(ws.colors), None, None, _lib.ptr(ws.sums[3:4]), _lib.ptr(ws.field_ws), sp)
     # K3/K4: composite + Huber + compositing backward
     with _Timer(timers, "composite", st):
         _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf),
@@ -303,12 +306,14 @@ def train_step(state, dataset, time_index=0, batch=None):
         ws.count64.fill_(P_glob)
         # K5: field backward with the fused Eikonal cotangent
         sdf_g, col_g, tab_g = lay.views(ws.grads)
-        with _Timer(timers, "field_backward", st):
-            _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(ws.pos32),
+        with _Timer(timers, "field_mlp_backward", st):
+            _lib.call("ns2b_field_mlp_backward", ctypes.byref(f), _lib.ptr(ws.pos32),
                       _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.dl_dc),
                       _lib.ptr(ws.dl_dsdf), None, cfg.eikonal_weight, _lib.ptr(ws.count64),
-                      _lib.ptr(sdf_g[0]), _lib.ptr(col_g[0]), _lib.ptr(tab_g),
-                      _lib.ptr(ws.field_ws), sp)
+                      _lib.ptr(sdf_g[0]), _lib.ptr(col_g[0]), _lib.ptr(ws.field_ws), sp)
+        with _Timer(timers, "field_scatter", st):
+            _lib.call("ns2b_field_scatter", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(count), P,
+                      _lib.ptr(tab_g), _lib.ptr(ws.field_ws), sp)
         if dp.active:
             with _Timer(timers, "allreduce", st):
                 dp.allreduce_(ws.grads[:end])
