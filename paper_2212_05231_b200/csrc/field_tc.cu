@@ -358,6 +358,31 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         const float *Jt = ws.jac + tile * JROWS * TILE;
         float *SBt = ws.sb + tile * SBROWS * TILE;
         // ------------------------------------------------ P0: E tile, J, Z1
+        if (t == 0) {  // next tile of this CTA -> L2 while this one runs
+            const int64_t nt = tile + gridDim.x;
+            if (nt * TILE < P) {
+                umma::prefetch_l2(ws.e_tiles + nt * 2 * TEB, 2 * TEB);
+                umma::prefetch_l2(ws.jac + nt * JROWS * TILE, JROWS * TILE * 4);
+            }
+        }
+        // per-sample inputs, issued up front so their latency overlaps P0-P1
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
+        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f;
+        if (valid) {
+            x0 = pos[3 * p];
+            x1 = pos[3 * p + 1];
+            x2 = pos[3 * p + 2];
+            const int rr = ray_ids[p];
+            v0 = static_cast<float>(dirs[3 * rr]);
+            v1 = static_cast<float>(dirs[3 * rr + 1]);
+            v2 = static_cast<float>(dirs[3 * rr + 2]);
+            if (kBwd) {
+                gc0 = dl_dc[3 * p];
+                gc1 = dl_dc[3 * p + 1];
+                gc2 = dl_dc[3 * p + 2];
+                gd = dl_dsdf[p];
+            }
+        }
         const int eE = ws.e_exp[tile];
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(ws.e_tiles + tile * 2 * TEB);
@@ -447,14 +472,19 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 umma::tmem_ld2(my + TM_SA + 2 * l, d0, d1);
                 d0 *= scd;
                 d1 *= scd;
-                const float *jr = Jt + 6 * l * TILE + r;
+                float jl[8];
                 if (kBwd) {
+                    umma::tmem_ld8(my + TM_J + 8 * l, jl);
                     SBt[(32 + 2 * l) * TILE + r] = d0;
                     SBt[(33 + 2 * l) * TILE + r] = d1;
+                } else {
+                    const float *jr = Jt + 6 * l * TILE + r;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) jl[k] = jr[k * TILE];
                 }
-                p0 = fmaf(d0, jr[0], fmaf(d1, jr[3 * TILE], p0));
-                p1 = fmaf(d0, jr[TILE], fmaf(d1, jr[4 * TILE], p1));
-                p2 = fmaf(d0, jr[2 * TILE], fmaf(d1, jr[5 * TILE], p2));
+                p0 = fmaf(d0, jl[0], fmaf(d1, jl[3], p0));
+                p1 = fmaf(d0, jl[1], fmaf(d1, jl[4], p1));
+                p2 = fmaf(d0, jl[2], fmaf(d1, jl[5], p2));
             }
             __syncthreads();  // xch reads of P1 are done
             xch[(3 * qt + 0) * TILE + r] = p0;
@@ -478,16 +508,6 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     gn1 += coef * n1 / Pf;
                     gn2 += coef * n2 / Pf;
                 }
-            }
-            float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
-            if (valid) {
-                x0 = pos[3 * p];
-                x1 = pos[3 * p + 1];
-                x2 = pos[3 * p + 2];
-                const int rr = ray_ids[p];
-                v0 = static_cast<float>(dirs[3 * rr]);
-                v1 = static_cast<float>(dirs[3 * rr + 1]);
-                v2 = static_cast<float>(dirs[3 * rr + 2]);
             }
             // cin = [x, n, v, y] (field.py:237-239); quarter k stages block k of the 32
             float blk[8];
@@ -610,9 +630,9 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int k = 0; k < 8; ++k) dlog[k] = 0.f;
             if (valid && qt == 0) {  // field.py:304
-                dlog[0] = dl_dc[3 * p] * cc0 * (1.f - cc0);
-                dlog[1] = dl_dc[3 * p + 1] * cc1 * (1.f - cc1);
-                dlog[2] = dl_dc[3 * p + 2] * cc2 * (1.f - cc2);
+                dlog[0] = gc0 * cc0 * (1.f - cc0);
+                dlog[1] = gc1 * cc1 * (1.f - cc1);
+                dlog[2] = gc2 * cc2 * (1.f - cc2);
             }
             eD = R.one(fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
@@ -718,7 +738,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             // dly = [dd + dcin[9], dcin[10..24]]: block 0 (quarter 0), block 1 (quarter 1)
             float blk[8];
             if (qt == 0) {
-                blk[0] = (valid ? dl_dsdf[p] : 0.f) + c1[1] * sc3;
+                blk[0] = gd + c1[1] * sc3;
 #pragma unroll
                 for (int k = 1; k < 7; ++k) blk[k] = c1[1 + k] * sc3;
                 blk[7] = c2[0] * sc3;
@@ -1054,6 +1074,10 @@ __device__ __forceinline__ void seg_red(float *gt, uint32_t row, float a, float 
     if (tail) red_add_f32x2(gt + 2 * row, a, b);
 }
 
+__device__ __forceinline__ void red_add_f32x4(float *addr, float a, float b, float c, float d) {
+    atomicAdd(reinterpret_cast<float4 *>(addr), make_float4(a, b, c, d));
+}
+
 __global__ void __launch_bounds__(TILE)
 field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count,
                      const Workspace ws, float *__restrict__ g_tab) {
@@ -1069,48 +1093,71 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
     const int NA = f.n_active;
     const int P = *count;
     const int64_t ntiles = (static_cast<int64_t>(P) + TILE - 1) / TILE;
-    for (int64_t item = blockIdx.x; item < ntiles * NA; item += gridDim.x) {
-        const int64_t tile = item / NA;
-        const int l = static_cast<int>(item - tile * NA);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t p = tile * TILE + t;
         const bool valid = p < P;
         const float *SBt = ws.sb + tile * SBROWS * TILE + t;
-        float x0 = 0.f, x1 = 0.f, x2 = 0.f, de0 = 0.f, de1 = 0.f, jd0 = 0.f, jd1 = 0.f, q0 = 0.f, q1 = 0.f, q2 = 0.f;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, q0 = 0.f, q1 = 0.f, q2 = 0.f;
         if (valid) {
             x0 = pos[3 * p];
             x1 = pos[3 * p + 1];
             x2 = pos[3 * p + 2];
-            de0 = SBt[(2 * l) * TILE];
-            de1 = SBt[(2 * l + 1) * TILE];
-            jd0 = SBt[(32 + 2 * l) * TILE];
-            jd1 = SBt[(33 + 2 * l) * TILE];
             q0 = SBt[64 * TILE];
             q1 = SBt[65 * TILE];
             q2 = SBt[66 * TILE];
         }
-        const LevelInfo lv = lvs[l].lv;
-        const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
-        int cx, cy, cz;
-        float fx, fy, fz;
-        cell_frac(normalize_coord(x0, f.lo[0], f.ext[0]), lv.n, cx, fx);
-        cell_frac(normalize_coord(x1, f.lo[1], f.ext[1]), lv.n, cy, fy);
-        cell_frac(normalize_coord(x2, f.lo[2], f.ext[2]), lv.n, cz, fz);
-        float *gt = g_tab + l * f.T * 2;
-        const bool agg = l < kAggLevels;  // block-uniform
+        const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+        const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+        const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+#pragma unroll 1
+        for (int l = 0; l < NA; ++l) {
+            float de0 = 0.f, de1 = 0.f, jd0 = 0.f, jd1 = 0.f;
+            if (valid) {
+                de0 = SBt[(2 * l) * TILE];
+                de1 = SBt[(2 * l + 1) * TILE];
+                jd0 = SBt[(32 + 2 * l) * TILE];
+                jd1 = SBt[(33 + 2 * l) * TILE];
+            }
+            const LevelInfo lv = lvs[l].lv;
+            const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
+            int cx, cy, cz;
+            float fx, fy, fz;
+            cell_frac(un0, lv.n, cx, fx);
+            cell_frac(un1, lv.n, cy, fy);
+            cell_frac(un2, lv.n, cz, fz);
+            float *gt = g_tab + l * f.T * 2;
+            // corner c = 4 ox + 2 oy + oz; handle the x-pairs (c, c + 4) together
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-            const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-            const float w = wx * wy * wz;
-            const float dwx = (ox ? sx : -sx) * (wy * wz);
-            const float dwy = (oy ? sy : -sy) * (wx * wz);
-            const float dwz = (oz ? sz : -sz) * (wx * wy);
-            const float qd = dwx * q0 + dwy * q1 + dwz * q2;
-            const float a = valid ? fmaf(w, de0, jd0 * qd) : 0.f;
-            const float b = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
-            const uint32_t row = corner_row(lv, cx + ox, cy + oy, cz + oz);
-            if (agg) seg_red(gt, row, a, b, lane);
-            else if (valid) red_add_f32x2(gt + 2 * row, a, b);
+            for (int c = 0; c < 4; ++c) {
+                const int oy = (c >> 1) & 1, oz = c & 1;
+                const float wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                float a[2], b[2];
+                uint32_t row[2];
+#pragma unroll
+                for (int ox = 0; ox < 2; ++ox) {
+                    const float wx = ox ? fx : 1.f - fx;
+                    const float w = wx * wy * wz;
+                    const float dwx = (ox ? sx : -sx) * (wy * wz);
+                    const float dwy = (oy ? sy : -sy) * (wx * wz);
+                    const float dwz = (oz ? sz : -sz) * (wx * wy);
+                    const float qd = dwx * q0 + dwy * q1 + dwz * q2;
+                    a[ox] = valid ? fmaf(w, de0, jd0 * qd) : 0.f;
+                    b[ox] = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
+                    row[ox] = corner_row(lv, cx + ox, cy + oy, cz + oz);
+                }
+                if (l < kAggLevels) {  // coarse levels: runs of equal rows along the rays
+                    seg_red(gt, row[0], a[0], b[0], lane);
+                    seg_red(gt, row[1], a[1], b[1], lane);
+                } else if (valid) {
+                    if ((row[0] ^ row[1]) == 1u) {  // both corners in one 16-B row pair
+                        const int lo = row[0] & 1u;
+                        red_add_f32x4(gt + 2 * (row[0] & ~1u), a[lo], b[lo], a[lo ^ 1], b[lo ^ 1]);
+                    } else {
+                        red_add_f32x2(gt + 2 * row[0], a[0], b[0]);
+                        red_add_f32x2(gt + 2 * row[1], a[1], b[1]);
+                    }
+                }
+            }
         }
     }
 }
@@ -1167,8 +1214,8 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
             dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
         return check_launch("field_mlp_backward");
     default:
-        tc::field_scatter_kernel<<<grid_for(ntiles * f.n_active, 1, kNumSMs * 16), tc::TILE, 0, st>>>(
-            f, pos32, count, ws, grad_tables);
+        tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
+                                                                                       grad_tables);
         return check_launch("field_scatter");
     }
 }
@@ -1209,8 +1256,8 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
         f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf, dl_dn_extra,
         static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
     if ((rc = check_launch("field_backward_tc"))) return rc;
-    tc::field_scatter_kernel<<<grid_for(ntiles * f.n_active, 1, kNumSMs * 16), tc::TILE, 0, st>>>(
-        f, pos32, count, ws, grad_tables);
+    tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
+                                                                                   grad_tables);
     return check_launch("field_scatter");
 }
 

@@ -178,6 +178,11 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float *v) {
     }
 }
 
+// Bulk L2 prefetch (TMA engine) of a contiguous global range; bytes % 16 == 0.
+__device__ __forceinline__ void prefetch_l2(const void *gptr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
+}
+
 // ---------------------------------------------------------------- staging --
 // Byte offset of element (r, c) in a core-matrix tiled tile with C columns.
 __host__ __device__ constexpr uint32_t tile_off(int r, int c, int C) {
