@@ -312,7 +312,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 const float *__restrict__ dl_dn_extra, float eik_w, const int64_t *__restrict__ eik_count,
                 float *__restrict__ g_sdf, float *__restrict__ g_color, Workspace ws) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar;   // chain GEMMs of a phase (the next epilogue needs them)
+    __shared__ uint64_t mbarw;  // weight-gradient GEMMs (overlap the next epilogue)
     __shared__ uint32_t tmem_base_s;
     __shared__ uint32_t red[2][2][NWARP];
     __shared__ uint32_t wmax[5];
@@ -333,12 +334,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) gacc[i] = 0.f;
     if (t == 0) {
         umma::mbar_init(&mbar, 1);
+        umma::mbar_init(&mbarw, 1);
         umma::fence_barrier_init();
     }
     if (warp == 0) umma::tmem_alloc(&tmem_base_s, 512);
     publish();
     const uint32_t tb = tmem_base_s;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    uint32_t phasew = 0;
     float *xch = reinterpret_cast<float *>(S.p(TZ));  // row-scalar exchange scratch (P1-P2)
     uint32_t phase = 0;
     Reducer16 R{red, 0};
@@ -640,20 +643,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), 1, ID_KM(64), false);
-            umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbar);
+            umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
+            umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P6: dC3 fold; u2 -> U1, dC2
+        // ------------------------------------------------ P6: u2 -> U1, dC2; dC3 fold
         int eU2;
         {
-            float d[8];
-            umma::tmem_ld8(my + TM_DC3, d);
-            if (lane < 16 && qt == 0) {
-                const float sc = pow2i(-(eA2c + eD));
-#pragma unroll
-                for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sc;
-            }
             float u[2][8], m = 0.f;
             const float sc = pow2i(-(eD + eC3));
 #pragma unroll
@@ -666,6 +663,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 }
             }
             eU2 = R.one(m);
+            wait_mma(&mbarw, phasew);  // dC3 (P5) done
+            float d[8];
+            umma::tmem_ld8(my + TM_DC3, d);
+            if (lane < 16 && qt == 0) {
+                const float sd = pow2i(-(eA2c + eD));
+#pragma unroll
+                for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sd;
+            }
             const float s = pow2i(eU2);
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
@@ -673,23 +678,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), 4, ID_KM(64), false);
-            umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), 8, ID_WG(64), false);
             umma::commit(&mbar);
+            umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), 8, ID_WG(64), false);
+            umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P7: dC2 fold; u1 -> DCIN, dC1
+        // ------------------------------------------------ P7: u1 -> DCIN, dC1; dC2 fold
         int eU1;
         {
-            float d[2][8];
-            umma::tmem_ld8(my + TM_DC2 + 8 * b0, d[0]);
-            umma::tmem_ld8(my + TM_DC2 + 8 * b1, d[1]);
-            if (lane < 16) {
-                const float sc = pow2i(-(eU2 + eA1c));
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) gacc[G_C2r + jrow * H + 8 * (i ? b1 : b0) + k] += d[i][k] * sc;
-            }
             float u[2][8], m = 0.f;
             const float sc = pow2i(-(eU2 + eC2));
 #pragma unroll
@@ -702,6 +698,17 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 }
             }
             eU1 = R.one(m);
+            wait_mma(&mbarw, phasew);  // dC2 (P6) done
+            float d[2][8];
+            umma::tmem_ld8(my + TM_DC2 + 8 * b0, d[0]);
+            umma::tmem_ld8(my + TM_DC2 + 8 * b1, d[1]);
+            if (lane < 16) {
+                const float sd = pow2i(-(eU2 + eA1c));
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) gacc[G_C2r + jrow * H + 8 * (i ? b1 : b0) + k] += d[i][k] * sd;
+            }
             const float s = pow2i(eU1);
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
@@ -709,22 +716,15 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), 4, ID_KM(32), false);
-            umma::gemm3(tb + TM_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), 8, ID_WG(32), false);
             umma::commit(&mbar);
+            umma::gemm3(tb + TM_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), 8, ID_WG(32), false);
+            umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P8: dC1 fold; q, dly -> U, dH2
+        // ------------------------------------------------ P8: q, dly -> U, dH2; dC1 fold
         float q0, q1, q2;
         int eDLY;
         {
-            float d[8];
-            umma::tmem_ld8(my + TM_DC1 + 8 * qt, d);
-            if (lane < 16) {
-                const float sc = pow2i(-(eU1 + eCin));
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (8 * qt + k < CIN) gacc[G_C1r + jrow * CIN + 8 * qt + k] += d[k] * sc;
-            }
             const float sc3 = pow2i(-(eU1 + eC1));
             float c0[8], c1[8], c2[8];
             umma::tmem_ld8(my + TM_SA, c0);
@@ -763,6 +763,15 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 for (int k = 0; k < 8; ++k) z[i][k] = z[i][k] > 0.f ? z[i][k] * sz : 0.f;
             }
             eDLY = R.one(m);
+            wait_mma(&mbarw, phasew);  // dC1 (P7) done
+            float d[8];
+            umma::tmem_ld8(my + TM_DC1 + 8 * qt, d);
+            if (lane < 16) {
+                const float sd = pow2i(-(eU1 + eCin));
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (8 * qt + k < CIN) gacc[G_C1r + jrow * CIN + 8 * qt + k] += d[k] * sd;
+            }
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
             const float sa = pow2i(eA1);
 #pragma unroll
@@ -771,25 +780,14 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), 1, ID_KM(64), false);
-            umma::gemm3(tb + TM_DH2, S.MN(TY, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbar);
+            umma::gemm3(tb + TM_DH2, S.MN(TY, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
+            umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P9: dH2 fold; u, mvec -> DE, PV, dH1
+        // ------------------------------------------------ P9: u, mvec -> DE, PV, dH1; dH2 fold
         int eU, eMV;
         {
-            if (qt < 2) {
-                float d[8];
-                umma::tmem_ld8(my + TM_DH2 + 8 * qt, d);
-                if (lane < 16) {
-                    const float sc = pow2i(-(eA1 + eDLY));
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) gacc[G_H2r + (8 * qt + k) * H + jrow] += d[k] * sc;
-                }
-            } else {
-                float d[8];
-                umma::tmem_ld8(my + TM_DH2, d);
-            }
             float u[2][8], mu = 0.f;
             const float sc4 = pow2i(-(eDLY + eH2));
 #pragma unroll
@@ -828,6 +826,19 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
             R.two(mu, mm, eU, eMV);
+            wait_mma(&mbarw, phasew);  // dH2 (P8) done
+            if (qt < 2) {
+                float d[8];
+                umma::tmem_ld8(my + TM_DH2 + 8 * qt, d);
+                if (lane < 16) {
+                    const float sd = pow2i(-(eA1 + eDLY));
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) gacc[G_H2r + (8 * qt + k) * H + jrow] += d[k] * sd;
+                }
+            } else {
+                float d[8];
+                umma::tmem_ld8(my + TM_DH2, d);
+            }
             const float su = pow2i(eU), sm = pow2i(eMV), ss = pow2i(eS1);
             float s1[8];
 #pragma unroll
@@ -845,29 +856,15 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
             umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
+            umma::commit(&mbar);
             umma::gemm3(tb + TM_DH1, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), 8, ID_WG(48), false);
             umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), false);
-            umma::commit(&mbar);
+            umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
-        // ------------------------------------------------ P10: dH1 fold; pvec; scatter inputs
+        // ------------------------------------------------ P10: pvec; scatter inputs; dH1 fold
         int ePV;
         {
-            const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int b = i ? b1 : b0;
-                float da[8], db[8];
-                umma::tmem_ld8(my + TM_DH1 + 8 * (b < 6 ? b : 0), da);
-                umma::tmem_ld8(my + TM_DC2 + 8 * (b < 6 ? b : 0), db);
-                if (lane < 16 && b < 6) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int rc = h1_col(8 * b + k, E);
-                        if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[k] * sa + db[k] * sb;
-                    }
-                }
-            }
             float pv[2][8], m = 0.f;
             const float sc = pow2i(-(eMV + eH1));
 #pragma unroll
@@ -892,6 +889,22 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 SBt[66 * TILE + r] = q2;
             }
             ePV = R.one(m);
+            wait_mma(&mbarw, phasew);  // dH1 (P9) done
+            const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                float da[8], db[8];
+                umma::tmem_ld8(my + TM_DH1 + 8 * (b < 6 ? b : 0), da);
+                umma::tmem_ld8(my + TM_DC2 + 8 * (b < 6 ? b : 0), db);
+                if (lane < 16 && b < 6) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int rc = h1_col(8 * b + k, E);
+                        if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[k] * sa + db[k] * sb;
+                    }
+                }
+            }
             const float s = pow2i(ePV);
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
@@ -905,9 +918,9 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
         publish();
         if (t == 0) {
             umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
-            umma::commit(&mbar);
+            umma::commit(&mbarw);
         }
-        wait_mma(&mbar, phase);
+        wait_mma(&mbarw, phasew);
         {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
             float d[8];
             umma::tmem_ld8(my + TM_DC3, d);
