@@ -319,7 +319,16 @@ def run_ours(args, wl):
     per_kernel = {k: statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:])
                   for k, v in timers.items()}
     # end-to-end leg through the public API with host batches
-    ms_e2e, _, _, _ = timed(host=True)
+    if os.environ.get("NS2B_BENCH_DEBUG"):
+        st.timers = {}
+    ms_e2e, _, _, wall_e2e = timed(host=True)
+    if os.environ.get("NS2B_BENCH_DEBUG"):
+        dbg = {k: round(statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:]), 3)
+               for k, v in st.timers.items()}
+        print(json.dumps({"debug_e2e_kernels": dbg, "ms_e2e": ms_e2e, "wall_e2e": wall_e2e,
+                          "ms_dev": ms_dev, "wall_dev": wall, "dev_kernels":
+                          {k: round(v, 3) for k, v in per_kernel.items()}}), file=sys.stderr)
+        st.timers = None
     P_mean = statistics.mean(r.sample_count for r in reps)
     value = m_global * args.steps / (ms_dev * 1e-3)
     e2e = m_global * args.steps / (ms_e2e * 1e-3)
@@ -330,14 +339,15 @@ def run_ours(args, wl):
     Pl = P_mean / world  # per-rank samples per launch
     L = wl["levels"]
     # Algorithmic work per sample:
-    #   gather:  8 corners x 2 fp32 features x L table reads + 12 B position
-    #            + 576 B written (pre-staged encoding tile 192 B + d feature/dx 384 B)
+    #   gather:  8 corners x 2 fp32 features x L table reads + 12 B position + 28 B ray id
+    #            and fp64 view dir + 600 B written (pre-staged encoding tile 192 B,
+    #            d feature/dx 384 B, fp32 position + view dir 24 B)
     #   scatter: 8 corners x L float2 REDs (8 B each) + 32 B of inputs
     #   MLP fwd: 11,520 MAC (SDF 36x64, 64x16, j_d 64x36; colour 25x64, 64x64, 64x3)
     #   MLP bwd: 34,624 MAC (forward recompute + input cotangents + weight gradients,
     #            incl. the Theorem-1 terms) -- algorithmic dims, not the 3x split
     work = {
-        "field_gather": ("hbm", Pl * (8 * 2 * 4 * L + 12 + 576), "GB/s"),
+        "field_gather": ("hbm", Pl * (8 * 2 * 4 * L + 12 + 28 + 600), "GB/s"),
         "field_scatter": ("hbm", Pl * (8 * 8 * L + 32), "GB/s"),
         "field_mlp_forward": ("tensor", Pl * 2 * 11520, "TFLOP/s"),
         "field_mlp_backward": ("tensor", Pl * 2 * 34624, "TFLOP/s"),

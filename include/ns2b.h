@@ -143,11 +143,15 @@ NS2B_API int ns2b_field_forward(const ns2b_field_t *field, const float *pos32, c
 NS2B_API int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes);
 
 /* The four kernels ns2b_field_forward / ns2b_field_backward chain, as separate entry
- * points (same arguments): gather (features + d feature/dx -> workspace), the tcgen05
- * MLP forward, the tcgen05 MLP backward (weight gradients + per-sample scatter inputs
- * -> workspace) and the table-gradient scatter (Eq. 9, warp-aggregated float2 REDs). */
-NS2B_API int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *count,
-                               int64_t capacity, void *workspace, void *stream);
+ * points (same arguments): gather (features + d feature/dx, positions and fp32 view
+ * directions -> workspace), the tcgen05 MLP forward, the tcgen05 MLP backward (weight
+ * gradients + per-sample scatter inputs -> workspace) and the table-gradient scatter
+ * (Eq. 9, warp-aggregated float2 REDs).  The MLP kernels take their per-sample inputs
+ * from the workspace the gather filled (pos32/ray_ids/dirs are kept in their signatures
+ * for the fused entry points). */
+NS2B_API int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                               const double *dirs, const int32_t *count, int64_t capacity,
+                               void *workspace, void *stream);
 NS2B_API int ns2b_field_mlp_forward(const ns2b_field_t *field, const float *pos32,
                                     const int32_t *ray_ids, const double *dirs,
                                     const int32_t *count, int64_t capacity, float *sdf,

@@ -64,7 +64,7 @@ _SIGS = {
     "ns2b_field_forward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
                                           P, P]),
     "ns2b_field_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),
-    "ns2b_field_gather": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, I64, P, P]),
+    "ns2b_field_gather": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P]),
     "ns2b_field_mlp_forward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
                                               P, P]),
     "ns2b_field_mlp_backward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, F64,

@@ -41,7 +41,7 @@ def _compile(src: Path, force: bool) -> Path:
     obj = BUILD / (src.stem + ".o")
     if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, _deps_mtime()):
         return obj
-    flags = list(COMMON)
+    flags = list(COMMON) + os.environ.get("NS2B_NVCC_EXTRA", "").split()
     if src.name in NO_FMA:
         flags.append("-fmad=false")
     cmd = [NVCC, *ARCH, *flags, "-Xptxas", "-v" if os.environ.get("NS2B_PTXAS_V") else "-O3",

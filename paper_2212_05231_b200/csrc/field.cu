@@ -634,9 +634,10 @@ int ns2b_field_workspace_bytes(int64_t capacity, size_t *bytes) {
     return field_workspace_bytes(capacity, bytes);
 }
 
-int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *count, int64_t capacity,
-                      void *workspace, void *stream) {
-    return field_stage_tc(0, field, pos32, nullptr, nullptr, count, capacity, nullptr, nullptr, nullptr, nullptr,
+int ns2b_field_gather(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
+                      const int32_t *count, int64_t capacity, void *workspace, void *stream) {
+    NS2B_REQUIRE(pos32 && ray_ids && dirs && count, "field_gather: null input");
+    return field_stage_tc(0, field, pos32, ray_ids, dirs, count, capacity, nullptr, nullptr, nullptr, nullptr,
                           nullptr, nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, workspace,
                           as_stream(stream));
 }

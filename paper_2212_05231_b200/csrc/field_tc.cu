@@ -32,6 +32,8 @@
 //   P8 q, dly -> U = DLY H2,     dH2 += A1^T DLY
 //   P9 u, mvec=[Jq,q] -> DE = U H1, PV = MV H1^T,  dH1 += U^T E + S1^T MV  (Thm 1)
 //   P10 dH2[0] += sum pv (PV^T ONES);  fused first+second-order table scatter (Eq. 9)
+#include <cstdio>
+
 #include "field_common.cuh"
 #include "umma.cuh"
 
@@ -82,6 +84,21 @@ constexpr uint32_t TM_SB = 432;   // 64 chain slot B
 constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
 constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
+
+#ifdef NS2B_PHASE_PROF
+#define PMARK(i)                                  \
+    do {                                          \
+        if (threadIdx.x == 160) {                 \
+            const long long c_ = clock64();       \
+            pacc[(i) & 63] += c_ - plast;         \
+            plast = c_;                           \
+        }                                         \
+    } while (0)
+#else
+#define PMARK(i) \
+    do {         \
+    } while (0)
+#endif
 
 __device__ __forceinline__ float pow2i(int e) {
     e = e < -120 ? -120 : (e > 120 ? 120 : e);
@@ -226,16 +243,18 @@ struct LevelSm {
 // Per-tile workspace written by the gather kernel and the backward MLP kernel
 // (see ns2b_field_workspace_bytes): pre-staged E tiles (fp16 hi | lo, tile layout),
 // their staging exponent, d feature/dx value-major [tile][96][128] fp32, and the
-// scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d feature rows (32) | q (3).
-constexpr int JROWS = 96, SBROWS = 68;
+// scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d feature rows (32) | q (3),
+// and the per-sample inputs of the MLP kernels [tile][6][128] = position | view dir (fp32).
+constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6;
 struct Workspace {
     uint8_t *e_tiles;
     int *e_exp;
     float *jac;
     float *sb;
+    float *xv;
 };
 __host__ __device__ inline size_t ws_tile_bytes() {
-    return 2 * static_cast<size_t>(TEB) + sizeof(int) + (JROWS + SBROWS) * TILE * sizeof(float);
+    return 2 * static_cast<size_t>(TEB) + sizeof(int) + (JROWS + SBROWS + XVROWS) * TILE * sizeof(float);
 }
 __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     uint8_t *b = static_cast<uint8_t *>(base);
@@ -246,6 +265,8 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     b += ntiles * JROWS * TILE * sizeof(float);
     w.sb = reinterpret_cast<float *>(b);
     b += ntiles * SBROWS * TILE * sizeof(float);
+    w.xv = reinterpret_cast<float *>(b);
+    b += ntiles * XVROWS * TILE * sizeof(float);
     w.e_exp = reinterpret_cast<int *>(b);
     return w;
 }
@@ -257,34 +278,33 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
 // quarter k owns blocks k and k+4 of a tile.  Row scalars (the SDF value, the normal)
 // are combined through shared memory.  One elected thread issues all MMAs.
 constexpr int MLP_THREADS = 512;
-constexpr int NWARP = MLP_THREADS / 32;
 
-struct Reducer16 {
-    uint32_t (*red)[2][NWARP];
-    int parity;
-    __device__ void two(float a, float b, int &ea, int &eb) {
-        const int warp = threadIdx.x >> 5;
-        const uint32_t ra = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(a)));
-        const uint32_t rb = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(b)));
-        if ((threadIdx.x & 31) == 0) {
-            red[parity][0][warp] = ra;
-            red[parity][1][warp] = rb;
-        }
-        __syncthreads();
-        uint32_t ma = 0, mb = 0;
-#pragma unroll
-        for (int w = 0; w < NWARP; ++w) {
-            ma = max(ma, red[parity][0][w]);
-            mb = max(mb, red[parity][1][w]);
-        }
-        parity ^= 1;
-        ea = exp_for(__uint_as_float(ma));
-        eb = exp_for(__uint_as_float(mb));
+// Predicted staging exponents.  The exponent a tile is staged with only has to keep its
+// maximum inside fp16's range with the lo parts normal, so instead of a block-wide max
+// before staging (one barrier per phase) each staging point uses the exponent its
+// previous tile ended with (one bit of extra headroom), every warp atomically maxes its
+// |value| into a shared slot, and the value is checked after the publish barrier the
+// phase needs anyway.  A tile whose max left [2^3, 2^15) is restaged with the exact
+// exponent (first tile of a CTA, sudden range changes).  Scaling by 2^e is exact, so
+// the products equal those of an exactly-scaled tile.
+enum Slot { kA1, kCin, kA1c, kA2c, kDlog, kU2, kU1, kDly, kU, kMv, kPv, NSLOT };
+struct PredScale {
+    uint32_t (*mx)[NSLOT];  // [2][NSLOT] block maxima (bits of |v|), tile parity
+    int *pred;              // [NSLOT]
+    int par;
+    __device__ __forceinline__ int guess(int k) const { return pred[k]; }
+    __device__ __forceinline__ void contrib(int k, float m) {
+        const uint32_t w = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+        if ((threadIdx.x & 31) == 0 && w) atomicMax(&mx[par][k], w);
     }
-    __device__ int one(float a) {
-        int ea, eb;
-        two(a, 0.f, ea, eb);
-        return ea;
+    // after the barrier: is e acceptable? (else e <- the exact exponent)
+    __device__ __forceinline__ bool check(int k, int &e) {
+        const float m = __uint_as_float(mx[par][k]);
+        const int ex = exp_for(m);
+        const bool ok = !(m > 0.f) || (e <= ex + 1 && e >= ex - 10);
+        if (!ok) e = ex;
+        if (threadIdx.x == 0 && m > 0.f) pred[k] = ex - 1;
+        return ok;
     }
 };
 
@@ -314,8 +334,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t mbar;   // chain GEMMs of a phase (the next epilogue needs them)
     __shared__ uint64_t mbarw;  // weight-gradient GEMMs (overlap the next epilogue)
+    __shared__ uint64_t mbare;  // bulk DMA of the next E tile
     __shared__ uint32_t tmem_base_s;
-    __shared__ uint32_t red[2][2][NWARP];
+    __shared__ uint32_t slot_mx[2][NSLOT];
+    __shared__ int slot_pred[NSLOT];
     __shared__ uint32_t wmax[5];
     __shared__ int wexp_s[5];
     __shared__ float h2row0[H];
@@ -332,19 +354,31 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     float *gacc = reinterpret_cast<float *>(S.p(GACC));
     if (kBwd)
         for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) gacc[i] = 0.f;
+    if (t < NSLOT) {
+        slot_mx[0][t] = 0u;
+        slot_mx[1][t] = 0u;
+        slot_pred[t] = 0;
+    }
     if (t == 0) {
         umma::mbar_init(&mbar, 1);
         umma::mbar_init(&mbarw, 1);
+        umma::mbar_init(&mbare, 1);
         umma::fence_barrier_init();
     }
     if (warp == 0) umma::tmem_alloc(&tmem_base_s, 512);
     publish();
     const uint32_t tb = tmem_base_s;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    uint32_t phasew = 0;
+    uint32_t phasew = 0, phasee = 0;
     float *xch = reinterpret_cast<float *>(S.p(TZ));  // row-scalar exchange scratch (P1-P2)
     uint32_t phase = 0;
-    Reducer16 R{red, 0};
+    PredScale PS{slot_mx, slot_pred, 1};
+    int eS1;  // |s1| <= max |H2[0]|: one exponent per CTA
+    {
+        float mh = 0.f;
+        for (int j = 0; j < H; ++j) mh = fmaxf(mh, fabsf(h2row0[j]));
+        eS1 = exp_for(mh);
+    }
     const int P = *count;
     const float Pf = (kBwd && eik_count) ? static_cast<float>(*eik_count) : 1.f;
     const int G_H1r = 0, G_H2r = H * (E + 1), G_C1r = G_H2r + NOUT * H, G_C2r = G_C1r + H * CIN,
@@ -353,32 +387,64 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
     const int b0 = qt, b1 = qt + 4;   // my column blocks of 64-wide tiles
     float eik = 0.f;
 
+    // d feature/dx of my quarter's levels of a tile -> registers -> TMEM (loads issued a
+    // phase ahead of the stores so their latency overlaps the epilogue in between)
+    float jv[4][6];
+    auto j_load = [&](int64_t tl) {
+        const float *jt = ws.jac + tl * JROWS * TILE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (4 * qt + i < NA) {
+                const float *jr = jt + 6 * (4 * qt + i) * TILE + r;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) jv[i][k] = jr[k * TILE];
+            }
+    };
+    auto j_store = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (4 * qt + i < NA) {
+                const uint32_t c = my + TM_J + 8 * (4 * qt + i);
+                umma::tmem_st4(c, jv[i][0], jv[i][1], jv[i][2], jv[i][3]);
+                umma::tmem_st2(c + 4, jv[i][4], jv[i][5]);
+            }
+        umma::tmem_st_wait();
+    };
+    // E tile (pre-staged fp16 hi|lo) of the next tile: one bulk DMA into TE once the
+    // tile in TE is dead (after P0's MMA in the forward, after dH1 in the backward)
+    auto e_fetch = [&](int64_t tl) {
+        if (t == 0 && tl * TILE < P) umma::bulk_g2s(S.p(TE), ws.e_tiles + tl * 2 * TEB, 2 * TEB, &mbare);
+    };
+    e_fetch(blockIdx.x);
+    if (static_cast<int64_t>(blockIdx.x) * TILE < P) {
+        j_load(blockIdx.x);
+        j_store();
+    }
+#ifdef NS2B_PHASE_PROF
+    __shared__ long long pacc[64];
+    long long plast = clock64();
+    if (t < 64) pacc[t] = 0;
+    __syncthreads();
+#endif
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
         const int64_t p = base + r;
         const bool valid = p < P;
         const int64_t tile = base / TILE;
-        const float *Jt = ws.jac + tile * JROWS * TILE;
+        PS.par ^= 1;
         float *SBt = ws.sb + tile * SBROWS * TILE;
         // ------------------------------------------------ P0: E tile, J, Z1
-        if (t == 0) {  // next tile of this CTA -> L2 while this one runs
+        if (t == 0) {  // next tile's J -> L2 while this one runs
             const int64_t nt = tile + gridDim.x;
-            if (nt * TILE < P) {
-                umma::prefetch_l2(ws.e_tiles + nt * 2 * TEB, 2 * TEB);
-                umma::prefetch_l2(ws.jac + nt * JROWS * TILE, JROWS * TILE * 4);
-            }
+            if (nt * TILE < P) umma::prefetch_l2(ws.jac + nt * JROWS * TILE, JROWS * TILE * 4);
         }
         // per-sample inputs, issued up front so their latency overlaps P0-P1
-        float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
+        // (position and view direction come coalesced from the gather pass's workspace)
+        const float *xvt = ws.xv + tile * XVROWS * TILE + r;
+        const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
+        const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
         float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f;
         if (valid) {
-            x0 = pos[3 * p];
-            x1 = pos[3 * p + 1];
-            x2 = pos[3 * p + 2];
-            const int rr = ray_ids[p];
-            v0 = static_cast<float>(dirs[3 * rr]);
-            v1 = static_cast<float>(dirs[3 * rr + 1]);
-            v2 = static_cast<float>(dirs[3 * rr + 2]);
             if (kBwd) {
                 gc0 = dl_dc[3 * p];
                 gc1 = dl_dc[3 * p + 1];
@@ -387,30 +453,21 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
         }
         const int eE = ws.e_exp[tile];
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(ws.e_tiles + tile * 2 * TEB);
-            uint4 *dst = reinterpret_cast<uint4 *>(S.p(TE));
-#pragma unroll
-            for (int i = t; i < static_cast<int>(2 * TEB / 16); i += MLP_THREADS) dst[i] = src[i];
-            if (kBwd) {
-#pragma unroll 1
-                for (int l = 4 * qt; l < min(NA, 4 * qt + 4); ++l) {
-                    const float *jr = Jt + 6 * l * TILE + r;
-                    umma::tmem_st4(my + TM_J + 8 * l, jr[0], jr[TILE], jr[2 * TILE], jr[3 * TILE]);
-                    umma::tmem_st2(my + TM_J + 8 * l + 4, jr[4 * TILE], jr[5 * TILE]);
-                }
-                umma::tmem_st_wait();
-            }
-        }
-        publish();
+        const int64_t ntile = tile + gridDim.x;
+        // this tile's J is in TMEM (stored during the previous tile), its E tile in TE
+        PMARK(0);
         if (t == 0) {
+            umma::mbar_wait(&mbare, phasee);
             umma::gemm3(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
             umma::commit(&mbar);
         }
+        phasee ^= 1u;
         wait_mma(&mbar, phase);
+        PMARK(1);
+        if (!kBwd) e_fetch(ntile);
         // ------------------------------------------------ P1: a1, s1 -> Y, JD; SDF value
         uint32_t m1 = 0u;  // my 16 hidden-unit mask bits (blocks b0, b1)
-        int eA1, eS1;
+        int eA1;
         {
             float z[2][8], s1[2][8], ma = 0.f, ms = 0.f, dpart = 0.f;
             const float sc = pow2i(-(eE + eH1));
@@ -433,22 +490,35 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 }
             }
             xch[qt * TILE + r] = dpart;
-            R.two(ma, ms, eA1, eS1);
-            const float sa = pow2i(eA1), ss = pow2i(eS1);
+            (void)ms;
+            eA1 = PS.guess(kA1);
+            PS.contrib(kA1, ma);
+            auto stg = [&](int e) {
+                const float sa = pow2i(e);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], sa);
-                stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], sa);
+            };
+            stg(eA1);
+            const float ss = pow2i(eS1);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
+            publish();
+            if (t < NSLOT) slot_mx[PS.par ^ 1][t] = 0u;  // next tile's slots (last read before this barrier)
+            PMARK(2);
+            if (!PS.check(kA1, eA1)) {
+                stg(eA1);
+                publish();
+                PMARK(3);
             }
         }
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), 4, ID_KK(16), false);
             umma::gemm3(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
+        PMARK(4);
         // ------------------------------------------------ P2: normal, cin -> Zc1
         float y[16], n0, n1, n2, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
         int eCin;
@@ -476,14 +546,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 d0 *= scd;
                 d1 *= scd;
                 float jl[8];
+                umma::tmem_ld8(my + TM_J + 8 * l, jl);
                 if (kBwd) {
-                    umma::tmem_ld8(my + TM_J + 8 * l, jl);
                     SBt[(32 + 2 * l) * TILE + r] = d0;
                     SBt[(33 + 2 * l) * TILE + r] = d1;
-                } else {
-                    const float *jr = Jt + 6 * l * TILE + r;
-#pragma unroll
-                    for (int k = 0; k < 6; ++k) jl[k] = jr[k * TILE];
                 }
                 p0 = fmaf(d0, jl[0], fmaf(d1, jl[3], p0));
                 p1 = fmaf(d0, jl[1], fmaf(d1, jl[4], p1));
@@ -532,7 +598,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) mc = fmaxf(mc, fabsf(blk[k]));
-            eCin = R.one(mc);
+            eCin = PS.guess(kCin);
+            PS.contrib(kCin, mc);
             stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
             if (!kBwd && valid && qt == 0) {
                 sdf_out[p] = d_sdf;
@@ -545,16 +612,25 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
                     for (int o = 1; o < 16; ++o) geo_out[15 * p + o - 1] = y[o];
             }
+            publish();
+            PMARK(5);
+            if (!PS.check(kCin, eCin)) {
+                stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
+                publish();
+                PMARK(6);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), 2, ID_KK(64), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
+        PMARK(7);
         // ------------------------------------------------ P3: a1c -> Zc2
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
+        const bool jnext = ntile * TILE < P;
+        if (!kBwd && jnext) j_load(ntile);
         {
             float z[2][8], m = 0.f;
             const float sc = pow2i(-(eCin + eC1));
@@ -569,17 +645,29 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     m = fmaxf(m, z[i][k]);
                 }
             }
-            eA1c = R.one(m);
-            const float s = pow2i(eA1c);
+            eA1c = PS.guess(kA1c);
+            PS.contrib(kA1c, m);
+            if (!kBwd && jnext) j_store();
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
+            };
+            stg(eA1c);
+            publish();
+            PMARK(8);
+            if (!PS.check(kA1c, eA1c)) {
+                stg(eA1c);
+                publish();
+                PMARK(9);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), 4, ID_KK(64), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
+        PMARK(10);
         // ------------------------------------------------ P4: a2c -> LOG
         {
             float z[2][8], m = 0.f;
@@ -595,17 +683,28 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     m = fmaxf(m, z[i][k]);
                 }
             }
-            eA2c = R.one(m);
-            const float s = pow2i(eA2c);
+            eA2c = PS.guess(kA2c);
+            PS.contrib(kA2c, m);
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], s);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], s);
+            };
+            stg(eA2c);
+            publish();
+            PMARK(11);
+            if (!PS.check(kA2c, eA2c)) {
+                stg(eA2c);
+                publish();
+                PMARK(12);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), 4, ID_KK(16), false);
             umma::commit(&mbar);
         }
         wait_mma(&mbar, phase);
+        PMARK(13);
         // ------------------------------------------------ P5: colours (+ backward start)
         float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;
         if (qt == 0) {
@@ -637,10 +736,17 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 dlog[1] = gc1 * cc1 * (1.f - cc1);
                 dlog[2] = gc2 * cc2 * (1.f - cc2);
             }
-            eD = R.one(fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
+            eD = PS.guess(kDlog);
+            PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
+            publish();
+            PMARK(14);
+            if (!PS.check(kDlog, eD)) {
+                if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
+                publish();
+                PMARK(15);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), 1, ID_KM(64), false);
             umma::commit(&mbar);
@@ -648,6 +754,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
+        PMARK(16);
         // ------------------------------------------------ P6: u2 -> U1, dC2; dC3 fold
         int eU2;
         {
@@ -662,8 +769,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     m = fmaxf(m, fabsf(u[i][k]));
                 }
             }
-            eU2 = R.one(m);
+            eU2 = PS.guess(kU2);
+            PS.contrib(kU2, m);
             wait_mma(&mbarw, phasew);  // dC3 (P5) done
+            PMARK(17);
             float d[8];
             umma::tmem_ld8(my + TM_DC3, d);
             if (lane < 16 && qt == 0) {
@@ -671,11 +780,20 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
                 for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sd;
             }
-            const float s = pow2i(eU2);
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
+            };
+            stg(eU2);
+            publish();
+            PMARK(18);
+            if (!PS.check(kU2, eU2)) {
+                stg(eU2);
+                publish();
+                PMARK(19);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), 4, ID_KM(64), false);
             umma::commit(&mbar);
@@ -683,6 +801,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
+        PMARK(20);
         // ------------------------------------------------ P7: u1 -> DCIN, dC1; dC2 fold
         int eU1;
         {
@@ -697,8 +816,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     m = fmaxf(m, fabsf(u[i][k]));
                 }
             }
-            eU1 = R.one(m);
+            eU1 = PS.guess(kU1);
+            PS.contrib(kU1, m);
             wait_mma(&mbarw, phasew);  // dC2 (P6) done
+            PMARK(21);
             float d[2][8];
             umma::tmem_ld8(my + TM_DC2 + 8 * b0, d[0]);
             umma::tmem_ld8(my + TM_DC2 + 8 * b1, d[1]);
@@ -709,11 +830,20 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
                     for (int k = 0; k < 8; ++k) gacc[G_C2r + jrow * H + 8 * (i ? b1 : b0) + k] += d[i][k] * sd;
             }
-            const float s = pow2i(eU1);
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
+            };
+            stg(eU1);
+            publish();
+            PMARK(22);
+            if (!PS.check(kU1, eU1)) {
+                stg(eU1);
+                publish();
+                PMARK(23);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), 4, ID_KM(32), false);
             umma::commit(&mbar);
@@ -721,6 +851,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
+        PMARK(24);
         // ------------------------------------------------ P8: q, dly -> U, dH2; dC1 fold
         float q0, q1, q2;
         int eDLY;
@@ -762,8 +893,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
                 for (int k = 0; k < 8; ++k) z[i][k] = z[i][k] > 0.f ? z[i][k] * sz : 0.f;
             }
-            eDLY = R.one(m);
+            eDLY = PS.guess(kDly);
+            PS.contrib(kDly, m);
             wait_mma(&mbarw, phasew);  // dC1 (P7) done
+            PMARK(25);
             float d[8];
             umma::tmem_ld8(my + TM_DC1 + 8 * qt, d);
             if (lane < 16) {
@@ -772,12 +905,18 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 for (int k = 0; k < 8; ++k)
                     if (8 * qt + k < CIN) gacc[G_C1r + jrow * CIN + 8 * qt + k] += d[k] * sd;
             }
-            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
             const float sa = pow2i(eA1);
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, z[i], sa);
+            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
+            publish();
+            PMARK(26);
+            if (!PS.check(kDly, eDLY)) {
+                if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
+                publish();
+                PMARK(27);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), 1, ID_KM(64), false);
             umma::commit(&mbar);
@@ -785,6 +924,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
+        PMARK(28);
         // ------------------------------------------------ P9: u, mvec -> DE, PV, dH1; dH2 fold
         int eU, eMV;
         {
@@ -825,8 +965,12 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
-            R.two(mu, mm, eU, eMV);
+            eU = PS.guess(kU);
+            eMV = PS.guess(kMv);
+            PS.contrib(kU, mu);
+            PS.contrib(kMv, mm);
             wait_mma(&mbarw, phasew);  // dH2 (P8) done
+            PMARK(29);
             if (qt < 2) {
                 float d[8];
                 umma::tmem_ld8(my + TM_DH2 + 8 * qt, d);
@@ -839,20 +983,33 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 float d[8];
                 umma::tmem_ld8(my + TM_DH2, d);
             }
-            const float su = pow2i(eU), sm = pow2i(eMV), ss = pow2i(eS1);
+            auto stg = [&](int eu, int emv) {
+                const float su = pow2i(eu), sm = pow2i(emv);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], su);
+                stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
+                if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
+            };
+            stg(eU, eMV);
+            const float ss = pow2i(eS1);
             float s1[8];
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int b = i ? b1 : b0;
-                stage_blk<64>(S, TX, T64B, r, b, u[i], su);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) s1[k] = ((m1 >> (8 * i + k)) & 1u) ? h2row0[8 * b + k] : 0.f;
                 stage_blk<64>(S, TY, T64B, r, b, s1, ss);
             }
-            stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
-            if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
+            publish();
+            PMARK(30);
+            const bool oku = PS.check(kU, eU);
+            const bool okm = PS.check(kMv, eMV);
+            if (!(oku && okm)) {
+                stg(eU, eMV);
+                publish();
+                PMARK(31);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
             umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
@@ -862,8 +1019,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             umma::commit(&mbarw);
         }
         wait_mma(&mbar, phase);
+        PMARK(32);
         // ------------------------------------------------ P10: pvec; scatter inputs; dH1 fold
         int ePV;
+        if (jnext) j_load(ntile);  // next tile's J (TMEM J is dead after P9)
         {
             float pv[2][8], m = 0.f;
             const float sc = pow2i(-(eMV + eH1));
@@ -888,8 +1047,11 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 SBt[65 * TILE + r] = q1;
                 SBt[66 * TILE + r] = q2;
             }
-            ePV = R.one(m);
+            ePV = PS.guess(kPv);
+            PS.contrib(kPv, m);
             wait_mma(&mbarw, phasew);  // dH1 (P9) done
+            PMARK(33);
+            e_fetch(ntile);  // TE is dead too
             const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -905,28 +1067,48 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     }
                 }
             }
-            const float s = pow2i(ePV);
-#pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
             if (qt < 2) {
                 float ones[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) ones[k] = (qt == 0 && k == 0) ? 1.f : 0.f;
                 stage_blk<16>(S, TD, TDB, r, qt, ones, 1.f);
             }
+            if (jnext) j_store();
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
+            };
+            stg(ePV);
+            publish();
+            PMARK(34);
+            if (!PS.check(kPv, ePV)) {
+                stg(ePV);
+                publish();
+                PMARK(35);
+            }
         }
-        publish();
         if (t == 0) {
             umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
             umma::commit(&mbarw);
         }
         wait_mma(&mbarw, phasew);
+        PMARK(36);
         {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
             float d[8];
             umma::tmem_ld8(my + TM_DC3, d);
             if (lane < 16 && qt == 0) gacc[G_H2r + jrow] += d[0] * pow2i(-ePV);
         }
     }
+#ifdef NS2B_PHASE_PROF
+    __syncthreads();
+    if (t == 0 && blockIdx.x == 0) {
+        printf("PHASEPROF kBwd=%d", int(kBwd));
+        for (int i = 0; i < 64; ++i)
+            if (pacc[i]) printf(" %d:%lld", i, pacc[i]);
+        printf("\n");
+    }
+#endif
     if (eik_sum) {
         double v = warp_sum(static_cast<double>(eik));
         if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
@@ -953,7 +1135,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 constexpr int GATHER_BLOCK = TILE;
 
 __global__ void __launch_bounds__(GATHER_BLOCK)
-field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count, Workspace ws) {
+field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
+                    const double *__restrict__ dirs, const int32_t *__restrict__ count, Workspace ws) {
     __shared__ float raw[32][TILE + 1];
     __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
     __shared__ uint32_t red[2][2][4];
@@ -972,11 +1155,15 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t p = tile * TILE + t;
         const bool valid = p < P;
-        float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
         if (valid) {
             x0 = pos[3 * p];
             x1 = pos[3 * p + 1];
             x2 = pos[3 * p + 2];
+            const int rr = ray_ids[p];
+            v0 = static_cast<float>(dirs[3 * rr]);  // field.py:216 (fp32 view dirs)
+            v1 = static_cast<float>(dirs[3 * rr + 1]);
+            v2 = static_cast<float>(dirs[3 * rr + 2]);
         }
         const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
         const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
@@ -1039,6 +1226,15 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
                     jr[5 * TILE] = j12;
                 }
             }
+        }
+        {  // (view-dir loads issued before the level loop)
+            float *xvt = ws.xv + tile * XVROWS * TILE + t;
+            xvt[0] = x0;
+            xvt[TILE] = x1;
+            xvt[2 * TILE] = x2;
+            xvt[3 * TILE] = v0;
+            xvt[4 * TILE] = v1;
+            xvt[5 * TILE] = v2;
         }
         const int eE = R.one(fmax_);
         float row[48];
@@ -1213,7 +1409,8 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
     switch (which) {
     case 0:
-        tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, count, ws);
+        tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
+                                                                                         count, ws);
         return check_launch("field_gather");
     case 1:
         tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
@@ -1244,7 +1441,8 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
-    tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, count, ws);
+    tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
+                                                                                         count, ws);
     if ((rc = check_launch("field_gather"))) return rc;
     tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
         f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,

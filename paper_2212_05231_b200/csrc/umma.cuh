@@ -183,6 +183,18 @@ __device__ __forceinline__ void prefetch_l2(const void *gptr, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
 }
 
+// One-thread bulk DMA global -> shared (TMA engine, no registers); completion is
+// signalled as transaction bytes on `mbar` (arrive + expect_tx by the same thread).
+__device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 // ---------------------------------------------------------------- staging --
 // Byte offset of element (r, c) in a core-matrix tiled tile with C columns.
 __host__ __device__ constexpr uint32_t tile_off(int r, int c, int C) {

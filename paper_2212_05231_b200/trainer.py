@@ -285,7 +285,8 @@ def train_step(state, dataset, time_index=0, batch=None):
     f = params.field_struct(na)
     # K2: gather (features + d feature/dx -> workspace), tcgen05 MLP forward (+ Eikonal sum)
     with _Timer(timers, "field_gather", st):
-        _lib.call("ns2b_field_gather", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(count), P,
+        _lib.call("ns2b_field_gather", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
+                  _lib.ptr(ws.d), _lib.ptr(count), P,
                   _lib.ptr(ws.field_ws), sp)
     with _Timer(timers, "field_mlp_forward", st):
         _lib.call("ns2b_field_mlp_forward", ctypes.byref(f), _lib.ptr(ws.pos32),
