@@ -1262,7 +1262,15 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
 // Consecutive lanes are consecutive samples of a ray; on the coarse levels they often
 // hit the same corner row, so runs of equal rows are pre-summed with a segmented
 // shuffle reduction and only the run's last lane issues the RED.
-constexpr int kAggLevels = 9;
+constexpr int kAggLevels = 9;  // default; NS2B_AGG_LEVELS overrides (tuning)
+static int agg_levels_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NS2B_AGG_LEVELS");
+        v = e ? atoi(e) : kAggLevels;
+    }
+    return v;
+}
 
 __device__ __forceinline__ void seg_red(float *gt, uint32_t row, float a, float b, int lane) {
     const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
@@ -1289,7 +1297,7 @@ __device__ __forceinline__ void red_add_f32x4(float *addr, float a, float b, flo
 
 __global__ void __launch_bounds__(TILE)
 field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count,
-                     const Workspace ws, float *__restrict__ g_tab) {
+                     const Workspace ws, float *__restrict__ g_tab, int agg_levels) {
     __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
     const int t = threadIdx.x, lane = t & 31;
     if (t < NS2B_MAX_LEVELS) {
@@ -1318,14 +1326,22 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
         const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
         const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
         const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+        // per-level inputs, loaded one level ahead
+        float nde0 = 0.f, nde1 = 0.f, njd0 = 0.f, njd1 = 0.f;
+        if (valid) {
+            nde0 = SBt[0];
+            nde1 = SBt[TILE];
+            njd0 = SBt[32 * TILE];
+            njd1 = SBt[33 * TILE];
+        }
 #pragma unroll 1
         for (int l = 0; l < NA; ++l) {
-            float de0 = 0.f, de1 = 0.f, jd0 = 0.f, jd1 = 0.f;
-            if (valid) {
-                de0 = SBt[(2 * l) * TILE];
-                de1 = SBt[(2 * l + 1) * TILE];
-                jd0 = SBt[(32 + 2 * l) * TILE];
-                jd1 = SBt[(33 + 2 * l) * TILE];
+            const float de0 = nde0, de1 = nde1, jd0 = njd0, jd1 = njd1;
+            if (valid && l + 1 < NA) {
+                nde0 = SBt[(2 * l + 2) * TILE];
+                nde1 = SBt[(2 * l + 3) * TILE];
+                njd0 = SBt[(34 + 2 * l) * TILE];
+                njd1 = SBt[(35 + 2 * l) * TILE];
             }
             const LevelInfo lv = lvs[l].lv;
             const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
@@ -1354,13 +1370,14 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
                     b[ox] = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
                     row[ox] = corner_row(lv, cx + ox, cy + oy, cz + oz);
                 }
-                if (l < kAggLevels) {  // coarse levels: runs of equal rows along the rays
+                if (l < agg_levels) {  // coarse levels: runs of equal rows along the rays
                     seg_red(gt, row[0], a[0], b[0], lane);
                     seg_red(gt, row[1], a[1], b[1], lane);
                 } else if (valid) {
                     if ((row[0] ^ row[1]) == 1u) {  // both corners in one 16-B row pair
-                        const int lo = row[0] & 1u;
-                        red_add_f32x4(gt + 2 * (row[0] & ~1u), a[lo], b[lo], a[lo ^ 1], b[lo ^ 1]);
+                        const bool sw = row[0] & 1u;
+                        red_add_f32x4(gt + 2 * (row[0] & ~1u), sw ? a[1] : a[0], sw ? b[1] : b[0],
+                                      sw ? a[0] : a[1], sw ? b[0] : b[1]);
                     } else {
                         red_add_f32x2(gt + 2 * row[0], a[0], b[0]);
                         red_add_f32x2(gt + 2 * row[1], a[1], b[1]);
@@ -1425,7 +1442,7 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
         return check_launch("field_mlp_backward");
     default:
         tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
-                                                                                       grad_tables);
+                                                                                       grad_tables, tc::agg_levels_env());
         return check_launch("field_scatter");
     }
 }
@@ -1468,7 +1485,7 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
         static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
     if ((rc = check_launch("field_backward_tc"))) return rc;
     tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
-                                                                                   grad_tables);
+                                                                                   grad_tables, tc::agg_levels_env());
     return check_launch("field_scatter");
 }
 
