@@ -128,7 +128,7 @@ class ClockSampler:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,clocks.mem")
 
     def __init__(self, gpu_index=0):
         self.proc = None
@@ -157,8 +157,12 @@ class ClockSampler:
         reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
                           if r[5 + i].strip() == "Active"})
         load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        mem = [float(r[9]) for r in rows if len(r) >= 10 and r[9].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if len(r) >= 9 and r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(load) if load else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "mem_mhz": statistics.median(mem) if mem else None,
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ CPU ---
@@ -174,7 +178,8 @@ def cpu_oracle_rate(wl, rays_sample, steps=1, threads=None):
     from paper_2212_05231_b200 import scene_io
 
     cfg = otrain.TrainConfig(batch_size=rays_sample, num_levels=wl["levels"],
-                             table_size=wl["table"], seed=0, level_init=wl["levels"])
+                             table_size=wl["table"], seed=0, level_init=wl["levels"],
+                             occupancy_update_every=1 << 30)
     st = otrain.TrainState.create(cfg)
     # occupancy from the SAL init (the frozen grid of the GPU run), computed on the CPU
     orender.update_occupancy(st.occ, st.params, wl["levels"])
@@ -272,7 +277,8 @@ def run_ours(args, wl):
     ds = make_dataset(wl, dev)
     m_global = wl["rays"] * world  # weak scaling: each GPU keeps 2^18 rays
     cfg = trainer.TrainConfig(batch_size=m_global, num_levels=wl["levels"], table_size=wl["table"],
-                              seed=0, level_init=wl["levels"], total_steps=15000)
+                              seed=0, level_init=wl["levels"], total_steps=15000,
+                              occupancy_update_every=1 << 30)  # frozen: a fixed workload per step
     st = trainer.TrainState.create(cfg, dp=dp)
     renderer.update_occupancy(st.occ, st.params, wl["levels"])  # step-0 refresh, then frozen
     st.step = 1
@@ -321,8 +327,21 @@ def run_ours(args, wl):
     # end-to-end leg through the public API with host batches
     if os.environ.get("NS2B_BENCH_DEBUG"):
         st.timers = {}
+        clk2 = ClockSampler(torch.cuda.current_device())
+        clk2.path = clk2.path.with_suffix(".e2e.csv")
+        clk2.start()
     ms_e2e, _, _, wall_e2e = timed(host=True)
     if os.environ.get("NS2B_BENCH_DEBUG"):
+        print(json.dumps({"clocks_dev": clk, "clocks_e2e": clk2.stop()}), file=sys.stderr)
+        st.timers = {}
+        ms_dev2, _, reps2, _ = timed(host=False)
+        print(json.dumps({"P_dev": [r.sample_count for r in reps], "loss_dev": [r.total for r in reps],
+                          "P_again": [r.sample_count for r in reps2],
+                          "loss_again": [r.total for r in reps2]}), file=sys.stderr)
+        print(json.dumps({"ms_dev_again": ms_dev2, "kernels": {
+            k: round(statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:]), 3)
+            for k, v in st.timers.items()}}), file=sys.stderr)
+        st.timers = {}
         dbg = {k: round(statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:]), 3)
                for k, v in st.timers.items()}
         print(json.dumps({"debug_e2e_kernels": dbg, "ms_e2e": ms_e2e, "wall_e2e": wall_e2e,

@@ -67,16 +67,19 @@ __device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
 }
 
+// try_wait suspends the warp until the phase completes or this many ns pass, so the
+// waiting warps do not spin on the issue slots the MMA-issuing warp needs.
+constexpr uint32_t kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
     uint32_t addr = smem_u32(mbar);
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@P1 bra DONE;\n\t"
         "bra LAB_WAIT;\n\t"
         "DONE:\n\t}\n" ::"r"(addr),
-        "r"(parity));
+        "r"(parity), "r"(kSuspendNs));
 }
 
 __device__ __forceinline__ void fence_barrier_init() {
