@@ -363,13 +363,15 @@ def run_ours(args, wl):
     #            d feature/dx 384 B, fp32 position + view dir 24 B)
     #   scatter: 8 corners x L float2 REDs (8 B each) + 32 B of inputs
     #   MLP fwd: 11,520 MAC (SDF 36x64, 64x16, j_d 64x36; colour 25x64, 64x64, 64x3)
-    #   MLP bwd: 34,624 MAC (forward recompute + input cotangents + weight gradients,
-    #            incl. the Theorem-1 terms) -- algorithmic dims, not the 3x split
+    #   MLP bwd: 23,104 MAC (input cotangents 5,888 colour + 3,328 SDF, weight gradients
+    #            5,888 + 3,328, Theorem-1 pvec + dH1 second term + dH2[0] 4,672) -- the
+    #            forward is not recomputed (its staged tiles are read back); algorithmic
+    #            dims, not the 3x split.  fwd + bwd = 34,624 MAC = SURVEY 8(d)'s ~34.9k.
     work = {
         "field_gather": ("hbm", Pl * (8 * 2 * 4 * L + 12 + 28 + 600), "GB/s"),
         "field_scatter": ("hbm", Pl * (8 * 8 * L + 32), "GB/s"),
         "field_mlp_forward": ("tensor", Pl * 2 * 11520, "TFLOP/s"),
-        "field_mlp_backward": ("tensor", Pl * 2 * 34624, "TFLOP/s"),
+        "field_mlp_backward": ("tensor", Pl * 2 * 23104, "TFLOP/s"),
         "composite": ("hbm", Pl * 100, "GB/s"),
     }
     kern = {}

@@ -65,21 +65,27 @@ constexpr uint32_t TCB = TILE * 32 * 2;
 constexpr uint32_t TD = TC + 2 * TCB;                 // 128 x 16
 constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
-constexpr uint32_t GACC = TEND;                       // fp32 gradient accumulator (bwd)
-constexpr int GACC_FLOATS = 9216;
+constexpr uint32_t TW = TEND;                         // 128 x 64 (backward: DMA'd A2c / A1)
 constexpr uint32_t SMEM_FWD = TEND;
-constexpr uint32_t SMEM_BWD = GACC + GACC_FLOATS * 4;
+constexpr uint32_t SMEM_BWD = TW + 2 * T64B;
 
-// TMEM columns (512 allocated)
-constexpr uint32_t TM_DC2 = 0;    // 64: dC2 acc; later mvec scratch (32) and dH1b acc (48)
-constexpr uint32_t TM_DC1 = 64;   // 32
-constexpr uint32_t TM_DC3 = 96;   // 16: dC3^T acc; later dPV acc
-constexpr uint32_t TM_DH2 = 112;  // 16
-constexpr uint32_t TM_DH1 = 128;  // 48: dH1a acc
-constexpr uint32_t TM_J = 176;    // 16 levels x 8: [dfeat/dx (6) | j_d feature pair (2)]
+// TMEM columns (512 allocated).  Forward:
+constexpr uint32_t TM_J = 176;    // 16 levels x 8: [dfeat/dx (6) | 2 spare]
 constexpr uint32_t TM_Z1 = 304;   // 64
-constexpr uint32_t TM_SA = 368;   // 64 chain slot A (P0: raw feature scratch)
+constexpr uint32_t TM_SA = 368;   // 64 chain slot A
 constexpr uint32_t TM_SB = 432;   // 64 chain slot B
+// Backward: weight-gradient accumulators (M = 64 rows in lanes 0-15 of each quadrant),
+// accumulated across tiles while their scale exponent is unchanged
+constexpr uint32_t TB_DC2 = 0;     // 64
+constexpr uint32_t TB_DC1 = 64;    // 32
+constexpr uint32_t TB_DC3 = 96;    // 16 (3 used)
+constexpr uint32_t TB_DH2 = 112;   // 16
+constexpr uint32_t TB_DH1A = 128;  // 48: U^T E
+constexpr uint32_t TB_DH1B = 176;  // 48: S1^T MV (Theorem 1)
+constexpr uint32_t TB_DPV = 224;   // 16 (1 used): PV^T 1 (Theorem 1, layer 2)
+constexpr uint32_t TB_J = 240;     // 128
+constexpr uint32_t TB_SA = 368;    // 64
+constexpr uint32_t TB_SB = 432;    // 64
 
 constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
@@ -240,27 +246,45 @@ struct LevelSm {
     float pad;
 };
 
-// Per-tile workspace written by the gather kernel and the backward MLP kernel
-// (see ns2b_field_workspace_bytes): pre-staged E tiles (fp16 hi | lo, tile layout),
-// their staging exponent, d feature/dx value-major [tile][96][128] fp32, and the
-// scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d feature rows (32) | q (3),
-// and the per-sample inputs of the MLP kernels [tile][6][128] = position | view dir (fp32).
-constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6;
+// Per-tile workspace (see ns2b_field_workspace_bytes):
+//   gather  -> pre-staged E tiles (fp16 hi | lo, UMMA tile layout) + exponent, d feature/dx
+//              value-major [tile][96][128] fp32, position | view dir [tile][6][128] fp32;
+//   MLP fwd -> its staged operand tiles A1 | CIN | A1c | A2c (fp16 hi | lo) + exponents,
+//              ReLU masks [tile][4][128] (uint2: m1 | mc1 << 16, mc2 of a column quarter),
+//              normal | colour [tile][6][128] fp32, j_d feature rows (into the sb block);
+//   MLP bwd -> scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d rows (32) | q (3).
+// The backward therefore never recomputes the forward: it DMAs the forward's tiles.
+constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6, NCROWS = 6;
+constexpr uint32_t FW_A1 = 0, FW_CIN = 2 * T64B, FW_A1C = FW_CIN + 2 * TCB, FW_A2C = FW_A1C + 2 * T64B,
+                   FWB = FW_A2C + 2 * T64B;
 struct Workspace {
     uint8_t *e_tiles;
     int *e_exp;
     float *jac;
     float *sb;
     float *xv;
+    uint8_t *fw_tiles;
+    int4 *fw_exp;
+    uint2 *fw_mask;
+    float *fw_nc;
 };
 __host__ __device__ inline size_t ws_tile_bytes() {
-    return 2 * static_cast<size_t>(TEB) + sizeof(int) + (JROWS + SBROWS + XVROWS) * TILE * sizeof(float);
+    return 2 * static_cast<size_t>(TEB) + FWB + sizeof(int4) + sizeof(int) + 4 * TILE * sizeof(uint2) +
+           (JROWS + SBROWS + XVROWS + NCROWS) * TILE * sizeof(float);
 }
 __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     uint8_t *b = static_cast<uint8_t *>(base);
     Workspace w;
     w.e_tiles = b;
     b += ntiles * 2 * static_cast<size_t>(TEB);
+    w.fw_tiles = b;
+    b += ntiles * static_cast<size_t>(FWB);
+    w.fw_exp = reinterpret_cast<int4 *>(b);
+    b += ntiles * sizeof(int4);
+    w.fw_mask = reinterpret_cast<uint2 *>(b);
+    b += ntiles * 4 * TILE * sizeof(uint2);
+    w.fw_nc = reinterpret_cast<float *>(b);
+    b += ntiles * NCROWS * TILE * sizeof(float);
     w.jac = reinterpret_cast<float *>(b);
     b += ntiles * JROWS * TILE * sizeof(float);
     w.sb = reinterpret_cast<float *>(b);
@@ -297,13 +321,17 @@ struct PredScale {
         const uint32_t w = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
         if ((threadIdx.x & 31) == 0 && w) atomicMax(&mx[par][k], w);
     }
-    // after the barrier: is e acceptable? (else e <- the exact exponent)
+    // after the barrier: is e acceptable?  Otherwise e <- the exact exponent less one
+    // (max in [2^12, 2^13)), which also becomes the new prediction.  Accepted exponents
+    // stay (sticky), so the weight-gradient accumulators keep one scale across tiles.
     __device__ __forceinline__ bool check(int k, int &e) {
         const float m = __uint_as_float(mx[par][k]);
         const int ex = exp_for(m);
         const bool ok = !(m > 0.f) || (e <= ex + 1 && e >= ex - 10);
-        if (!ok) e = ex;
-        if (threadIdx.x == 0 && m > 0.f) pred[k] = ex - 1;
+        if (!ok) {
+            e = ex - 1;
+            if (threadIdx.x == 0) pred[k] = e;
+        }
         return ok;
     }
 };
@@ -322,73 +350,72 @@ __device__ __forceinline__ void stage_blk(const Smem &s, uint32_t off, uint32_t 
     *reinterpret_cast<uint4 *>(s.p(off + part) + o) = l;
 }
 
-template <bool kBwd>
-__global__ void __launch_bounds__(MLP_THREADS, 1)
-field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
-                const double *__restrict__ dirs, const int32_t *__restrict__ count,
-                float *__restrict__ sdf_out, float *__restrict__ col_out, float *__restrict__ nrm_out,
-                float *__restrict__ geo_out, double *__restrict__ eik_sum,
-                const float *__restrict__ dl_dc, const float *__restrict__ dl_dsdf,
-                const float *__restrict__ dl_dn_extra, float eik_w, const int64_t *__restrict__ eik_count,
-                float *__restrict__ g_sdf, float *__restrict__ g_color, Workspace ws) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ uint64_t mbar;   // chain GEMMs of a phase (the next epilogue needs them)
-    __shared__ uint64_t mbarw;  // weight-gradient GEMMs (overlap the next epilogue)
-    __shared__ uint64_t mbare;  // bulk DMA of the next E tile
-    __shared__ uint32_t tmem_base_s;
-    __shared__ uint32_t slot_mx[2][NSLOT];
-    __shared__ int slot_pred[NSLOT];
-    __shared__ uint32_t wmax[5];
-    __shared__ int wexp_s[5];
-    __shared__ float h2row0[H];
-    const Smem S{smem_raw};
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int qd = warp & 3, qt = warp >> 2;        // TMEM lane quadrant, column quarter
-    const int r = 32 * qd + lane;                    // sample row in the tile
-    const int E = 3 + 2 * f.L;
-    const int NA = f.n_active;
+// Common per-CTA setup of both MLP kernels: weight tiles, H2 row 0, barriers, TMEM.
+struct MlpShared {
+    uint32_t tmem_base;
+    uint32_t slot_mx[2][NSLOT];
+    int slot_pred[NSLOT];
+    uint32_t wmax[5];
+    int wexp[5];
+    float h2row0[H];
+};
 
-    if (t < H) h2row0[t] = f.sdf_w[H * (E + 1) + t];
-    load_weight_tiles(S, f, wmax, wexp_s);
-    const int eH1 = wexp_s[0], eH2 = wexp_s[1], eC1 = wexp_s[2], eC2 = wexp_s[3], eC3 = wexp_s[4];
-    float *gacc = reinterpret_cast<float *>(S.p(GACC));
-    if (kBwd)
-        for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) gacc[i] = 0.f;
+__device__ __forceinline__ void mlp_setup(const Smem &S, const FieldDev &f, MlpShared &sh, uint64_t *bars, int nbars) {
+    const int t = threadIdx.x;
+    const int E = 3 + 2 * f.L;
+    if (t < H) sh.h2row0[t] = f.sdf_w[H * (E + 1) + t];
+    load_weight_tiles(S, f, sh.wmax, sh.wexp);
     if (t < NSLOT) {
-        slot_mx[0][t] = 0u;
-        slot_mx[1][t] = 0u;
-        slot_pred[t] = 0;
+        sh.slot_mx[0][t] = 0u;
+        sh.slot_mx[1][t] = 0u;
+        sh.slot_pred[t] = 0;
     }
     if (t == 0) {
-        umma::mbar_init(&mbar, 1);
-        umma::mbar_init(&mbarw, 1);
-        umma::mbar_init(&mbare, 1);
+        for (int i = 0; i < nbars; ++i) umma::mbar_init(bars + i, 1);
         umma::fence_barrier_init();
     }
-    if (warp == 0) umma::tmem_alloc(&tmem_base_s, 512);
+    if ((t >> 5) == 0) umma::tmem_alloc(&sh.tmem_base, 512);
     publish();
-    const uint32_t tb = tmem_base_s;
+}
+
+// |s1| <= max |H2[0]|: one staging exponent per CTA
+__device__ __forceinline__ int s1_exponent(const float *h2row0) {
+    float mh = 0.f;
+    for (int j = 0; j < H; ++j) mh = fmaxf(mh, fabsf(h2row0[j]));
+    return exp_for(mh);
+}
+
+// ---------------------------------------------------------------------------
+// MLP forward (field.py:208-244): per tile P0 Z1 = E H1^T; P1 a1 -> Y = A1 H2^T (SDF
+// value in fp32 FMAs), JD = S1 H1 (j_d); P2 normal n = j_d J, cin = [x, n, v, y] ->
+// Zc1; P3 Zc2; P4 logits; P5 colours.  Every staged operand tile the backward needs (A1,
+// CIN, A1c, A2c) leaves by bulk DMA to the workspace, with the ReLU masks, n and c.
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restrict__ sdf_out,
+                 float *__restrict__ col_out, float *__restrict__ nrm_out, float *__restrict__ geo_out,
+                 double *__restrict__ eik_sum, Workspace ws) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bars[2];  // [0] chain MMAs, [1] E-tile DMA
+    __shared__ MlpShared sh;
+    uint64_t *mbar = bars, *mbare = bars + 1;
+    const Smem S{smem_raw};
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int qd = warp & 3, qt = warp >> 2;  // TMEM lane quadrant, column quarter
+    const int r = 32 * qd + lane;              // sample row in the tile
+    const int NA = f.n_active;
+    mlp_setup(S, f, sh, bars, 2);
+    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
+    const float *h2row0 = sh.h2row0;
+    const uint32_t tb = sh.tmem_base;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    uint32_t phasew = 0, phasee = 0;
     float *xch = reinterpret_cast<float *>(S.p(TZ));  // row-scalar exchange scratch (P1-P2)
-    uint32_t phase = 0;
-    PredScale PS{slot_mx, slot_pred, 1};
-    int eS1;  // |s1| <= max |H2[0]|: one exponent per CTA
-    {
-        float mh = 0.f;
-        for (int j = 0; j < H; ++j) mh = fmaxf(mh, fabsf(h2row0[j]));
-        eS1 = exp_for(mh);
-    }
+    uint32_t phase = 0, phasee = 0;
+    PredScale PS{sh.slot_mx, sh.slot_pred, 1};
+    const int eS1 = s1_exponent(h2row0);
     const int P = *count;
-    const float Pf = (kBwd && eik_count) ? static_cast<float>(*eik_count) : 1.f;
-    const int G_H1r = 0, G_H2r = H * (E + 1), G_C1r = G_H2r + NOUT * H, G_C2r = G_C1r + H * CIN,
-              G_C3r = G_C2r + H * H;
-    const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
-    const int b0 = qt, b1 = qt + 4;   // my column blocks of 64-wide tiles
+    const int b0 = qt, b1 = qt + 4;  // my column blocks of 64-wide tiles
     float eik = 0.f;
 
-    // d feature/dx of my quarter's levels of a tile -> registers -> TMEM (loads issued a
-    // phase ahead of the stores so their latency overlaps the epilogue in between)
     float jv[4][6];
     auto j_load = [&](int64_t tl) {
         const float *jt = ws.jac + tl * JROWS * TILE;
@@ -410,66 +437,44 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
         umma::tmem_st_wait();
     };
-    // E tile (pre-staged fp16 hi|lo) of the next tile: one bulk DMA into TE once the
-    // tile in TE is dead (after P0's MMA in the forward, after dH1 in the backward)
     auto e_fetch = [&](int64_t tl) {
-        if (t == 0 && tl * TILE < P) umma::bulk_g2s(S.p(TE), ws.e_tiles + tl * 2 * TEB, 2 * TEB, &mbare);
+        if (t == 0 && tl * TILE < P) umma::bulk_g2s(S.p(TE), ws.e_tiles + tl * 2 * TEB, 2 * TEB, mbare);
     };
     e_fetch(blockIdx.x);
     if (static_cast<int64_t>(blockIdx.x) * TILE < P) {
         j_load(blockIdx.x);
         j_store();
     }
-#ifdef NS2B_PHASE_PROF
-    __shared__ long long pacc[64];
-    long long plast = clock64();
-    if (t < 64) pacc[t] = 0;
-    __syncthreads();
-#endif
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
         const int64_t p = base + r;
         const bool valid = p < P;
         const int64_t tile = base / TILE;
+        const int64_t ntile = tile + gridDim.x;
         PS.par ^= 1;
         float *SBt = ws.sb + tile * SBROWS * TILE;
-        // ------------------------------------------------ P0: E tile, J, Z1
-        if (t == 0) {  // next tile's J -> L2 while this one runs
-            const int64_t nt = tile + gridDim.x;
-            if (nt * TILE < P) umma::prefetch_l2(ws.jac + nt * JROWS * TILE, JROWS * TILE * 4);
-        }
-        // per-sample inputs, issued up front so their latency overlaps P0-P1
-        // (position and view direction come coalesced from the gather pass's workspace)
+        uint8_t *fwt = ws.fw_tiles + tile * static_cast<int64_t>(FWB);
+        float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
+        if (t == 0 && ntile * TILE < P) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
         const float *xvt = ws.xv + tile * XVROWS * TILE + r;
         const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
         const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
-        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f;
-        if (valid) {
-            if (kBwd) {
-                gc0 = dl_dc[3 * p];
-                gc1 = dl_dc[3 * p + 1];
-                gc2 = dl_dc[3 * p + 2];
-                gd = dl_dsdf[p];
-            }
-        }
         const int eE = ws.e_exp[tile];
-        const int64_t ntile = tile + gridDim.x;
-        // this tile's J is in TMEM (stored during the previous tile), its E tile in TE
-        PMARK(0);
+        // ------------------------------------------------ P0: Z1 = E H1^T
         if (t == 0) {
-            umma::mbar_wait(&mbare, phasee);
+            umma::bulk_wait_read();  // the previous tile's tile stores have left smem
+            umma::mbar_wait(mbare, phasee);
             umma::gemm3(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
-            umma::commit(&mbar);
+            umma::commit(mbar);
         }
         phasee ^= 1u;
-        wait_mma(&mbar, phase);
-        PMARK(1);
-        if (!kBwd) e_fetch(ntile);
+        wait_mma(mbar, phase);
+        e_fetch(ntile);
         // ------------------------------------------------ P1: a1, s1 -> Y, JD; SDF value
         uint32_t m1 = 0u;  // my 16 hidden-unit mask bits (blocks b0, b1)
         int eA1;
         {
-            float z[2][8], s1[2][8], ma = 0.f, ms = 0.f, dpart = 0.f;
+            float z[2][8], s1[2][8], ma = 0.f, dpart = 0.f;
             const float sc = pow2i(-(eE + eH1));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -483,14 +488,12 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     z[i][k] = a;
                     s1[i][k] = on ? h2row0[8 * b + k] : 0.f;
                     ma = fmaxf(ma, a);
-                    ms = fmaxf(ms, fabsf(s1[i][k]));
                     // d = H2[0] a1 in fp32 FMAs: a cancelling sum the NeuS alpha
                     // differentiates along the ray (the MMA accumulator truncates)
                     dpart = fmaf(h2row0[8 * b + k], a, dpart);
                 }
             }
             xch[qt * TILE + r] = dpart;
-            (void)ms;
             eA1 = PS.guess(kA1);
             PS.contrib(kA1, ma);
             auto stg = [&](int e) {
@@ -503,26 +506,24 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
             publish();
-            if (t < NSLOT) slot_mx[PS.par ^ 1][t] = 0u;  // next tile's slots (last read before this barrier)
-            PMARK(2);
+            if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;  // next tile's slots (last read before this barrier)
             if (!PS.check(kA1, eA1)) {
                 stg(eA1);
                 publish();
-                PMARK(3);
             }
         }
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), 4, ID_KK(16), false);
             umma::gemm3(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
-            umma::commit(&mbar);
+            umma::commit(mbar);
+            umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
         }
-        wait_mma(&mbar, phase);
-        PMARK(4);
+        wait_mma(mbar, phase);
         // ------------------------------------------------ P2: normal, cin -> Zc1
-        float y[16], n0, n1, n2, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
         int eCin;
         {
+            float y[16];
             umma::tmem_ld8(my + TM_SB, *reinterpret_cast<float(*)[8]>(y));
             umma::tmem_ld8(my + TM_SB + 8, *reinterpret_cast<float(*)[8]>(y + 8));
             const float scy = pow2i(-(eA1 + eH2));
@@ -547,10 +548,8 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 d1 *= scd;
                 float jl[8];
                 umma::tmem_ld8(my + TM_J + 8 * l, jl);
-                if (kBwd) {
-                    SBt[(32 + 2 * l) * TILE + r] = d0;
-                    SBt[(33 + 2 * l) * TILE + r] = d1;
-                }
+                SBt[(32 + 2 * l) * TILE + r] = d0;  // j_d feature rows for the scatter (Eq. 9)
+                SBt[(33 + 2 * l) * TILE + r] = d1;
                 p0 = fmaf(d0, jl[0], fmaf(d1, jl[3], p0));
                 p1 = fmaf(d0, jl[1], fmaf(d1, jl[4], p1));
                 p2 = fmaf(d0, jl[2], fmaf(d1, jl[5], p2));
@@ -560,30 +559,20 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             xch[(3 * qt + 1) * TILE + r] = p1;
             xch[(3 * qt + 2) * TILE + r] = p2;
             __syncthreads();
-            n0 = xch[r] + xch[3 * TILE + r] + xch[6 * TILE + r] + xch[9 * TILE + r];
-            n1 = xch[TILE + r] + xch[4 * TILE + r] + xch[7 * TILE + r] + xch[10 * TILE + r];
-            n2 = xch[2 * TILE + r] + xch[5 * TILE + r] + xch[8 * TILE + r] + xch[11 * TILE + r];
+            const float n0 = xch[r] + xch[3 * TILE + r] + xch[6 * TILE + r] + xch[9 * TILE + r];
+            const float n1 = xch[TILE + r] + xch[4 * TILE + r] + xch[7 * TILE + r] + xch[10 * TILE + r];
+            const float n2 = xch[2 * TILE + r] + xch[5 * TILE + r] + xch[8 * TILE + r] + xch[11 * TILE + r];
             const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
             if (valid && qt == 0) eik += (nn - 1.f) * (nn - 1.f);
-            if (kBwd && valid) {
-                if (dl_dn_extra) {
-                    gn0 = dl_dn_extra[3 * p];
-                    gn1 = dl_dn_extra[3 * p + 1];
-                    gn2 = dl_dn_extra[3 * p + 2];
-                }
-                if (eik_w != 0.f) {  // trainer.py:229-235 (fp32, numpy's order)
-                    const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
-                    gn0 += coef * n0 / Pf;
-                    gn1 += coef * n1 / Pf;
-                    gn2 += coef * n2 / Pf;
-                }
-            }
             // cin = [x, n, v, y] (field.py:237-239); quarter k stages block k of the 32
             float blk[8];
             float mc = 0.f;
             if (qt == 0) {
                 blk[0] = x0; blk[1] = x1; blk[2] = x2; blk[3] = n0;
                 blk[4] = n1; blk[5] = n2; blk[6] = v0; blk[7] = v1;
+                nct[0] = n0;
+                nct[TILE] = n1;
+                nct[2 * TILE] = n2;
             } else if (qt == 1) {
                 blk[0] = v2;
 #pragma unroll
@@ -601,7 +590,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             eCin = PS.guess(kCin);
             PS.contrib(kCin, mc);
             stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
-            if (!kBwd && valid && qt == 0) {
+            if (valid && qt == 0) {
                 sdf_out[p] = d_sdf;
                 if (nrm_out) {
                     nrm_out[3 * p] = n0;
@@ -613,24 +602,22 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                     for (int o = 1; o < 16; ++o) geo_out[15 * p + o - 1] = y[o];
             }
             publish();
-            PMARK(5);
             if (!PS.check(kCin, eCin)) {
                 stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
                 publish();
-                PMARK(6);
             }
         }
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), 2, ID_KK(64), false);
-            umma::commit(&mbar);
+            umma::commit(mbar);
+            umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
         }
-        wait_mma(&mbar, phase);
-        PMARK(7);
+        wait_mma(mbar, phase);
         // ------------------------------------------------ P3: a1c -> Zc2
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
         const bool jnext = ntile * TILE < P;
-        if (!kBwd && jnext) j_load(ntile);
+        if (jnext) j_load(ntile);
         {
             float z[2][8], m = 0.f;
             const float sc = pow2i(-(eCin + eC1));
@@ -647,27 +634,26 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
             eA1c = PS.guess(kA1c);
             PS.contrib(kA1c, m);
-            if (!kBwd && jnext) j_store();
+            if (jnext) j_store();
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
             };
             stg(eA1c);
+            if (t == 0) umma::bulk_wait_read();  // A1 has left TX before P4 restages it
             publish();
-            PMARK(8);
             if (!PS.check(kA1c, eA1c)) {
                 stg(eA1c);
                 publish();
-                PMARK(9);
             }
         }
         if (t == 0) {
             umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), 4, ID_KK(64), false);
-            umma::commit(&mbar);
+            umma::commit(mbar);
+            umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
         }
-        wait_mma(&mbar, phase);
-        PMARK(10);
+        wait_mma(mbar, phase);
         // ------------------------------------------------ P4: a2c -> LOG
         {
             float z[2][8], m = 0.f;
@@ -692,46 +678,263 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             };
             stg(eA2c);
             publish();
-            PMARK(11);
             if (!PS.check(kA2c, eA2c)) {
                 stg(eA2c);
                 publish();
-                PMARK(12);
             }
         }
         if (t == 0) {
             umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), 4, ID_KK(16), false);
-            umma::commit(&mbar);
+            umma::commit(mbar);
+            umma::bulk_s2g(fwt + FW_A2C, S.p(TX), 2 * T64B);
+            ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
-        wait_mma(&mbar, phase);
-        PMARK(13);
-        // ------------------------------------------------ P5: colours (+ backward start)
-        float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;
-        if (qt == 0) {
+        ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ P5: colours
+        {
             float lg[4];
-            umma::tmem_ld4(my + TM_SA, lg);
-            const float sc = pow2i(-(eA2c + eC3));
-            cc0 = sigmoid_f(lg[0] * sc);
-            cc1 = sigmoid_f(lg[1] * sc);
-            cc2 = sigmoid_f(lg[2] * sc);
-        } else {
-            float lg[4];
-            umma::tmem_ld4(my + TM_SA, lg);  // keep the warp-collective load uniform
-        }
-        if (!kBwd) {
-            if (valid && qt == 0) {
-                col_out[3 * p] = cc0;
-                col_out[3 * p + 1] = cc1;
-                col_out[3 * p + 2] = cc2;
+            umma::tmem_ld4(my + TM_SA, lg);  // (warp-collective; quarter 0 uses it)
+            if (qt == 0) {
+                const float sc = pow2i(-(eA2c + eC3));
+                const float cc0 = sigmoid_f(lg[0] * sc), cc1 = sigmoid_f(lg[1] * sc), cc2 = sigmoid_f(lg[2] * sc);
+                nct[3 * TILE] = cc0;
+                nct[4 * TILE] = cc1;
+                nct[5 * TILE] = cc2;
+                if (valid) {
+                    col_out[3 * p] = cc0;
+                    col_out[3 * p + 1] = cc1;
+                    col_out[3 * p + 2] = cc2;
+                }
             }
-            continue;
         }
+    }
+    if (eik_sum) {
+        double v = warp_sum(static_cast<double>(eik));
+        if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
+    }
+    if (t == 0) umma::bulk_wait_all();
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tb, 512);
+}
+
+// ---------------------------------------------------------------------------
+// MLP backward (field.py:272-331, relu_mlp.py:132-216) from the forward's stored tiles:
+//   B0 dlog = dL/dc c(1-c) -> U2 = DLOG C3,           dC3 += A2c^T DLOG
+//   B1 u2 = U2 . mc2       -> U1 = U2 C2,             dC2 += U2^T A1c
+//   B2 u1 = U1 . mc1       -> DCIN = U1 C1,           dC1 += U1^T CIN
+//   B3 q, dly              -> U = DLY H2,             dH2 += A1^T DLY
+//   B4 u = U . m1, mvec = [J q, q] -> DE = U H1, PV = MV H1^T;  dH1 += U^T E + S1^T MV
+//   B5 dH2[0] += PV^T 1 (Theorem 1); DE and q -> the scatter's inputs.
+// The forward's tiles arrive by bulk DMA (A2c, A1 -> TW; A1c -> TZ; CIN -> TC; E -> TE),
+// each issued as soon as its buffer's last reader has retired.  Weight-gradient GEMMs
+// run behind the chain GEMMs in the in-order MMA pipe; only B4's and B5's are awaited.  Weight gradients
+// accumulate in TMEM across tiles while their operand exponents stay the same (sticky
+// predictions), and are folded into global memory every kFoldTiles tiles, when an
+// exponent changes, and at the end.
+constexpr int kFoldTiles = 8;
+enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, aPv, NACC };
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
+                 const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
+                 const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
+                 Workspace ws) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // [0] chain MMAs, [1] weight-gradient MMAs, [2..5] DMA into TW, TZ, TC, TE
+    __shared__ uint64_t bars[6];
+    __shared__ MlpShared sh;
+    uint64_t *mbar = bars, *mbarw = bars + 1, *mb_w = bars + 2, *mb_z = bars + 3, *mb_c = bars + 4,
+             *mb_e = bars + 5;
+    const Smem S{smem_raw};
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int qd = warp & 3, qt = warp >> 2;
+    const int r = 32 * qd + lane;
+    const int E = 3 + 2 * f.L;
+    const int NA = f.n_active;
+    mlp_setup(S, f, sh, bars, 6);
+    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
+    const float *h2row0 = sh.h2row0;
+    const uint32_t tb = sh.tmem_base;
+    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0;
+    PredScale PS{sh.slot_mx, sh.slot_pred, 1};
+    const int eS1 = s1_exponent(h2row0);
+    const int P = *count;
+    const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
+    const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
+    const int b0 = qt, b1 = qt + 4;
+    const int nsdf = H * (E + 1) + NOUT * H;
+
+    // ---- weight-gradient accumulators (TMEM) and their folds into global memory
+    int acc_e[NACC];
+    bool acc_live[NACC];
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) {
+        acc_e[j] = 0;
+        acc_live[j] = false;
+    }
+    auto fold = [&](int j) {  // all threads; the accumulator's MMAs have completed
+        const float sc = pow2i(-acc_e[j]);
+        float d[8];
+        switch (j) {
+        case aC3:  // dC3^T: row = hidden unit, col = output (3)
+            umma::tmem_ld8(my + TB_DC3, d);
+            if (lane < 16 && qt == 0)
+                for (int o = 0; o < 3; ++o) atomicAdd(g_color + H * CIN + H * H + o * H + jrow, d[o] * sc);
+            break;
+        case aC2:
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                umma::tmem_ld8(my + TB_DC2 + 8 * b, d);
+                if (lane < 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) atomicAdd(g_color + H * CIN + jrow * H + 8 * b + k, d[k] * sc);
+            }
+            break;
+        case aC1:
+            umma::tmem_ld8(my + TB_DC1 + 8 * qt, d);
+            if (lane < 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (8 * qt + k < CIN) atomicAdd(g_color + jrow * CIN + 8 * qt + k, d[k] * sc);
+            break;
+        case aH2:  // dH2^T: row = hidden unit, col = output unit
+            umma::tmem_ld8(my + TB_DH2 + 8 * (qt & 1), d);
+            if (lane < 16 && qt < 2)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) atomicAdd(g_sdf + H * (E + 1) + (8 * qt + k) * H + jrow, d[k] * sc);
+            break;
+        case aH1a:
+        case aH1b:
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                umma::tmem_ld8(my + (j == aH1a ? TB_DH1A : TB_DH1B) + 8 * (b < 6 ? b : 0), d);
+                if (lane < 16 && b < 6)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int rc = h1_col(8 * b + k, E);
+                        if (rc >= 0) atomicAdd(g_sdf + jrow * (E + 1) + rc, d[k] * sc);
+                    }
+            }
+            break;
+        default:  // dH2[0] += sum_s pvec
+            umma::tmem_ld8(my + TB_DPV, d);
+            if (lane < 16 && qt == 0) atomicAdd(g_sdf + H * (E + 1) + jrow, d[0] * sc);
+            break;
+        }
+        acc_live[j] = false;
+    };
+    // before a weight-gradient GEMM into j with operand exponent sum e: fold on a scale
+    // change; returns the accumulate flag
+    auto acc_begin = [&](int j, int e) -> bool {
+        if (acc_live[j] && acc_e[j] != e) {
+            fold(j);
+            block_sync_tc();
+        }
+        const bool accumulate = acc_live[j];
+        acc_e[j] = e;
+        acc_live[j] = true;
+        return accumulate;
+    };
+    (void)nsdf;
+
+    float jv[4][6];
+    auto j_load = [&](int64_t tl) {
+        const float *jt = ws.jac + tl * JROWS * TILE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (4 * qt + i < NA) {
+                const float *jr = jt + 6 * (4 * qt + i) * TILE + r;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) jv[i][k] = jr[k * TILE];
+            }
+    };
+    auto j_store = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (4 * qt + i < NA) {
+                const uint32_t c = my + TB_J + 8 * (4 * qt + i);
+                umma::tmem_st4(c, jv[i][0], jv[i][1], jv[i][2], jv[i][3]);
+                umma::tmem_st2(c + 4, jv[i][4], jv[i][5]);
+            }
+        umma::tmem_st_wait();
+    };
+    auto fwt = [&](int64_t tl) { return ws.fw_tiles + tl * static_cast<int64_t>(FWB); };
+    auto dma = [&](uint32_t soff, const uint8_t *g, uint32_t bytes, uint64_t *mb) {
+        umma::bulk_g2s(S.p(soff), g, bytes, mb);
+    };
+    {
+        const int64_t t0 = blockIdx.x;
+        if (t0 * TILE < P) {
+            if (t == 0) {
+                dma(TW, fwt(t0) + FW_A2C, 2 * T64B, mb_w);
+                dma(TZ, fwt(t0) + FW_A1C, 2 * T64B, mb_z);
+                dma(TC, fwt(t0) + FW_CIN, 2 * TCB, mb_c);
+                dma(TE, ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mb_e);
+            }
+            j_load(t0);
+            j_store();
+        }
+    }
+    int ntiles_done = 0;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
+         base += static_cast<int64_t>(gridDim.x) * TILE) {
+        const int64_t p = base + r;
+        const bool valid = p < P;
+        const int64_t tile = base / TILE;
+        const int64_t ntile = tile + gridDim.x;
+        const bool has_next = ntile * TILE < P;
+        PS.par ^= 1;
+        float *SBt = ws.sb + tile * SBROWS * TILE;
+        if (t == 0 && has_next) {  // next tile's inputs -> L2 while this one runs
+            umma::prefetch_l2(fwt(ntile), FWB);
+            umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
+            umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, 2 * TEB);
+        }
+        // per-sample inputs
+        const float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
+        const uint2 mk = ws.fw_mask[(tile * 4 + qt) * TILE + r];
+        const uint32_t m1 = mk.x & 0xFFFFu, mc1 = mk.x >> 16, mc2 = mk.y;
+        const int4 fe = ws.fw_exp[tile];
+        const int eA1 = fe.x, eCin = fe.y, eA1c = fe.z, eA2c = fe.w;
+        const int eE = ws.e_exp[tile];
+        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
+        float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;
+        if (valid && qt == 0) {
+            gc0 = dl_dc[3 * p];
+            gc1 = dl_dc[3 * p + 1];
+            gc2 = dl_dc[3 * p + 2];
+            cc0 = nct[3 * TILE];
+            cc1 = nct[4 * TILE];
+            cc2 = nct[5 * TILE];
+        }
+        if (valid && qt <= 1) gd = dl_dsdf[p];
+        if (valid) {
+            const float n0 = nct[0], n1 = nct[TILE], n2 = nct[2 * TILE];
+            if (dl_dn_extra) {
+                gn0 = dl_dn_extra[3 * p];
+                gn1 = dl_dn_extra[3 * p + 1];
+                gn2 = dl_dn_extra[3 * p + 2];
+            }
+            if (eik_w != 0.f) {  // trainer.py:229-235 (fp32, numpy's order)
+                const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+                const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
+                gn0 += coef * n0 / Pf;
+                gn1 += coef * n1 / Pf;
+                gn2 += coef * n2 / Pf;
+            }
+        }
+        // ------------------------------------------------ B0: dlog -> U2, dC3
         int eD;
         {
             float dlog[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) dlog[k] = 0.f;
-            if (valid && qt == 0) {  // field.py:304
+            if (qt == 0) {  // field.py:304
                 dlog[0] = gc0 * cc0 * (1.f - cc0);
                 dlog[1] = gc1 * cc1 * (1.f - cc1);
                 dlog[2] = gc2 * cc2 * (1.f - cc2);
@@ -740,29 +943,31 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
             publish();
-            PMARK(14);
+            if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;
             if (!PS.check(kDlog, eD)) {
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
                 publish();
-                PMARK(15);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), 1, ID_KM(64), false);
-            umma::commit(&mbar);
-            umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
-            umma::commit(&mbarw);
+        {
+            const bool acc = acc_begin(aC3, eA2c + eD);
+            if (t == 0) {
+                umma::gemm3(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), 1, ID_KM(64), false);
+                umma::commit(mbar);
+                umma::mbar_wait(mb_w, ph_w);
+                umma::gemm3(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
+            }
+            ph_w ^= 1u;
         }
-        wait_mma(&mbar, phase);
-        PMARK(16);
-        // ------------------------------------------------ P6: u2 -> U1, dC2; dC3 fold
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ B1: u2 -> U1, dC2
         int eU2;
         {
             float u[2][8], m = 0.f;
             const float sc = pow2i(-(eD + eC3));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TM_SA + 8 * (i ? b1 : b0), u[i]);
+                umma::tmem_ld8(my + TB_SA + 8 * (i ? b1 : b0), u[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     u[i][k] = ((mc2 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
@@ -771,15 +976,6 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
             eU2 = PS.guess(kU2);
             PS.contrib(kU2, m);
-            wait_mma(&mbarw, phasew);  // dC3 (P5) done
-            PMARK(17);
-            float d[8];
-            umma::tmem_ld8(my + TM_DC3, d);
-            if (lane < 16 && qt == 0) {
-                const float sd = pow2i(-(eA2c + eD));
-#pragma unroll
-                for (int o = 0; o < 3; ++o) gacc[G_C3r + o * H + jrow] += d[o] * sd;
-            }
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
@@ -787,29 +983,30 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             };
             stg(eU2);
             publish();
-            PMARK(18);
             if (!PS.check(kU2, eU2)) {
                 stg(eU2);
                 publish();
-                PMARK(19);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), 4, ID_KM(64), false);
-            umma::commit(&mbar);
-            umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), 8, ID_WG(64), false);
-            umma::commit(&mbarw);
+        {
+            const bool acc = acc_begin(aC2, eU2 + eA1c);
+            if (t == 0) {
+                umma::gemm3(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), 4, ID_KM(64), false);
+                umma::commit(mbar);
+                umma::mbar_wait(mb_z, ph_z);
+                umma::gemm3(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), 8, ID_WG(64), acc);
+            }
+            ph_z ^= 1u;
         }
-        wait_mma(&mbar, phase);
-        PMARK(20);
-        // ------------------------------------------------ P7: u1 -> DCIN, dC1; dC2 fold
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ B2: u1 -> DCIN, dC1
         int eU1;
         {
             float u[2][8], m = 0.f;
             const float sc = pow2i(-(eU2 + eC2));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), u[i]);
+                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
@@ -818,18 +1015,6 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
             eU1 = PS.guess(kU1);
             PS.contrib(kU1, m);
-            wait_mma(&mbarw, phasew);  // dC2 (P6) done
-            PMARK(21);
-            float d[2][8];
-            umma::tmem_ld8(my + TM_DC2 + 8 * b0, d[0]);
-            umma::tmem_ld8(my + TM_DC2 + 8 * b1, d[1]);
-            if (lane < 16) {
-                const float sd = pow2i(-(eU2 + eA1c));
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) gacc[G_C2r + jrow * H + 8 * (i ? b1 : b0) + k] += d[i][k] * sd;
-            }
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
@@ -837,32 +1022,34 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             };
             stg(eU1);
             publish();
-            PMARK(22);
             if (!PS.check(kU1, eU1)) {
                 stg(eU1);
                 publish();
-                PMARK(23);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), 4, ID_KM(32), false);
-            umma::commit(&mbar);
-            umma::gemm3(tb + TM_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), 8, ID_WG(32), false);
-            umma::commit(&mbarw);
+        {
+            const bool acc = acc_begin(aC1, eU1 + eCin);
+            if (t == 0) {
+                umma::gemm3(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), 4, ID_KM(32), false);
+                umma::commit(mbar);
+                // TW is free: dC3 (B0) completed before B1's chain GEMM did
+                dma(TW, fwt(tile) + FW_A1, 2 * T64B, mb_w);
+                umma::mbar_wait(mb_c, ph_c);
+                umma::gemm3(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), 8, ID_WG(32), acc);
+            }
+            ph_c ^= 1u;
         }
-        wait_mma(&mbar, phase);
-        PMARK(24);
-        // ------------------------------------------------ P8: q, dly -> U, dH2; dC1 fold
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ B3: q, dly -> U, dH2
         float q0, q1, q2;
         int eDLY;
         {
             const float sc3 = pow2i(-(eU1 + eC1));
-            float c0[8], c1[8], c2[8];
-            umma::tmem_ld8(my + TM_SA, c0);
-            umma::tmem_ld8(my + TM_SA + 8, c1);
-            umma::tmem_ld8(my + TM_SA + 16, c2);
-            float c3[8];
-            umma::tmem_ld8(my + TM_SA + 24, c3);
+            float c0[8], c1[8], c2[8], c3[8];
+            umma::tmem_ld8(my + TB_SA, c0);
+            umma::tmem_ld8(my + TB_SA + 8, c1);
+            umma::tmem_ld8(my + TB_SA + 16, c2);
+            umma::tmem_ld8(my + TB_SA + 24, c3);
             q0 = gn0 + c0[3] * sc3;  // field.py:308-312
             q1 = gn1 + c0[4] * sc3;
             q2 = gn2 + c0[5] * sc3;
@@ -884,55 +1071,36 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             float m = 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(blk[k]));
-            // A1 restage (ReLU of Z1) for dH2 += A1^T DLY
-            float z[2][8];
-            const float sz = pow2i(-(eE + eH1));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TM_Z1 + 8 * (i ? b1 : b0), z[i]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) z[i][k] = z[i][k] > 0.f ? z[i][k] * sz : 0.f;
-            }
             eDLY = PS.guess(kDly);
             PS.contrib(kDly, m);
-            wait_mma(&mbarw, phasew);  // dC1 (P7) done
-            PMARK(25);
-            float d[8];
-            umma::tmem_ld8(my + TM_DC1 + 8 * qt, d);
-            if (lane < 16) {
-                const float sd = pow2i(-(eU1 + eCin));
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (8 * qt + k < CIN) gacc[G_C1r + jrow * CIN + 8 * qt + k] += d[k] * sd;
-            }
-            const float sa = pow2i(eA1);
-#pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, z[i], sa);
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
             publish();
-            PMARK(26);
             if (!PS.check(kDly, eDLY)) {
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
                 publish();
-                PMARK(27);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), 1, ID_KM(64), false);
-            umma::commit(&mbar);
-            umma::gemm3(tb + TM_DH2, S.MN(TY, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
-            umma::commit(&mbarw);
+        {
+            const bool acc = acc_begin(aH2, eA1 + eDLY);
+            if (t == 0) {
+                umma::gemm3(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), 1, ID_KM(64), false);
+                umma::commit(mbar);
+                umma::mbar_wait(mb_w, ph_w);
+                umma::gemm3(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
+            }
+            ph_w ^= 1u;
         }
-        wait_mma(&mbar, phase);
-        PMARK(28);
-        // ------------------------------------------------ P9: u, mvec -> DE, PV, dH1; dH2 fold
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ B4: u, mvec -> DE, PV, dH1
+        // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
+        if (t == 0 && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
         int eU, eMV;
         {
             float u[2][8], mu = 0.f;
             const float sc4 = pow2i(-(eDLY + eH2));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), u[i]);
+                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
@@ -947,12 +1115,11 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 mv[0][k] = 0.f;
                 mv[1][k] = 0.f;
             }
-            float mm = 0.f;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int l = 4 * qt + i;
                 float jl[8];
-                umma::tmem_ld8(my + TM_J + 8 * l, jl);
+                umma::tmem_ld8(my + TB_J + 8 * l, jl);
                 if (l < NA) {
                     mv[0][2 * i] = jl[0] * q0 + jl[1] * q1 + jl[2] * q2;
                     mv[0][2 * i + 1] = jl[3] * q0 + jl[4] * q1 + jl[5] * q2;
@@ -963,26 +1130,13 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 mv[1][1] = q1;
                 mv[1][2] = q2;
             }
+            float mm = 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
             eU = PS.guess(kU);
             eMV = PS.guess(kMv);
             PS.contrib(kU, mu);
             PS.contrib(kMv, mm);
-            wait_mma(&mbarw, phasew);  // dH2 (P8) done
-            PMARK(29);
-            if (qt < 2) {
-                float d[8];
-                umma::tmem_ld8(my + TM_DH2 + 8 * qt, d);
-                if (lane < 16) {
-                    const float sd = pow2i(-(eA1 + eDLY));
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) gacc[G_H2r + (8 * qt + k) * H + jrow] += d[k] * sd;
-                }
-            } else {
-                float d[8];
-                umma::tmem_ld8(my + TM_DH2, d);
-            }
             auto stg = [&](int eu, int emv) {
                 const float su = pow2i(eu), sm = pow2i(emv);
 #pragma unroll
@@ -1001,34 +1155,39 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 stage_blk<64>(S, TY, T64B, r, b, s1, ss);
             }
             publish();
-            PMARK(30);
             const bool oku = PS.check(kU, eU);
             const bool okm = PS.check(kMv, eMV);
             if (!(oku && okm)) {
                 stg(eU, eMV);
                 publish();
-                PMARK(31);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
-            umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
-            umma::commit(&mbar);
-            umma::gemm3(tb + TM_DH1, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), 8, ID_WG(48), false);
-            umma::gemm3(tb + TM_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), false);
-            umma::commit(&mbarw);
+        {
+            const bool acca = acc_begin(aH1a, eU + eE);
+            const bool accb = acc_begin(aH1b, eS1 + eMV);
+            if (t == 0) {
+                umma::gemm3(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
+                umma::gemm3(tb + TB_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
+                umma::commit(mbar);
+                umma::mbar_wait(mb_e, ph_e);
+                umma::gemm3(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), 8, ID_WG(48), acca);
+                umma::gemm3(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), accb);
+                umma::commit(mbarw);
+            }
+            ph_e ^= 1u;
         }
-        wait_mma(&mbar, phase);
-        PMARK(32);
-        // ------------------------------------------------ P10: pvec; scatter inputs; dH1 fold
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ B5: pvec; scatter inputs; dPV
+        // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
+        if (t == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
+        if (has_next) j_load(ntile);  // TMEM J is dead after B4
         int ePV;
-        if (jnext) j_load(ntile);  // next tile's J (TMEM J is dead after P9)
         {
             float pv[2][8], m = 0.f;
             const float sc = pow2i(-(eMV + eH1));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TM_SB + 8 * (i ? b1 : b0), pv[i]);
+                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), pv[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     pv[i][k] = ((m1 >> (8 * i + k)) & 1u) ? pv[i][k] * sc : 0.f;
@@ -1038,7 +1197,7 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             // dL/dfeature pairs (DE) and q for the scatter kernel
             const float sde = pow2i(-(eU + eH1));
             float de[8];
-            umma::tmem_ld8(my + TM_SA + 8 * qt, de);
+            umma::tmem_ld8(my + TB_SA + 8 * qt, de);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 if (8 * qt + k < 2 * NA) SBt[(8 * qt + k) * TILE + r] = de[k] * sde;
@@ -1049,23 +1208,10 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
             }
             ePV = PS.guess(kPv);
             PS.contrib(kPv, m);
-            wait_mma(&mbarw, phasew);  // dH1 (P9) done
-            PMARK(33);
-            e_fetch(ntile);  // TE is dead too
-            const float sa = pow2i(-(eU + eE)), sb = pow2i(-(eS1 + eMV));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int b = i ? b1 : b0;
-                float da[8], db[8];
-                umma::tmem_ld8(my + TM_DH1 + 8 * (b < 6 ? b : 0), da);
-                umma::tmem_ld8(my + TM_DC2 + 8 * (b < 6 ? b : 0), db);
-                if (lane < 16 && b < 6) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int rc = h1_col(8 * b + k, E);
-                        if (rc >= 0) gacc[G_H1r + jrow * (E + 1) + rc] += da[k] * sa + db[k] * sb;
-                    }
-                }
+            wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
+            if (t == 0 && has_next) {
+                dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
+                dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
             }
             if (qt < 2) {
                 float ones[8];
@@ -1073,57 +1219,40 @@ field_tc_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__rest
                 for (int k = 0; k < 8; ++k) ones[k] = (qt == 0 && k == 0) ? 1.f : 0.f;
                 stage_blk<16>(S, TD, TDB, r, qt, ones, 1.f);
             }
-            if (jnext) j_store();
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
             };
             stg(ePV);
+            if (has_next) j_store();
             publish();
-            PMARK(34);
             if (!PS.check(kPv, ePV)) {
                 stg(ePV);
                 publish();
-                PMARK(35);
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_DC3, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), false);
-            umma::commit(&mbarw);
+        {
+            const bool acc = acc_begin(aPv, ePV);
+            if (t == 0) {
+                umma::gemm3(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
+                umma::commit(mbarw);
+            }
         }
-        wait_mma(&mbarw, phasew);
-        PMARK(36);
-        {  // dH2[0] += sum_s pvec  (Theorem 1, layer 2)
-            float d[8];
-            umma::tmem_ld8(my + TM_DC3, d);
-            if (lane < 16 && qt == 0) gacc[G_H2r + jrow] += d[0] * pow2i(-ePV);
+        wait_mma(mbarw, phasew);  // TX and TD are restaged by the next tile
+        if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run
+            ntiles_done = 0;
+#pragma unroll 1
+            for (int j = 0; j < NACC; ++j)
+                if (acc_live[j]) fold(j);
+            block_sync_tc();
         }
     }
-#ifdef NS2B_PHASE_PROF
-    __syncthreads();
-    if (t == 0 && blockIdx.x == 0) {
-        printf("PHASEPROF kBwd=%d", int(kBwd));
-        for (int i = 0; i < 64; ++i)
-            if (pacc[i]) printf(" %d:%lld", i, pacc[i]);
-        printf("\n");
-    }
-#endif
-    if (eik_sum) {
-        double v = warp_sum(static_cast<double>(eik));
-        if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
-    }
+#pragma unroll 1
+    for (int j = 0; j < NACC; ++j)
+        if (acc_live[j]) fold(j);
     umma::fence_before_sync();
     __syncthreads();
-    if (kBwd) {
-        const int nsdf = H * (E + 1) + NOUT * H;
-        for (int i = t; i < GACC_FLOATS; i += MLP_THREADS) {
-            const float v = gacc[i];
-            if (v == 0.f) continue;
-            if (i < nsdf) atomicAdd(g_sdf + i, v);
-            else if (i < G_C3r + 3 * H) atomicAdd(g_color + (i - nsdf), v);
-        }
-    }
     if (warp == 0) umma::tmem_dealloc(tb, 512);
 }
 
@@ -1391,10 +1520,10 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
 static int g_tc_attr = 0;
 static int ensure_tc_attrs() {
     if (g_tc_attr) return NS2B_OK;
-    cudaError_t e = cudaFuncSetAttribute(field_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(field_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(SMEM_FWD));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(field_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(field_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_BWD));
     if (e != cudaSuccess) return set_error(NS2B_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
     g_tc_attr = 1;
@@ -1430,15 +1559,13 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
                                                                                          count, ws);
         return check_launch("field_gather");
     case 1:
-        tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
-            f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,
-            nullptr, nullptr, nullptr, ws);
+        tc::field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
+            f, count, sdf, colors, normals, geo, eik_sum, ws);
         return check_launch("field_mlp_forward");
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
-        tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-            f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf,
-            dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+        tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
+            f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
         return check_launch("field_mlp_backward");
     default:
         tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
@@ -1461,9 +1588,8 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
                                                                                          count, ws);
     if ((rc = check_launch("field_gather"))) return rc;
-    tc::field_tc_kernel<false><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
-        f, pos32, ray_ids, dirs, count, sdf, colors, normals, geo, eik_sum, nullptr, nullptr, nullptr, 0.f,
-        nullptr, nullptr, nullptr, ws);
+    tc::field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
+            f, count, sdf, colors, normals, geo, eik_sum, ws);
     return check_launch("field_forward_tc");
 }
 
@@ -1480,9 +1606,8 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
-    tc::field_tc_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-        f, pos32, ray_ids, dirs, count, nullptr, nullptr, nullptr, nullptr, nullptr, dl_dc, dl_dsdf, dl_dn_extra,
-        static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+    tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
+        f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
     if ((rc = check_launch("field_backward_tc"))) return rc;
     tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
                                                                                    grad_tables, tc::agg_levels_env());
