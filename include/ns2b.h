@@ -243,6 +243,12 @@ NS2B_API int ns2b_bench_l2_read(const float *buf, int64_t nfloats, int32_t iters
 /* nops random float2 REDs over nrows 8-B rows of buf (the scatter's access pattern). */
 NS2B_API int ns2b_bench_red(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void *stream);
 
+/* tcgen05 issue-rate probe (profiling aid, one CTA): `iters` kind::f16 MMAs of one of the
+ * MLP kernels' shapes (0: M128 N64 K/MN, 1: M64 N16 MN/MN, 2: M64 N64 MN/MN, 3: M128
+ * N16 K/K, 4: M64 N8 MN/MN, 5: M128 N64 K/K) rotating over nacc (1|2|4) accumulators;
+ * *cycles (device int64) = clock64 cycles from first issue to commit completion. */
+NS2B_API int ns2b_bench_umma(int32_t shape, int32_t iters, int32_t nacc, long long *cycles, void *stream);
+
 /* tcgen05 building-block self-test (one CTA): mode 0: D[128x64] = A[128x48] B[64x48]^T
  * (f16 split, K-major/K-major); 1: D = A[128x48] B[48x64] (B MN-major); 2: D[64x48] =
  * U[128x64]^T V[128x48] (bf16, M=64, MN-major both); 3: mode 0 in bf16. fp32 in/out. */

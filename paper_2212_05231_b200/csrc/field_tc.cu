@@ -100,14 +100,21 @@ constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
             plast = c_;                           \
         }                                         \
     } while (0)
+#define PWAIT(stmt)                              \
+    do {                                         \
+        const long long w0_ = clock64();         \
+        stmt;                                    \
+        pacc[63] += clock64() - w0_;             \
+    } while (0)
 #else
+#define PWAIT(stmt) stmt
 #define PMARK(i) \
     do {         \
     } while (0)
 #endif
 
 __device__ __forceinline__ float pow2i(int e) {
-    e = e < -120 ? -120 : (e > 120 ? 120 : e);
+    e = max(-120, min(120, e));
     return __int_as_float((127 + e) << 23);
 }
 
@@ -140,11 +147,11 @@ __device__ __forceinline__ void stage(const Smem &s, uint32_t off, uint32_t part
     umma::stage_row<0, C>(s.p(off), s.p(off + part), r, w);
 }
 
+// staging exponent for a tile maximum m >= 0: 2^e m in [2^13, 2^14); 0 for 0 / inf / nan
 __device__ __forceinline__ int exp_for(float m) {
-    if (!(m > 0.f) || !(m < INFINITY)) return 0;
-    int G;
-    frexpf(m, &G);
-    return kHead - G;
+    const int biased = static_cast<int>(__float_as_uint(m) >> 23);  // m >= 0: no sign bit
+    if (biased == 0 || biased >= 255) return m > 0.f ? kHead + 126 : 0;  // denormal / 0, inf, nan
+    return kHead + 126 - biased;  // frexp exponent of m = biased - 126
 }
 
 // block-wide max of up to two values -> their staging exponents (one barrier)
@@ -461,11 +468,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
         const int eE = ws.e_exp[tile];
         // ------------------------------------------------ P0: Z1 = E H1^T
-        if (t == 0) {
-            umma::bulk_wait_read();  // the previous tile's tile stores have left smem
+        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (lane == 0) umma::bulk_wait_read();  // the previous tile's tile stores have left smem
             umma::mbar_wait(mbare, phasee);
-            umma::gemm3(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
-            umma::commit(mbar);
+            umma::gemm3w<3>(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
+            umma::commit_elect(mbar);
         }
         phasee ^= 1u;
         wait_mma(mbar, phase);
@@ -513,11 +520,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
         }
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
-        if (t == 0) {
-            umma::gemm3(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), 4, ID_KK(16), false);
-            umma::gemm3(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
-            umma::commit(mbar);
-            umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
+        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            umma::gemm3w<4>(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
+            umma::gemm3w<4>(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
         }
         wait_mma(mbar, phase);
         // ------------------------------------------------ P2: normal, cin -> Zc1
@@ -607,10 +614,10 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 publish();
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), 2, ID_KK(64), false);
-            umma::commit(mbar);
-            umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
+        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            umma::gemm3w<2>(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), ID_KK(64), false);
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
         }
         wait_mma(mbar, phase);
         // ------------------------------------------------ P3: a1c -> Zc2
@@ -648,10 +655,10 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 publish();
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), 4, ID_KK(64), false);
-            umma::commit(mbar);
-            umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
+        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            umma::gemm3w<4>(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), ID_KK(64), false);
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
         }
         wait_mma(mbar, phase);
         // ------------------------------------------------ P4: a2c -> LOG
@@ -683,11 +690,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 publish();
             }
         }
-        if (t == 0) {
-            umma::gemm3(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), 4, ID_KK(16), false);
-            umma::commit(mbar);
-            umma::bulk_s2g(fwt + FW_A2C, S.p(TX), 2 * T64B);
-            ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
+        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            umma::gemm3w<4>(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), ID_KK(16), false);
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A2C, S.p(TX), 2 * T64B);
+            if (lane == 0) ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
         ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
         wait_mma(mbar, phase);
@@ -733,7 +740,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 // accumulate in TMEM across tiles while their operand exponents stay the same (sticky
 // predictions), and are folded into global memory every kFoldTiles tiles, when an
 // exponent changes, and at the end.
-constexpr int kFoldTiles = 8;
+constexpr int kFoldTiles = 32;
 enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, aPv, NACC };
 
 __global__ void __launch_bounds__(MLP_THREADS, 1)
@@ -881,6 +888,12 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
     }
     int ntiles_done = 0;
+#ifdef NS2B_PHASE_PROF
+    __shared__ long long pacc[64];
+    long long plast = clock64();
+    if (t < 64) pacc[t] = 0;
+    __syncthreads();
+#endif
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
         const int64_t p = base + r;
@@ -894,6 +907,12 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             umma::prefetch_l2(fwt(ntile), FWB);
             umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
             umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, 2 * TEB);
+            umma::prefetch_l2(ws.fw_nc + ntile * NCROWS * TILE, NCROWS * TILE * 4);
+            umma::prefetch_l2(ws.fw_mask + ntile * 4 * TILE, 4 * TILE * 8);
+            const int64_t nlast = min(static_cast<int64_t>(P), (ntile + 1) * TILE);  // dl_dc / dl_dsdf rows
+            const uint32_t nb = static_cast<uint32_t>(nlast - ntile * TILE);
+            umma::prefetch_l2(dl_dc + 3 * ntile * TILE, (12 * nb + 15) & ~15u);
+            umma::prefetch_l2(dl_dsdf + ntile * TILE, (4 * nb + 15) & ~15u);
         }
         // per-sample inputs
         const float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
@@ -943,23 +962,26 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
             publish();
+            PMARK(1);
             if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;
             if (!PS.check(kDlog, eD)) {
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
                 publish();
+                PMARK(2);
             }
         }
         {
             const bool acc = acc_begin(aC3, eA2c + eD);
-            if (t == 0) {
-                umma::gemm3(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), 1, ID_KM(64), false);
-                umma::commit(mbar);
-                umma::mbar_wait(mb_w, ph_w);
-                umma::gemm3(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<1>(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), ID_KM(64), false);
+                umma::commit_elect(mbar);
+                PWAIT(umma::mbar_wait(mb_w, ph_w));
+                umma::gemm3w<8>(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
             }
             ph_w ^= 1u;
         }
         wait_mma(mbar, phase);
+        PMARK(3);
         // ------------------------------------------------ B1: u2 -> U1, dC2
         int eU2;
         {
@@ -983,22 +1005,25 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             };
             stg(eU2);
             publish();
+            PMARK(4);
             if (!PS.check(kU2, eU2)) {
                 stg(eU2);
                 publish();
+                PMARK(5);
             }
         }
         {
             const bool acc = acc_begin(aC2, eU2 + eA1c);
-            if (t == 0) {
-                umma::gemm3(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), 4, ID_KM(64), false);
-                umma::commit(mbar);
-                umma::mbar_wait(mb_z, ph_z);
-                umma::gemm3(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), 8, ID_WG(64), acc);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<4>(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), ID_KM(64), false);
+                umma::commit_elect(mbar);
+                PWAIT(umma::mbar_wait(mb_z, ph_z));
+                umma::gemm3w<8>(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), ID_WG(64), acc);
             }
             ph_z ^= 1u;
         }
         wait_mma(mbar, phase);
+        PMARK(6);
         // ------------------------------------------------ B2: u1 -> DCIN, dC1
         int eU1;
         {
@@ -1022,24 +1047,27 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             };
             stg(eU1);
             publish();
+            PMARK(7);
             if (!PS.check(kU1, eU1)) {
                 stg(eU1);
                 publish();
+                PMARK(8);
             }
         }
         {
             const bool acc = acc_begin(aC1, eU1 + eCin);
-            if (t == 0) {
-                umma::gemm3(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), 4, ID_KM(32), false);
-                umma::commit(mbar);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), ID_KM(32), false);
+                umma::commit_elect(mbar);
                 // TW is free: dC3 (B0) completed before B1's chain GEMM did
-                dma(TW, fwt(tile) + FW_A1, 2 * T64B, mb_w);
-                umma::mbar_wait(mb_c, ph_c);
-                umma::gemm3(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), 8, ID_WG(32), acc);
+                if (lane == 0) dma(TW, fwt(tile) + FW_A1, 2 * T64B, mb_w);
+                PWAIT(umma::mbar_wait(mb_c, ph_c));
+                umma::gemm3w<8>(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), ID_WG(32), acc);
             }
             ph_c ^= 1u;
         }
         wait_mma(mbar, phase);
+        PMARK(9);
         // ------------------------------------------------ B3: q, dly -> U, dH2
         float q0, q1, q2;
         int eDLY;
@@ -1075,22 +1103,25 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             PS.contrib(kDly, m);
             if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
             publish();
+            PMARK(10);
             if (!PS.check(kDly, eDLY)) {
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
                 publish();
+                PMARK(11);
             }
         }
         {
             const bool acc = acc_begin(aH2, eA1 + eDLY);
-            if (t == 0) {
-                umma::gemm3(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), 1, ID_KM(64), false);
-                umma::commit(mbar);
-                umma::mbar_wait(mb_w, ph_w);
-                umma::gemm3(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<1>(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), ID_KM(64), false);
+                umma::commit_elect(mbar);
+                PWAIT(umma::mbar_wait(mb_w, ph_w));
+                umma::gemm3w<8>(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
             }
             ph_w ^= 1u;
         }
         wait_mma(mbar, phase);
+        PMARK(12);
         // ------------------------------------------------ B4: u, mvec -> DE, PV, dH1
         // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
         if (t == 0 && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
@@ -1155,28 +1186,31 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 stage_blk<64>(S, TY, T64B, r, b, s1, ss);
             }
             publish();
+            PMARK(13);
             const bool oku = PS.check(kU, eU);
             const bool okm = PS.check(kMv, eMV);
             if (!(oku && okm)) {
                 stg(eU, eMV);
                 publish();
+                PMARK(14);
             }
         }
         {
             const bool acca = acc_begin(aH1a, eU + eE);
             const bool accb = acc_begin(aH1b, eS1 + eMV);
-            if (t == 0) {
-                umma::gemm3(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), 4, ID_KM(48), false);
-                umma::gemm3(tb + TB_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), 3, ID_KK(64), false);
-                umma::commit(mbar);
-                umma::mbar_wait(mb_e, ph_e);
-                umma::gemm3(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), 8, ID_WG(48), acca);
-                umma::gemm3(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), 8, ID_WG(48), accb);
-                umma::commit(mbarw);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
+                umma::gemm3w<3>(tb + TB_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
+                umma::commit_elect(mbar);
+                PWAIT(umma::mbar_wait(mb_e, ph_e));
+                umma::gemm3w<8>(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), ID_WG(48), acca);
+                umma::gemm3w<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
+                umma::commit_elect(mbarw);
             }
             ph_e ^= 1u;
         }
         wait_mma(mbar, phase);
+        PMARK(15);
         // ------------------------------------------------ B5: pvec; scatter inputs; dPV
         // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
         if (t == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
@@ -1209,6 +1243,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             ePV = PS.guess(kPv);
             PS.contrib(kPv, m);
             wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
+            PMARK(16);
             if (t == 0 && has_next) {
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
@@ -1227,19 +1262,22 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             stg(ePV);
             if (has_next) j_store();
             publish();
+            PMARK(17);
             if (!PS.check(kPv, ePV)) {
                 stg(ePV);
                 publish();
+                PMARK(18);
             }
         }
         {
             const bool acc = acc_begin(aPv, ePV);
-            if (t == 0) {
-                umma::gemm3(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), 8, ID_WG(16), acc);
-                umma::commit(mbarw);
+            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+                umma::gemm3w<8>(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
+                umma::commit_elect(mbarw);
             }
         }
         wait_mma(mbarw, phasew);  // TX and TD are restaged by the next tile
+        PMARK(19);
         if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run
             ntiles_done = 0;
 #pragma unroll 1
@@ -1251,6 +1289,15 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
 #pragma unroll 1
     for (int j = 0; j < NACC; ++j)
         if (acc_live[j]) fold(j);
+#ifdef NS2B_PHASE_PROF
+    __syncthreads();
+    if (blockIdx.x == 0 && t == 0) {
+        printf("PHASEPROF bwd");
+        for (int i = 0; i < 64; ++i)
+            if (pacc[i]) printf(" %d:%lld", i, pacc[i]);
+        printf("\n");
+    }
+#endif
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tb, 512);

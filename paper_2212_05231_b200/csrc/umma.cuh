@@ -279,11 +279,74 @@ __device__ __forceinline__ Operand col_offset(Operand o, int c0, bool k_major) {
 // nk K-steps of 16.  Issued by one thread.
 __device__ __forceinline__ void gemm3(uint32_t tmem_d, const Operand &a, const Operand &b, int nk,
                                       uint32_t idesc, bool accumulate) {
+    // descriptors built once; a K step only advances the 14-bit start-address field
+    const uint64_t ah = make_desc(a.hi, a.lbo, a.sbo), al = make_desc(a.lo, a.lbo, a.sbo);
+    const uint64_t bh = make_desc(b.hi, b.lbo, b.sbo), bl = make_desc(b.lo, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+#pragma unroll 1
     for (int k = 0; k < nk; ++k) {
-        const uint64_t ah = a.desc_hi(k), al = a.desc_lo(k), bh = b.desc_hi(k), bl = b.desc_lo(k);
-        mma_f16(tmem_d, ah, bh, idesc, (accumulate || k > 0) ? 1u : 0u);
-        mma_f16(tmem_d, al, bh, idesc, 1u);
-        mma_f16(tmem_d, ah, bl, idesc, 1u);
+        const uint64_t oa = k * sa, ob = k * sb;
+        mma_f16(tmem_d, ah + oa, bh + ob, idesc, (accumulate || k > 0) ? 1u : 0u);
+        mma_f16(tmem_d, al + oa, bh + ob, idesc, 1u);
+        mma_f16(tmem_d, ah + oa, bl + ob, idesc, 1u);
+    }
+}
+
+// One K step of the 3-term split (A_hi B_hi [+acc], A_lo B_hi, A_hi B_lo) issued by the
+// lane elect.sync picks: call from a converged warp.  Doing the election inside the asm
+// lets ptxas emit the three UTCHMMAs back to back instead of a per-instruction
+// single-thread loop.
+__device__ __forceinline__ void mma3_elect(uint32_t tmem_d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "setp.eq.b32 p, 1, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate));
+}
+template <int NK>
+__device__ __forceinline__ void gemm3w(uint32_t tmem_d, const Operand &a, const Operand &b, uint32_t idesc,
+                                       bool accumulate) {
+    uint64_t ah = make_desc(a.hi, a.lbo, a.sbo), al = make_desc(a.lo, a.lbo, a.sbo);
+    uint64_t bh = make_desc(b.hi, b.lbo, b.sbo), bl = make_desc(b.lo, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+    mma3_elect(tmem_d, ah, al, bh, bl, idesc, accumulate ? 1u : 0u);
+#pragma unroll 1
+    for (int k = 1; k < NK; ++k) {  // running descriptors: four live 64-bit values
+        ah += sa;
+        al += sa;
+        bh += sb;
+        bl += sb;
+        mma3_elect(tmem_d, ah, al, bh, bl, idesc, 1u);
+    }
+}
+// commit by the elected lane (the one that issued the MMAs)
+__device__ __forceinline__ void commit_elect(uint64_t *mbar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(mbar)));
+}
+
+// Same with a compile-time K-step count: fully unrolled, so the issue loop is just the
+// descriptor adds and the MMAs on the uniform datapath.
+template <int NK>
+__device__ __forceinline__ void gemm3u(uint32_t tmem_d, const Operand &a, const Operand &b, uint32_t idesc,
+                                       bool accumulate) {
+    const uint64_t ah = make_desc(a.hi, a.lbo, a.sbo), al = make_desc(a.lo, a.lbo, a.sbo);
+    const uint64_t bh = make_desc(b.hi, b.lbo, b.sbo), bl = make_desc(b.lo, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const uint64_t oa = k * sa, ob = k * sb;
+        mma_f16(tmem_d, ah + oa, bh + ob, idesc, (accumulate || k > 0) ? 1u : 0u);
+        mma_f16(tmem_d, al + oa, bh + ob, idesc, 1u);
+        mma_f16(tmem_d, ah + oa, bl + ob, idesc, 1u);
     }
 }
 
