@@ -66,8 +66,9 @@ constexpr uint32_t TD = TC + 2 * TCB;                 // 128 x 16
 constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
 constexpr uint32_t TW = TEND;                         // 128 x 64 (backward: DMA'd A2c / A1)
+constexpr uint32_t TONES = TW + 2 * T64B;             // 128 x 8 ones column, hi part only (backward)
 constexpr uint32_t SMEM_FWD = TEND;
-constexpr uint32_t SMEM_BWD = TW + 2 * T64B;
+constexpr uint32_t SMEM_BWD = TONES + TILE * 8 * 2;
 
 // TMEM columns (512 allocated).  Forward:
 constexpr uint32_t TM_J = 176;    // 16 levels x 8: [dfeat/dx (6) | 2 spare]
@@ -452,6 +453,12 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         j_load(blockIdx.x);
         j_store();
     }
+#ifdef NS2B_PHASE_PROF
+    __shared__ long long pacc[64];
+    long long plast = clock64();
+    if (t < 64) pacc[t] = 0;
+    __syncthreads();
+#endif
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
         const int64_t p = base + r;
@@ -476,6 +483,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         }
         phasee ^= 1u;
         wait_mma(mbar, phase);
+        PMARK(1);
         e_fetch(ntile);
         // ------------------------------------------------ P1: a1, s1 -> Y, JD; SDF value
         uint32_t m1 = 0u;  // my 16 hidden-unit mask bits (blocks b0, b1)
@@ -513,10 +521,12 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 #pragma unroll
             for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
             publish();
+            PMARK(2);
             if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;  // next tile's slots (last read before this barrier)
             if (!PS.check(kA1, eA1)) {
                 stg(eA1);
                 publish();
+                PMARK(3);
             }
         }
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
@@ -527,6 +537,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
         }
         wait_mma(mbar, phase);
+        PMARK(4);
         // ------------------------------------------------ P2: normal, cin -> Zc1
         int eCin;
         {
@@ -609,9 +620,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                     for (int o = 1; o < 16; ++o) geo_out[15 * p + o - 1] = y[o];
             }
             publish();
+            PMARK(5);
             if (!PS.check(kCin, eCin)) {
                 stage_blk<32>(S, TC, TCB, r, qt, blk, pow2i(eCin));
                 publish();
+                PMARK(6);
             }
         }
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
@@ -620,6 +633,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
         }
         wait_mma(mbar, phase);
+        PMARK(7);
         // ------------------------------------------------ P3: a1c -> Zc2
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
@@ -650,9 +664,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             stg(eA1c);
             if (t == 0) umma::bulk_wait_read();  // A1 has left TX before P4 restages it
             publish();
+            PMARK(8);
             if (!PS.check(kA1c, eA1c)) {
                 stg(eA1c);
                 publish();
+                PMARK(9);
             }
         }
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
@@ -661,6 +677,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
         }
         wait_mma(mbar, phase);
+        PMARK(10);
         // ------------------------------------------------ P4: a2c -> LOG
         {
             float z[2][8], m = 0.f;
@@ -685,9 +702,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             };
             stg(eA2c);
             publish();
+            PMARK(11);
             if (!PS.check(kA2c, eA2c)) {
                 stg(eA2c);
                 publish();
+                PMARK(12);
             }
         }
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
@@ -698,6 +717,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         }
         ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
         wait_mma(mbar, phase);
+        PMARK(13);
         // ------------------------------------------------ P5: colours
         {
             float lg[4];
@@ -716,6 +736,15 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
         }
     }
+#ifdef NS2B_PHASE_PROF
+    __syncthreads();
+    if (blockIdx.x == 0 && t == 0) {
+        printf("PHASEPROF fwd");
+        for (int i = 0; i < 64; ++i)
+            if (pacc[i]) printf(" %d:%lld", i, pacc[i]);
+        printf("\n");
+    }
+#endif
     if (eik_sum) {
         double v = warp_sum(static_cast<double>(eik));
         if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
@@ -761,6 +790,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
     mlp_setup(S, f, sh, bars, 6);
+    if (t < TILE)  // ones column (fp16 1.0 in column 0) for dH2[0] += PV^T 1; published by B0's barrier
+        *reinterpret_cast<uint4 *>(S.p(TONES) + umma::tile_off(t, 0, 8)) = make_uint4(0x3C00u, 0u, 0u, 0u);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
@@ -1248,12 +1279,6 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
             }
-            if (qt < 2) {
-                float ones[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) ones[k] = (qt == 0 && k == 0) ? 1.f : 0.f;
-                stage_blk<16>(S, TD, TDB, r, qt, ones, 1.f);
-            }
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
@@ -1269,16 +1294,20 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 PMARK(18);
             }
         }
+        // dH2[0] += PV^T 1: the ones column is exact in fp16, so two split terms.  Not
+        // awaited: TX is restaged at the next tile's B2, after B0/B1's chain GEMMs
+        // (issued behind it in the in-order MMA pipe) have completed.
+        const bool fold_now = ++ntiles_done == kFoldTiles;
         {
             const bool acc = acc_begin(aPv, ePV);
             if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
-                umma::gemm3w<8>(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
-                umma::commit_elect(mbarw);
+                umma::gemm2w<8>(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TONES, 0, 8), ID_WG(8), acc);
+                if (fold_now) umma::commit_elect(mbarw);
             }
         }
-        wait_mma(mbarw, phasew);  // TX and TD are restaged by the next tile
-        PMARK(19);
-        if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run
+        if (fold_now) {  // bound the TMEM accumulation run
+            wait_mma(mbarw, phasew);
+            PMARK(19);
             ntiles_done = 0;
 #pragma unroll 1
             for (int j = 0; j < NACC; ++j)
@@ -1286,6 +1315,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             block_sync_tc();
         }
     }
+    if (warp == 0) umma::commit_elect(mbarw);
+    wait_mma(mbarw, phasew);
 #pragma unroll 1
     for (int j = 0; j < NACC; ++j)
         if (acc_live[j]) fold(j);

@@ -82,6 +82,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
         "r"(parity), "r"(kSuspendNs));
 }
 
+// plain spin (no suspend hint), for latency comparisons
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *mbar, uint32_t parity) {
+    uint32_t addr = smem_u32(mbar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t}\n" ::"r"(addr),
+        "r"(parity));
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -324,6 +337,35 @@ __device__ __forceinline__ void gemm3w(uint32_t tmem_d, const Operand &a, const 
         mma3_elect(tmem_d, ah, al, bh, bl, idesc, 1u);
     }
 }
+// Two-term split (A_hi B + A_lo B) for a B operand that is exact in fp16 (lo part zero):
+// only b.hi is read.
+__device__ __forceinline__ void mma2_elect(uint32_t tmem_d, uint64_t ah, uint64_t al, uint64_t bh, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n\t"
+        "setp.eq.b32 p, 1, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(ah), "l"(al), "l"(bh), "r"(idesc), "r"(accumulate));
+}
+template <int NK>
+__device__ __forceinline__ void gemm2w(uint32_t tmem_d, const Operand &a, const Operand &b, uint32_t idesc,
+                                       bool accumulate) {
+    uint64_t ah = make_desc(a.hi, a.lbo, a.sbo), al = make_desc(a.lo, a.lbo, a.sbo);
+    uint64_t bh = make_desc(b.hi, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+    mma2_elect(tmem_d, ah, al, bh, idesc, accumulate ? 1u : 0u);
+#pragma unroll 1
+    for (int k = 1; k < NK; ++k) {
+        ah += sa;
+        al += sa;
+        bh += sb;
+        mma2_elect(tmem_d, ah, al, bh, idesc, 1u);
+    }
+}
+
 // commit by the elected lane (the one that issued the MMAs)
 __device__ __forceinline__ void commit_elect(uint64_t *mbar) {
     asm volatile(

@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(128) umma_rate_kernel(int shape, int iters, in
         const long long c0 = clock64();
         for (int i = 0; i < iters / 12; ++i) umma::gemm3w<4>(tbase, A, B, idesc, i > 0);
         umma::commit_elect(&mbar);
-        umma::mbar_wait(&mbar, 0);
+        if (shape == 5) umma::mbar_wait_spin(&mbar, 0);  // shape 5: compare the plain spin wait
+        else umma::mbar_wait(&mbar, 0);
         if (t == 0) out[0] = clock64() - c0;
     } else if (t == 0) {
         const int M = (shape == 1 || shape == 2 || shape == 4) ? 64 : 128;
