@@ -237,7 +237,23 @@ def occupancy_case():
                         ema_sum=ema.sum(), frac=st.occ.bits.mean())
 
 
+def checkpoint_case():
+    """NS2C checkpoint (checkpoint.py:76-114) of a small trained state, written by the
+    reference itself: the byte-level fixture for the checkpoint reader/writer."""
+    from hashsdf import checkpoint
+
+    with tempfile.TemporaryDirectory() as td:
+        ds = scene_io.make_synthetic("sphere", td, views=4, image_size=32, seed=0)
+    cfg = trainer.TrainConfig(batch_size=64, num_levels=4, table_size=2**10, seed=0,
+                              occupancy_resolution=16, level_init=4)
+    st = trainer.TrainState.create(cfg, aabb=ds.scene_aabb)
+    for _ in range(2):
+        trainer.train_step(st, ds)
+    checkpoint.save_checkpoint(OUT / "ckpt_small.ns2c", st, extra_sections=[(b"XTRA", b"kept")])
+
+
 def main():
+    checkpoint_case()
     kat()
     mlp_case()
     for g in cases.GRIDS:
