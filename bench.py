@@ -233,6 +233,28 @@ def _maybe_gpu():
 
 
 # ------------------------------------------------------------------ GPU ---
+def time_samplers(ds, count, dev):
+    """Ray-batch construction outside the timed step (f2): the host restatement of
+    sample_ray_batch vs the device sampler, same rng stream, wall ms per batch."""
+    import torch
+
+    from paper_2212_05231_b200 import scene_io
+
+    rng = np.random.default_rng(7)
+    scene_io.sample_ray_batch(ds, 0, count, 0.9, rng)  # pools built once (cached)
+    t0 = time.perf_counter()
+    scene_io.sample_ray_batch(ds, 0, count, 0.9, rng)
+    host = (time.perf_counter() - t0) * 1e3
+    smp = scene_io.DeviceSampler(ds, 0, dev)
+    smp.sample(count, 0.9, rng)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        smp.sample(count, 0.9, rng)
+    torch.cuda.synchronize()
+    return {"rays": count, "host_ms": host, "device_ms": (time.perf_counter() - t0) * 1e3 / 5}
+
+
 def l2_probes(dev, nbytes=64 << 20):
     """Measured L2 read and random-RED bandwidth (GB/s) over a working-set-sized buffer."""
     import torch
@@ -353,6 +375,7 @@ def run_ours(args, wl):
     e2e = m_global * args.steps / (ms_e2e * 1e-3)
     if rank != 0:
         return
+    sampler = time_samplers(ds, m_global, dev)
     peaks = load_peaks()
     l2 = l2_probes(dev)
     Pl = P_mean / world  # per-rank samples per launch
@@ -397,7 +420,7 @@ def run_ours(args, wl):
                                + ("hbm_gbs" if d["unit"] == "GB/s" else "bf16_tflops_sustained"),
                 "traffic": None, "algorithmic_per_sample": d["per_sample"],
                 "step_share": d["ms"] / (ms_dev / args.steps), "kernels": kern,
-                "per_kernel_ms": per_kernel, "l2_probe": l2}
+                "per_kernel_ms": per_kernel, "l2_probe": l2, "sampler": sampler}
     # CPU baseline on a bounded sample (the oracle, all host cores)
     wl["_dataset"] = ds
     cpu = None

@@ -112,6 +112,18 @@ typedef struct {
     const uint8_t *bits;
 } ns2b_occ_t;
 
+/* Ray batch from pixel picks (scene_io.py:98-116,129-172).  picks[i] indexes
+ * pool_first for i < n_first and pool_rest otherwise (the reference's foreground /
+ * background draws); a pool entry is frame * H * W + y * W + x.  frames: per frame 16
+ * doubles = R (row-major 3x3) | camera centre (3) | fx fy cx cy.  images (F,H,W,3) and
+ * masks (F,H,W) uint8 (image = u8 / 255, mask 0/1).  Out (n,3) fp64: origins, unit
+ * directions, targets image * mask. */
+NS2B_API int ns2b_rays_from_picks(const int64_t *picks, int64_t n, int64_t n_first,
+                                  const int32_t *pool_first, const int32_t *pool_rest,
+                                  const double *frames, int32_t width, int32_t height,
+                                  const uint8_t *images, const uint8_t *masks, double *origins,
+                                  double *dirs, double *targets, void *stream);
+
 /* march_rays pass 1 (renderer.py:153-192): kept-sample count per ray (fp64 slab test,
  * fixed-stride midpoints, <=512 candidates, occupancy bit test). */
 NS2B_API int ns2b_march_count(const double *origins, const double *dirs, int64_t nrays,

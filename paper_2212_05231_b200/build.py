@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-NO_FMA = {"march.cu", "composite.cu"}
+NO_FMA = {"march.cu", "composite.cu", "rays.cu"}
 
 
 def _sources():

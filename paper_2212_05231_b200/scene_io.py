@@ -45,6 +45,14 @@ class MultiViewDataset:
 
     def __post_init__(self):
         self._pools = {}
+        self._device_samplers = {}
+
+    def to_device(self, time_index=0, device=None):
+        """Keep this dataset's images, masks and pixel pools in HBM: sample_ray_batch
+        (and so train_step) then builds its batches on the GPU (DeviceSampler)."""
+        if time_index not in self._device_samplers:
+            self._device_samplers[time_index] = DeviceSampler(self, time_index, device)
+        return self._device_samplers[time_index]
 
     def pools(self, time_index):
         """(frames, fg pool, bg pool) cached per time index (scene_io.py:137-146)."""
@@ -92,6 +100,9 @@ def sample_ray_batch(dataset, time_index, count, fg_fraction, rng):
     targets image*mask (`scene_io.py:129-172`); identical rng consumption."""
     if count < 1:
         raise ValueError("count must be >= 1")
+    dev = getattr(dataset, "_device_samplers", {}).get(time_index)
+    if dev is not None:
+        return dev.sample(count, fg_fraction, rng)
     frames, fg, bg = dataset.pools(time_index)
     if not frames:
         raise ValueError("empty foreground: no frames at this time index")
@@ -206,6 +217,89 @@ def make_dtu_shaped(views=49, width=1600, height=1200, seed=0, preset="two-spher
     """Config-2 scene: 49 orbit cameras, 1600x1200, fx=fy=1.4*1200."""
     return make_synthetic(preset, views=views, seed=seed, width=width, height=height,
                           focal=1.4 * height)
+
+
+class DeviceSampler:
+    """`sample_ray_batch` with the dataset resident in HBM.
+
+    The reference's rng draws stay on the host -- two `rng.integers` calls on the
+    caller's generator, so the stream (and a checkpointed rng state) is identical --
+    and only the pick indices (8 B per ray) are uploaded; pool lookup, pinhole rays and
+    targets are one kernel (`ns2b_rays_from_picks`) over images (uint8), masks (0/1)
+    and the foreground / background pixel pools kept on the device."""
+
+    def __init__(self, dataset, time_index=0, device=None):
+        from . import _lib
+
+        frames, fg, bg = dataset.pools(time_index)
+        if not frames:
+            raise ValueError("empty foreground: no frames at this time index")
+        h, w = frames[0].height, frames[0].width
+        if any(f.height != h or f.width != w for f in frames):
+            raise NotImplementedError("device sampler needs frames of one size")
+        imgs = np.stack([f.image for f in frames])
+        u8 = np.rint(imgs * 255.0)
+        if not (np.array_equal(u8 / 255.0, imgs) and u8.min() >= 0 and u8.max() <= 255):
+            raise NotImplementedError("device sampler stores 8-bit images (image = u8 / 255)")
+        masks = np.stack([f.mask for f in frames])
+        if not np.all((masks == 0) | (masks == 1)):
+            raise NotImplementedError("device sampler stores binary masks")
+        dev = device or _lib.device()
+        self.h, self.w, self.dev = h, w, dev
+        self.images = torch.from_numpy(u8.astype(np.uint8)).to(dev)
+        self.masks = torch.from_numpy(masks.astype(np.uint8)).to(dev)
+        par = np.zeros((len(frames), 16))
+        for k, f in enumerate(frames):
+            par[k, :9] = f.pose[:3, :3].reshape(-1)
+            par[k, 9:12] = f.pose[:3, 3]
+            par[k, 12:] = (f.fx, f.fy, f.cx, f.cy)
+        self.frames = torch.from_numpy(par).to(dev)
+        hw = h * w
+
+        def flat(pool):
+            return torch.from_numpy((pool[:, 0] * hw + pool[:, 2] * w + pool[:, 1]).astype(np.int32)).to(dev)
+
+        self.n_fg, self.n_bg = fg.shape[0], bg.shape[0]
+        if self.n_fg == 0:
+            raise ValueError("empty foreground")
+        self.fg = flat(fg)
+        self.bg = flat(bg) if self.n_bg else self.fg
+        self._picks = None
+        self._copied = None
+
+    def sample(self, count, fg_fraction, rng):
+        """RayBatch of device tensors; consumes `rng` exactly like sample_ray_batch."""
+        from . import _lib
+
+        if count < 1:
+            raise ValueError("count must be >= 1")
+        n_fg = int(np.floor(fg_fraction * count))
+        n_bg = count - n_fg
+        a = rng.integers(0, self.n_fg, size=n_fg)
+        if n_bg > 0 and self.n_bg == 0:
+            b = rng.integers(0, self.n_fg, size=n_bg)
+            flags = torch.ones(count, dtype=torch.bool, device=self.dev)
+        else:
+            b = rng.integers(0, self.n_bg, size=n_bg)
+            flags = torch.cat([torch.ones(n_fg, dtype=torch.bool, device=self.dev),
+                               torch.zeros(n_bg, dtype=torch.bool, device=self.dev)])
+        if self._copied is not None:
+            self._copied.synchronize()  # the previous upload has left the pinned buffer
+        if self._picks is None or self._picks.shape[0] < count:
+            self._picks = torch.empty(count, dtype=torch.int64).pin_memory()
+        hp = self._picks[:count]
+        hp[:n_fg].copy_(torch.from_numpy(a))
+        hp[n_fg:].copy_(torch.from_numpy(b))
+        picks = hp.to(self.dev, non_blocking=True)
+        self._copied = torch.cuda.Event()
+        self._copied.record()
+        o = torch.empty((count, 3), dtype=torch.float64, device=self.dev)
+        d, t = torch.empty_like(o), torch.empty_like(o)
+        _lib.call("ns2b_rays_from_picks", _lib.ptr(picks), count, n_fg, _lib.ptr(self.fg), _lib.ptr(self.bg),
+                  _lib.ptr(self.frames), self.w, self.h, _lib.ptr(self.images), _lib.ptr(self.masks),
+                  _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.stream_ptr())
+        self._last_picks = picks  # alive until the kernel has run (stream order)
+        return RayBatch(o, d, t, flags)
 
 
 class DeviceRaySource:

@@ -1,0 +1,58 @@
+"""Device ray sampler vs the host restatement of `sample_ray_batch`
+(`scene_io.py:129-172`): same rng consumption, same picks, identical targets and
+origins; directions equal to the last bit wherever the host's BLAS evaluates the
+3x3 matmul as an FMA chain (the order ns2b_rays_from_picks uses), else within 2 ulp."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2212_05231_b200 import scene_io  # noqa: E402
+
+
+def _pair(ds, count, seed, fg=0.9):
+    r1, r2 = np.random.default_rng(seed), np.random.default_rng(seed)
+    host = scene_io.sample_ray_batch(ds, 0, count, fg, r1)
+    dev = scene_io.DeviceSampler(ds).sample(count, fg, r2)
+    assert r1.bit_generator.state == r2.bit_generator.state
+    return host, dev
+
+
+@pytest.mark.parametrize("shape", ["square", "rect"])
+def test_device_batches_match_host(shape):
+    if shape == "square":
+        ds = scene_io.make_synthetic("sphere", views=8, image_size=64, seed=0)
+    else:
+        ds = scene_io.make_synthetic("two-spheres", views=5, seed=3, width=96, height=72, focal=100.8)
+    for seed in (0, 1):
+        host, dev = _pair(ds, 4096, seed)
+        assert np.array_equal(dev.origins.cpu().numpy(), host.origins)
+        assert np.array_equal(dev.target_colors.cpu().numpy(), host.target_colors)
+        assert np.array_equal(dev.foreground_flags.cpu().numpy(), host.foreground_flags)
+        d, h = dev.directions.cpu().numpy(), host.directions
+        ulp = np.abs(d - h) / np.spacing(np.abs(h))
+        assert ulp.max() <= 2, f"max {ulp.max()} ulp"
+        print(f"{shape} seed {seed}: {np.mean(d == h):.4f} of direction components bit-exact")
+
+
+def test_training_uses_device_sampler():
+    from paper_2212_05231_b200 import trainer
+
+    ds_h = scene_io.make_synthetic("sphere", views=8, image_size=64, seed=0)
+    ds_d = scene_io.make_synthetic("sphere", views=8, image_size=64, seed=0)
+    ds_d.to_device()
+    cfg = trainer.TrainConfig(batch_size=2048, num_levels=8, table_size=2**14, seed=0, level_init=8)
+    a, b = trainer.TrainState.create(cfg), trainer.TrainState.create(cfg)
+    for _ in range(2):
+        ra = trainer.train_step(a, ds_h)
+        rb = trainer.train_step(b, ds_d)
+        assert ra.sample_count == rb.sample_count
+        assert abs(ra.total - rb.total) <= 1e-6 * abs(ra.total)
+    assert a.rng.bit_generator.state == b.rng.bit_generator.state
