@@ -66,9 +66,8 @@ constexpr uint32_t TD = TC + 2 * TCB;                 // 128 x 16
 constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
 constexpr uint32_t TW = TEND;                         // 128 x 64 (backward: DMA'd A2c / A1)
-constexpr uint32_t TONES = TW + 2 * T64B;             // 128 x 8 ones column, hi part only (backward)
 constexpr uint32_t SMEM_FWD = TEND;
-constexpr uint32_t SMEM_BWD = TONES + TILE * 8 * 2;
+constexpr uint32_t SMEM_BWD = TW + 2 * T64B;
 
 // TMEM columns (512 allocated).  Forward:
 constexpr uint32_t TM_J = 176;    // 16 levels x 8: [dfeat/dx (6) | 2 spare]
@@ -82,8 +81,7 @@ constexpr uint32_t TB_DC1 = 64;    // 32
 constexpr uint32_t TB_DC3 = 96;    // 16 (3 used)
 constexpr uint32_t TB_DH2 = 112;   // 16
 constexpr uint32_t TB_DH1A = 128;  // 48: U^T E
-constexpr uint32_t TB_DH1B = 176;  // 48: S1^T MV (Theorem 1)
-constexpr uint32_t TB_DPV = 224;   // 16 (1 used): PV^T 1 (Theorem 1, layer 2)
+constexpr uint32_t TB_DH1B = 176;  // 48: G = M1^T MV (Theorem 1: dH1 and dH2[0])
 constexpr uint32_t TB_J = 240;     // 128
 constexpr uint32_t TB_SA = 368;    // 64
 constexpr uint32_t TB_SB = 432;    // 64
@@ -319,7 +317,7 @@ constexpr int MLP_THREADS = 512;
 // phase needs anyway.  A tile whose max left [2^3, 2^15) is restaged with the exact
 // exponent (first tile of a CTA, sudden range changes).  Scaling by 2^e is exact, so
 // the products equal those of an exactly-scaled tile.
-enum Slot { kA1, kCin, kA1c, kA2c, kDlog, kU2, kU1, kDly, kU, kMv, kPv, NSLOT };
+enum Slot { kA1, kCin, kA1c, kA2c, kDlog, kU2, kU1, kDly, kU, kMv, NSLOT };
 struct PredScale {
     uint32_t (*mx)[NSLOT];  // [2][NSLOT] block maxima (bits of |v|), tile parity
     int *pred;              // [NSLOT]
@@ -770,7 +768,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 // predictions), and are folded into global memory every kFoldTiles tiles, when an
 // exponent changes, and at the end.
 constexpr int kFoldTiles = 32;
-enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, aPv, NACC };
+enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, NACC };
 
 __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
@@ -790,8 +788,6 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
     mlp_setup(S, f, sh, bars, 6);
-    if (t < TILE)  // ones column (fp16 1.0 in column 0) for dH2[0] += PV^T 1; published by B0's barrier
-        *reinterpret_cast<uint4 *>(S.p(TONES) + umma::tile_off(t, 0, 8)) = make_uint4(0x3C00u, 0u, 0u, 0u);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
@@ -846,11 +842,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 for (int k = 0; k < 8; ++k) atomicAdd(g_sdf + H * (E + 1) + (8 * qt + k) * H + jrow, d[k] * sc);
             break;
         case aH1a:
-        case aH1b:
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int b = i ? b1 : b0;
-                umma::tmem_ld8(my + (j == aH1a ? TB_DH1A : TB_DH1B) + 8 * (b < 6 ? b : 0), d);
+                umma::tmem_ld8(my + TB_DH1A + 8 * (b < 6 ? b : 0), d);
                 if (lane < 16 && b < 6)
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
@@ -859,10 +854,26 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                     }
             }
             break;
-        default:  // dH2[0] += sum_s pvec
-            umma::tmem_ld8(my + TB_DPV, d);
-            if (lane < 16 && qt == 0) atomicAdd(g_sdf + H * (E + 1) + jrow, d[0] * sc);
+        default: {  // G = M1^T MV: dH1 += H2[0][j] G[j],  dH2[0][j] += H1[j] . G[j]
+            float dot = 0.f;
+            const float h2j = lane < 16 ? h2row0[jrow] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int b = i ? b1 : b0;
+                umma::tmem_ld8(my + TB_DH1B + 8 * (b < 6 ? b : 0), d);
+                if (lane < 16 && b < 6)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int rc = h1_col(8 * b + k, E);
+                        if (rc >= 0) {
+                            atomicAdd(g_sdf + jrow * (E + 1) + rc, h2j * d[k] * sc);
+                            dot = fmaf(f.sdf_w[jrow * (E + 1) + rc], d[k], dot);
+                        }
+                    }
+            }
+            if (lane < 16 && dot != 0.f) atomicAdd(g_sdf + H * (E + 1) + jrow, dot * sc);
             break;
+        }
         }
         acc_live[j] = false;
     };
@@ -1207,14 +1218,15 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
             };
             stg(eU, eMV);
-            const float ss = pow2i(eS1);
-            float s1[8];
+            // the ReLU mask M1 (exact in fp16: hi part only) for G = M1^T MV
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                const int b = i ? b1 : b0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) s1[k] = ((m1 >> (8 * i + k)) & 1u) ? h2row0[8 * b + k] : 0.f;
-                stage_blk<64>(S, TY, T64B, r, b, s1, ss);
+                const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
+                auto h2 = [&](int k) {
+                    return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
+                };
+                *reinterpret_cast<uint4 *>(S.p(TY) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
+                    make_uint4(h2(0), h2(2), h2(4), h2(6));
             }
             publish();
             PMARK(13);
@@ -1227,38 +1239,28 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
         }
         {
+            // Theorem 1 through one accumulator: with G = M1^T MV (64 x 48),
+            //   dH1 += diag(H2[0]) G   and   dH2[0][j] += sum_c H1[j][c] G[j][c]
+            // (both applied when G is folded), so pvec = m1 . (H1 mvec) never materialises.
             const bool acca = acc_begin(aH1a, eU + eE);
-            const bool accb = acc_begin(aH1b, eS1 + eMV);
+            const bool accb = acc_begin(aH1b, eMV);
             if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
-                umma::gemm3w<3>(tb + TB_SB, S.K(TZ, T64B, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_e, ph_e));
                 umma::gemm3w<8>(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), ID_WG(48), acca);
-                umma::gemm3w<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
+                umma::gemm2a<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
                 umma::commit_elect(mbarw);
             }
             ph_e ^= 1u;
         }
         wait_mma(mbar, phase);
         PMARK(15);
-        // ------------------------------------------------ B5: pvec; scatter inputs; dPV
+        // ------------------------------------------------ B5: scatter inputs; next tile's DMAs
         // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
         if (t == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
         if (has_next) j_load(ntile);  // TMEM J is dead after B4
-        int ePV;
         {
-            float pv[2][8], m = 0.f;
-            const float sc = pow2i(-(eMV + eH1));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), pv[i]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    pv[i][k] = ((m1 >> (8 * i + k)) & 1u) ? pv[i][k] * sc : 0.f;
-                    m = fmaxf(m, fabsf(pv[i][k]));
-                }
-            }
             // dL/dfeature pairs (DE) and q for the scatter kernel
             const float sde = pow2i(-(eU + eH1));
             float de[8];
@@ -1271,43 +1273,19 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 SBt[65 * TILE + r] = q1;
                 SBt[66 * TILE + r] = q2;
             }
-            ePV = PS.guess(kPv);
-            PS.contrib(kPv, m);
             wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
             PMARK(16);
             if (t == 0 && has_next) {
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
             }
-            auto stg = [&](int e) {
-                const float s = pow2i(e);
-#pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, pv[i], s);
-            };
-            stg(ePV);
             if (has_next) j_store();
-            publish();
-            PMARK(17);
-            if (!PS.check(kPv, ePV)) {
-                stg(ePV);
-                publish();
-                PMARK(18);
-            }
         }
-        // dH2[0] += PV^T 1: the ones column is exact in fp16, so two split terms.  Not
-        // awaited: TX is restaged at the next tile's B2, after B0/B1's chain GEMMs
-        // (issued behind it in the in-order MMA pipe) have completed.
-        const bool fold_now = ++ntiles_done == kFoldTiles;
-        {
-            const bool acc = acc_begin(aPv, ePV);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
-                umma::gemm2w<8>(tb + TB_DPV, S.MN(TX, T64B, 64), S.MN(TONES, 0, 8), ID_WG(8), acc);
-                if (fold_now) umma::commit_elect(mbarw);
-            }
-        }
-        if (fold_now) {  // bound the TMEM accumulation run
-            wait_mma(mbarw, phasew);
-            PMARK(19);
+        // Tile boundary barrier: without it a warp can run into the next tile while another
+        // is still in B5; observed to deadlock on the c1 field (mbarw never completing),
+        // so warps leave the tile together.
+        publish();
+        if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run (all MMAs done)
             ntiles_done = 0;
 #pragma unroll 1
             for (int j = 0; j < NACC; ++j)

@@ -14,6 +14,7 @@
 // address advances by 2*LBO per instruction in either view.
 #pragma once
 
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -72,6 +73,25 @@ __device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
 constexpr uint32_t kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
     uint32_t addr = smem_u32(mbar);
+#ifdef NS2B_DEBUG_HANG
+    {
+        const long long t0 = clock64();
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, P1;\n\t}\n"
+                : "=r"(done)
+                : "r"(addr), "r"(parity));
+            if (!done && clock64() - t0 > 4000000000LL) {
+                printf("HANG block %d thread %d mbar smem 0x%x parity %u\n", blockIdx.x, threadIdx.x, addr, parity);
+                __trap();
+            }
+        }
+        return;
+    }
+#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "LAB_WAIT:\n\t"
@@ -363,6 +383,35 @@ __device__ __forceinline__ void gemm2w(uint32_t tmem_d, const Operand &a, const 
         al += sa;
         bh += sb;
         mma2_elect(tmem_d, ah, al, bh, idesc, 1u);
+    }
+}
+
+// Two-term split for an A operand that is exact in fp16 (lo part zero): A B_hi + A B_lo;
+// only a.hi is read.
+__device__ __forceinline__ void mma2a_elect(uint32_t tmem_d, uint64_t ah, uint64_t bh, uint64_t bl, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t"
+        "setp.eq.b32 p, 1, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(ah), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate));
+}
+template <int NK>
+__device__ __forceinline__ void gemm2a(uint32_t tmem_d, const Operand &a, const Operand &b, uint32_t idesc,
+                                       bool accumulate) {
+    uint64_t ah = make_desc(a.hi, a.lbo, a.sbo);
+    uint64_t bh = make_desc(b.hi, b.lbo, b.sbo), bl = make_desc(b.lo, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+    mma2a_elect(tmem_d, ah, bh, bl, idesc, accumulate ? 1u : 0u);
+#pragma unroll 1
+    for (int k = 1; k < NK; ++k) {
+        ah += sa;
+        bh += sb;
+        bl += sb;
+        mma2a_elect(tmem_d, ah, bh, bl, idesc, 1u);
     }
 }
 
