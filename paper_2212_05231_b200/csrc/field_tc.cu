@@ -66,7 +66,8 @@ constexpr uint32_t TD = TC + 2 * TCB;                 // 128 x 16
 constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
 constexpr uint32_t TW = TEND;                         // 128 x 64 (backward: DMA'd A2c / A1)
-constexpr uint32_t SMEM_FWD = TEND;
+constexpr uint32_t WH1S = TEND;                       // forward: H1' = diag(H2[0]) H1, 64 x 48
+constexpr uint32_t SMEM_FWD = WH1S + 2 * WH1B;
 constexpr uint32_t SMEM_BWD = TW + 2 * T64B;
 
 // TMEM columns (512 allocated).  Forward:
@@ -191,32 +192,38 @@ __device__ __forceinline__ float absmax(const float *v) {
     return m;
 }
 
-// weights -> fp16 hi/lo tiles, each matrix scaled by its own power of two
+// weights -> fp16 hi/lo tiles, each matrix scaled by its own power of two.  With kH1S
+// (forward) a sixth tile holds H1' = diag(H2[0]) H1, so the j_d GEMM S1 H1 becomes
+// M1 H1' with the exact 0/1 ReLU mask M1 as its A operand.
+template <bool kH1S>
 __device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wmax, int *wexp) {
     const int E = 3 + 2 * f.L;
-    auto fetch = [&](int r, int c) -> float {  // row r of the stacked [H1|H2|C1|C2|C3] tiles
-        if (r < 64) {
+    constexpr int NM = kH1S ? 6 : 5, NR = kH1S ? 288 : 224;
+    auto fetch = [&](int r, int c) -> float {  // row r of the stacked [H1|H2|C1|C2|C3|H1'] tiles
+        if (r < 64 || r >= 224) {
+            const int rr = r < 64 ? r : r - 224;
             const int rc = h1_col(c, E);
-            return (c < 48 && rc >= 0) ? f.sdf_w[r * (E + 1) + rc] : 0.f;
+            const float v = (c < 48 && rc >= 0) ? f.sdf_w[rr * (E + 1) + rc] : 0.f;
+            return r < 64 ? v : v * f.sdf_w[H * (E + 1) + rr];
         }
         if (r < 80) return f.sdf_w[H * (E + 1) + (r - 64) * H + c];
         if (r < 144) return c < CIN ? f.color_w[(r - 80) * CIN + c] : 0.f;
         if (r < 208) return f.color_w[H * CIN + (r - 144) * H + c];
         return (r - 208) < 3 ? f.color_w[H * CIN + H * H + (r - 208) * H + c] : 0.f;
     };
-    auto mat = [](int r) { return r < 64 ? 0 : r < 80 ? 1 : r < 144 ? 2 : r < 208 ? 3 : 4; };
-    const int cols[5] = {48, 64, 32, 64, 64};
-    if (threadIdx.x < 5) wmax[threadIdx.x] = 0u;
+    auto mat = [](int r) { return r < 64 ? 0 : r < 80 ? 1 : r < 144 ? 2 : r < 208 ? 3 : r < 224 ? 4 : 5; };
+    const int cols[6] = {48, 64, 32, 64, 64, 48};
+    if (threadIdx.x < NM) wmax[threadIdx.x] = 0u;
     __syncthreads();
-    for (int r = threadIdx.x; r < 224; r += blockDim.x) {
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
         float m = 0.f;
         for (int c = 0; c < cols[mat(r)]; ++c) m = fmaxf(m, fabsf(fetch(r, c)));
         atomicMax(&wmax[mat(r)], __float_as_uint(m));
     }
     __syncthreads();
-    if (threadIdx.x < 5) wexp[threadIdx.x] = exp_for(__uint_as_float(wmax[threadIdx.x]));
+    if (threadIdx.x < NM) wexp[threadIdx.x] = exp_for(__uint_as_float(wmax[threadIdx.x]));
     __syncthreads();
-    for (int r = threadIdx.x; r < 224; r += blockDim.x) {
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
         float row[64];
         const int k = mat(r);
         for (int c = 0; c < 64; ++c) row[c] = c < cols[k] ? fetch(r, c) : 0.f;
@@ -225,7 +232,8 @@ __device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wm
         else if (k == 1) stage<64>(s, WH2, WH2B, r - 64, row, e);
         else if (k == 2) stage<32>(s, WC1, WC1B, r - 80, row, e);
         else if (k == 3) stage<64>(s, WC2, WC2B, r - 144, row, e);
-        else stage<64>(s, WC3, WC3B, r - 208, row, e);
+        else if (k == 4) stage<64>(s, WC3, WC3B, r - 208, row, e);
+        else stage<48>(s, WH1S, WH1B, r - 224, row, e);
     }
 }
 
@@ -361,16 +369,17 @@ struct MlpShared {
     uint32_t tmem_base;
     uint32_t slot_mx[2][NSLOT];
     int slot_pred[NSLOT];
-    uint32_t wmax[5];
-    int wexp[5];
+    uint32_t wmax[6];
+    int wexp[6];
     float h2row0[H];
 };
 
+template <bool kH1S>
 __device__ __forceinline__ void mlp_setup(const Smem &S, const FieldDev &f, MlpShared &sh, uint64_t *bars, int nbars) {
     const int t = threadIdx.x;
     const int E = 3 + 2 * f.L;
     if (t < H) sh.h2row0[t] = f.sdf_w[H * (E + 1) + t];
-    load_weight_tiles(S, f, sh.wmax, sh.wexp);
+    load_weight_tiles<kH1S>(S, f, sh.wmax, sh.wexp);
     if (t < NSLOT) {
         sh.slot_mx[0][t] = 0u;
         sh.slot_mx[1][t] = 0u;
@@ -384,12 +393,6 @@ __device__ __forceinline__ void mlp_setup(const Smem &S, const FieldDev &f, MlpS
     publish();
 }
 
-// |s1| <= max |H2[0]|: one staging exponent per CTA
-__device__ __forceinline__ int s1_exponent(const float *h2row0) {
-    float mh = 0.f;
-    for (int j = 0; j < H; ++j) mh = fmaxf(mh, fabsf(h2row0[j]));
-    return exp_for(mh);
-}
 
 // ---------------------------------------------------------------------------
 // MLP forward (field.py:208-244): per tile P0 Z1 = E H1^T; P1 a1 -> Y = A1 H2^T (SDF
@@ -409,7 +412,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
     const int qd = warp & 3, qt = warp >> 2;  // TMEM lane quadrant, column quarter
     const int r = 32 * qd + lane;              // sample row in the tile
     const int NA = f.n_active;
-    mlp_setup(S, f, sh, bars, 2);
+    mlp_setup<true>(S, f, sh, bars, 2);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
@@ -417,7 +420,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
     float *xch = reinterpret_cast<float *>(S.p(TZ));  // row-scalar exchange scratch (P1-P2)
     uint32_t phase = 0, phasee = 0;
     PredScale PS{sh.slot_mx, sh.slot_pred, 1};
-    const int eS1 = s1_exponent(h2row0);
+    const int eH1s = sh.wexp[5];
     const int P = *count;
     const int b0 = qt, b1 = qt + 4;  // my column blocks of 64-wide tiles
     float eik = 0.f;
@@ -487,7 +490,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         uint32_t m1 = 0u;  // my 16 hidden-unit mask bits (blocks b0, b1)
         int eA1;
         {
-            float z[2][8], s1[2][8], ma = 0.f, dpart = 0.f;
+            float z[2][8], ma = 0.f, dpart = 0.f;
             const float sc = pow2i(-(eE + eH1));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -499,7 +502,6 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                     m1 |= on ? (1u << (8 * i + k)) : 0u;
                     const float a = on ? z[i][k] * sc : 0.f;
                     z[i][k] = a;
-                    s1[i][k] = on ? h2row0[8 * b + k] : 0.f;
                     ma = fmaxf(ma, a);
                     // d = H2[0] a1 in fp32 FMAs: a cancelling sum the NeuS alpha
                     // differentiates along the ray (the MMA accumulator truncates)
@@ -515,9 +517,16 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], sa);
             };
             stg(eA1);
-            const float ss = pow2i(eS1);
+            // j_d = (H2[0] . m1) H1 = M1 H1': the mask is exact in fp16 (hi part only)
 #pragma unroll
-            for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, s1[i], ss);
+            for (int i = 0; i < 2; ++i) {
+                const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
+                auto h2 = [&](int k) {
+                    return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
+                };
+                *reinterpret_cast<uint4 *>(S.p(TY) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
+                    make_uint4(h2(0), h2(2), h2(4), h2(6));
+            }
             publish();
             PMARK(2);
             if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;  // next tile's slots (last read before this barrier)
@@ -530,7 +539,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
             umma::gemm3w<4>(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
-            umma::gemm3w<4>(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
+            umma::gemm2a<4>(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1S, WH1B, 48), ID_KM(48), false);
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
         }
@@ -547,7 +556,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             for (int o = 0; o < 16; ++o) y[o] *= scy;
             y[0] = d_sdf;
             // normal: my quarter's levels (+ the x rows for quarter 0), summed via smem
-            const float scd = pow2i(-(eS1 + eH1));
+            const float scd = pow2i(-eH1s);
             float p0 = 0.f, p1 = 0.f, p2 = 0.f;
             if (qt == 0) {
                 float jx[4];
@@ -787,14 +796,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     const int r = 32 * qd + lane;
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
-    mlp_setup(S, f, sh, bars, 6);
+    mlp_setup<false>(S, f, sh, bars, 6);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
     uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0;
     PredScale PS{sh.slot_mx, sh.slot_pred, 1};
-    const int eS1 = s1_exponent(h2row0);
     const int P = *count;
     const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
     const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
