@@ -1465,25 +1465,6 @@ static int agg_levels_env() {
     return v;
 }
 
-__device__ __forceinline__ void seg_red(float *gt, uint32_t row, float a, float b, int lane) {
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
-    const uint32_t next = __shfl_down_sync(0xffffffffu, row, 1);
-    const bool head = lane == 0 || prev != row;
-    const bool tail = lane == 31 || next != row;
-    const uint32_t heads = __ballot_sync(0xffffffffu, head);
-    const int seg_start = 31 - __clz(heads & ((2u << lane) - 1u));  // last head at or before lane
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan
-        const float pa = __shfl_up_sync(0xffffffffu, a, o);
-        const float pb = __shfl_up_sync(0xffffffffu, b, o);
-        if (lane - o >= seg_start) {
-            a += pa;
-            b += pb;
-        }
-    }
-    if (tail) red_add_f32x2(gt + 2 * row, a, b);
-}
-
 __device__ __forceinline__ void red_add_f32x4(float *addr, float a, float b, float c, float d) {
     atomicAdd(reinterpret_cast<float4 *>(addr), make_float4(a, b, c, d));
 }
@@ -1544,36 +1525,60 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
             cell_frac(un1, lv.n, cy, fy);
             cell_frac(un2, lv.n, cz, fz);
             float *gt = g_tab + l * f.T * 2;
-            // corner c = 4 ox + 2 oy + oz; handle the x-pairs (c, c + 4) together
+            // runs of equal cells along the warp's samples (consecutive samples of a ray):
+            // on the coarse levels all 8 corners of a run are pre-summed by one segmented
+            // scan and only the run's last lane issues the REDs
+            uint32_t heads = 0xFFFFFFFFu;
+            if (l < agg_levels) {
+                const uint64_t key = static_cast<uint64_t>(cx) | (static_cast<uint64_t>(cy) << 21) |
+                                     (static_cast<uint64_t>(cz) << 42);
+                const uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+                heads = __ballot_sync(0xFFFFFFFFu, lane == 0 || prev != key);
+            }
+            // corner c = 4 ox + 2 oy + oz
+            float a[8], b[8];
+            uint32_t row[8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int oy = (c >> 1) & 1, oz = c & 1;
-                const float wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                float a[2], b[2];
-                uint32_t row[2];
+            for (int c = 0; c < 8; ++c) {
+                const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                const float w = wx * wy * wz;
+                const float dwx = (ox ? sx : -sx) * (wy * wz);
+                const float dwy = (oy ? sy : -sy) * (wx * wz);
+                const float dwz = (oz ? sz : -sz) * (wx * wy);
+                const float qd = dwx * q0 + dwy * q1 + dwz * q2;
+                a[c] = valid ? fmaf(w, de0, jd0 * qd) : 0.f;
+                b[c] = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
+                row[c] = corner_row(lv, cx + ox, cy + oy, cz + oz);
+            }
+            if (heads != 0xFFFFFFFFu) {  // some run is longer than one sample (warp-uniform)
+                const int seg_start = 31 - __clz(heads & ((2u << lane) - 1u));
 #pragma unroll
-                for (int ox = 0; ox < 2; ++ox) {
-                    const float wx = ox ? fx : 1.f - fx;
-                    const float w = wx * wy * wz;
-                    const float dwx = (ox ? sx : -sx) * (wy * wz);
-                    const float dwy = (oy ? sy : -sy) * (wx * wz);
-                    const float dwz = (oz ? sz : -sz) * (wx * wy);
-                    const float qd = dwx * q0 + dwy * q1 + dwz * q2;
-                    a[ox] = valid ? fmaf(w, de0, jd0 * qd) : 0.f;
-                    b[ox] = valid ? fmaf(w, de1, jd1 * qd) : 0.f;
-                    row[ox] = corner_row(lv, cx + ox, cy + oy, cz + oz);
+                for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan of all 16 values
+                    const bool take = lane - o >= seg_start;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float pa = __shfl_up_sync(0xFFFFFFFFu, a[c], o);
+                        const float pb = __shfl_up_sync(0xFFFFFFFFu, b[c], o);
+                        if (take) {
+                            a[c] += pa;
+                            b[c] += pb;
+                        }
+                    }
                 }
-                if (l < agg_levels) {  // coarse levels: runs of equal rows along the rays
-                    seg_red(gt, row[0], a[0], b[0], lane);
-                    seg_red(gt, row[1], a[1], b[1], lane);
-                } else if (valid) {
-                    if ((row[0] ^ row[1]) == 1u) {  // both corners in one 16-B row pair
-                        const bool sw = row[0] & 1u;
-                        red_add_f32x4(gt + 2 * (row[0] & ~1u), sw ? a[1] : a[0], sw ? b[1] : b[0],
-                                      sw ? a[0] : a[1], sw ? b[0] : b[1]);
+                if (lane == 31 || ((heads >> (lane + 1)) & 1u))
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) red_add_f32x2(gt + 2 * row[c], a[c], b[c]);
+            } else if (valid) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {  // x-pairs (c, c + 4): one 16-B RED when adjacent
+                    if ((row[c] ^ row[c + 4]) == 1u) {
+                        const bool sw = row[c] & 1u;
+                        red_add_f32x4(gt + 2 * (row[c] & ~1u), sw ? a[c + 4] : a[c], sw ? b[c + 4] : b[c],
+                                      sw ? a[c] : a[c + 4], sw ? b[c] : b[c + 4]);
                     } else {
-                        red_add_f32x2(gt + 2 * row[0], a[0], b[0]);
-                        red_add_f32x2(gt + 2 * row[1], a[1], b[1]);
+                        red_add_f32x2(gt + 2 * row[c], a[c], b[c]);
+                        red_add_f32x2(gt + 2 * row[c + 4], a[c + 4], b[c + 4]);
                     }
                 }
             }
