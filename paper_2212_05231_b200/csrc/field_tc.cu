@@ -669,7 +669,6 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
             };
             stg(eA1c);
-            if (t == 0) umma::bulk_wait_read();  // A1 has left TX before P4 restages it
             publish();
             PMARK(8);
             if (!PS.check(kA1c, eA1c)) {
@@ -705,9 +704,9 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, z[i], s);
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, z[i], s);
             };
-            stg(eA2c);
+            stg(eA2c);  // into TY (the mask tile is dead): TX's A1 store may still be reading
             publish();
             PMARK(11);
             if (!PS.check(kA2c, eA2c)) {
@@ -717,9 +716,9 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
         }
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
-            umma::gemm3w<4>(tb + TM_SA, S.K(TX, T64B, 64), S.K(WC3, WC3B, 64), ID_KK(16), false);
+            umma::gemm3w<4>(tb + TM_SA, S.K(TY, T64B, 64), S.K(WC3, WC3B, 64), ID_KK(16), false);
             umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_A2C, S.p(TX), 2 * T64B);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A2C, S.p(TY), 2 * T64B);
             if (lane == 0) ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
         ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
@@ -937,6 +936,34 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             j_store();
         }
     }
+    // per-sample inputs of a tile, loaded a tile ahead (their latency then hides behind
+    // the previous tile's last phase instead of stalling B0)
+    struct BwdIn {
+        float gc0, gc1, gc2, cc0, cc1, cc2, gd, n0, n1, n2;
+        uint2 mk;
+    };
+    auto load_in = [&](int64_t tl) {
+        BwdIn v{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, make_uint2(0u, 0u)};
+        const int64_t pp = tl * TILE + r;
+        v.mk = ws.fw_mask[(tl * 4 + qt) * TILE + r];
+        if (pp < P) {
+            const float *nc = ws.fw_nc + tl * NCROWS * TILE + r;
+            if (qt == 0) {
+                v.gc0 = dl_dc[3 * pp];
+                v.gc1 = dl_dc[3 * pp + 1];
+                v.gc2 = dl_dc[3 * pp + 2];
+                v.cc0 = nc[3 * TILE];
+                v.cc1 = nc[4 * TILE];
+                v.cc2 = nc[5 * TILE];
+                v.gd = dl_dsdf[pp];
+            }
+            v.n0 = nc[0];
+            v.n1 = nc[TILE];
+            v.n2 = nc[2 * TILE];
+        }
+        return v;
+    };
+    BwdIn in = load_in(blockIdx.x);
     int ntiles_done = 0;
 #ifdef NS2B_PHASE_PROF
     __shared__ long long pacc[64];
@@ -964,26 +991,16 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             umma::prefetch_l2(dl_dc + 3 * ntile * TILE, (12 * nb + 15) & ~15u);
             umma::prefetch_l2(dl_dsdf + ntile * TILE, (4 * nb + 15) & ~15u);
         }
-        // per-sample inputs
-        const float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
-        const uint2 mk = ws.fw_mask[(tile * 4 + qt) * TILE + r];
-        const uint32_t m1 = mk.x & 0xFFFFu, mc1 = mk.x >> 16, mc2 = mk.y;
+        // per-sample inputs (loaded at the end of the previous tile)
+        const uint32_t m1 = in.mk.x & 0xFFFFu, mc1 = in.mk.x >> 16, mc2 = in.mk.y;
         const int4 fe = ws.fw_exp[tile];
         const int eA1 = fe.x, eCin = fe.y, eA1c = fe.z, eA2c = fe.w;
         const int eE = ws.e_exp[tile];
-        float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gd = 0.f, gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
-        float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;
-        if (valid && qt == 0) {
-            gc0 = dl_dc[3 * p];
-            gc1 = dl_dc[3 * p + 1];
-            gc2 = dl_dc[3 * p + 2];
-            cc0 = nct[3 * TILE];
-            cc1 = nct[4 * TILE];
-            cc2 = nct[5 * TILE];
-        }
-        if (valid && qt <= 1) gd = dl_dsdf[p];
+        const float gc0 = in.gc0, gc1 = in.gc1, gc2 = in.gc2, gd = in.gd;
+        const float cc0 = in.cc0, cc1 = in.cc1, cc2 = in.cc2;
+        float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
         if (valid) {
-            const float n0 = nct[0], n1 = nct[TILE], n2 = nct[2 * TILE];
+            const float n0 = in.n0, n1 = in.n1, n2 = in.n2;
             if (dl_dn_extra) {
                 gn0 = dl_dn_extra[3 * p];
                 gn1 = dl_dn_extra[3 * p + 1];
@@ -1287,7 +1304,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
             }
-            if (has_next) j_store();
+            if (has_next) {
+                j_store();
+                in = load_in(ntile);
+            }
         }
         // Tile boundary barrier: without it a warp can run into the next tile while another
         // is still in B5; observed to deadlock on the c1 field (mbarw never completing),
