@@ -1315,7 +1315,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         publish();
         if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run (all MMAs done)
             ntiles_done = 0;
-#pragma unroll 1
+#pragma unroll  // compile-time j: acc_e / acc_live stay in registers
             for (int j = 0; j < NACC; ++j)
                 if (acc_live[j]) fold(j);
             block_sync_tc();
@@ -1323,7 +1323,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     }
     if (warp == 0) umma::commit_elect(mbarw);
     wait_mma(mbarw, phasew);
-#pragma unroll 1
+#pragma unroll
     for (int j = 0; j < NACC; ++j)
         if (acc_live[j]) fold(j);
 #ifdef NS2B_PHASE_PROF
