@@ -460,6 +460,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
     if (t < 64) pacc[t] = 0;
     __syncthreads();
 #endif
+    int eE_cur = static_cast<int64_t>(blockIdx.x) * TILE < P ? ws.e_exp[blockIdx.x] : 0;
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * TILE; base < P;
          base += static_cast<int64_t>(gridDim.x) * TILE) {
         const int64_t p = base + r;
@@ -474,7 +475,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const float *xvt = ws.xv + tile * XVROWS * TILE + r;
         const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
         const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
-        const int eE = ws.e_exp[tile];
+        const int eE = eE_cur;  // loaded during the previous tile
         // ------------------------------------------------ P0: Z1 = E H1^T
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
             if (lane == 0) umma::bulk_wait_read();  // the previous tile's tile stores have left smem
@@ -547,6 +548,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         PMARK(4);
         // ------------------------------------------------ P2: normal, cin -> Zc1
         int eCin;
+        if (ntile * TILE < P) eE_cur = ws.e_exp[ntile];  // next tile's E exponent, a tile ahead
         {
             float y[16];
             umma::tmem_ld8(my + TM_SB, *reinterpret_cast<float(*)[8]>(y));
