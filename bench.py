@@ -425,7 +425,8 @@ def run_ours(args, wl):
     wl["_dataset"] = ds
     cpu = None
     if not args.no_cpu:
-        rays_sample = 1024 if args.config == "c2" else wl["rays"]
+        rays_sample = 16384 if args.config == "c2" else wl["rays"]
+        cpu_oracle_rate(wl, 1024 if args.config == "c2" else wl["rays"], steps=1)  # warm-up
         rate, sec, Pc, cores = cpu_oracle_rate(wl, rays_sample, steps=1)
         cpu = {"value": rate, "unit": "rays/s", "cores": cores, "kind": "port",
                "sample": f"1 oracle train_step on a {rays_sample}-ray sub-batch of the workload "
