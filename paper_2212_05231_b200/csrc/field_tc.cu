@@ -1575,8 +1575,10 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
             }
             if (heads != 0xFFFFFFFFu) {  // some run is longer than one sample (warp-uniform)
                 const int seg_start = 31 - __clz(heads & ((2u << lane) - 1u));
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan of all 16 values
+                // only as many scan steps as the longest run needs
+                const int maxrun = static_cast<int>(__reduce_max_sync(0xFFFFFFFFu, lane - seg_start + 1));
+#pragma unroll 1
+                for (int o = 1; o < maxrun; o <<= 1) {  // segmented inclusive scan of all 16 values
                     const bool take = lane - o >= seg_start;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
