@@ -67,7 +67,8 @@ constexpr uint32_t TDB = TILE * 16 * 2;
 constexpr uint32_t TEND = TD + 2 * TDB;
 constexpr uint32_t TW = TEND;                         // 128 x 64 (backward: DMA'd A2c / A1)
 constexpr uint32_t WH1S = TEND;                       // forward: H1' = diag(H2[0]) H1, 64 x 48
-constexpr uint32_t SMEM_FWD = WH1S + 2 * WH1B;
+constexpr uint32_t TLG = WH1S + 2 * WH1B;             // forward: per-quarter logit partials [4][3][128] fp32
+constexpr uint32_t SMEM_FWD = TLG + 4 * 3 * TILE * 4;
 constexpr uint32_t SMEM_BWD = TW + 2 * T64B;
 
 // TMEM columns (512 allocated).  Forward:
@@ -372,6 +373,7 @@ struct MlpShared {
     uint32_t wmax[6];
     int wexp[6];
     float h2row0[H];
+    float c3[3][H];  // colour output layer (fp32): logits / u2 as FMA dot products
 };
 
 template <bool kH1S>
@@ -379,6 +381,7 @@ __device__ __forceinline__ void mlp_setup(const Smem &S, const FieldDev &f, MlpS
     const int t = threadIdx.x;
     const int E = 3 + 2 * f.L;
     if (t < H) sh.h2row0[t] = f.sdf_w[H * (E + 1) + t];
+    if (t < 3 * H) sh.c3[t / H][t % H] = f.color_w[H * CIN + H * H + t];
     load_weight_tiles<kH1S>(S, f, sh.wmax, sh.wexp);
     if (t < NSLOT) {
         sh.slot_mx[0][t] = 0u;
@@ -413,7 +416,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
     const int r = 32 * qd + lane;              // sample row in the tile
     const int NA = f.n_active;
     mlp_setup<true>(S, f, sh, bars, 2);
-    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
+    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
@@ -703,6 +706,25 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
             eA2c = PS.guess(kA2c);
             PS.contrib(kA2c, m);
+            // logits = C3 a2c (3 outputs): fp32 FMA partials over my 16 hidden units,
+            // summed across the four quarter-threads of the row after the barrier
+            {
+                float lp0 = 0.f, lp1 = 0.f, lp2 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int b = i ? b1 : b0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        lp0 = fmaf(sh.c3[0][8 * b + k], z[i][k], lp0);
+                        lp1 = fmaf(sh.c3[1][8 * b + k], z[i][k], lp1);
+                        lp2 = fmaf(sh.c3[2][8 * b + k], z[i][k], lp2);
+                    }
+                }
+                float *lg = reinterpret_cast<float *>(S.p(TLG)) + 3 * qt * TILE + r;
+                lg[0] = lp0;
+                lg[TILE] = lp1;
+                lg[2 * TILE] = lp2;
+            }
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
@@ -717,22 +739,23 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 PMARK(12);
             }
         }
-        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
-            umma::gemm3w<4>(tb + TM_SA, S.K(TY, T64B, 64), S.K(WC3, WC3B, 64), ID_KK(16), false);
-            umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_A2C, S.p(TY), 2 * T64B);
-            if (lane == 0) ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
+        if (t == 0) {
+            umma::bulk_s2g(fwt + FW_A2C, S.p(TY), 2 * T64B);
+            ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
         ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
-        wait_mma(mbar, phase);
-        PMARK(13);
         // ------------------------------------------------ P5: colours
         {
-            float lg[4];
-            umma::tmem_ld4(my + TM_SA, lg);  // (warp-collective; quarter 0 uses it)
             if (qt == 0) {
-                const float sc = pow2i(-(eA2c + eC3));
-                const float cc0 = sigmoid_f(lg[0] * sc), cc1 = sigmoid_f(lg[1] * sc), cc2 = sigmoid_f(lg[2] * sc);
+                const float *lg = reinterpret_cast<const float *>(S.p(TLG)) + r;
+                float l0 = 0.f, l1 = 0.f, l2 = 0.f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    l0 += lg[3 * q * TILE];
+                    l1 += lg[(3 * q + 1) * TILE];
+                    l2 += lg[(3 * q + 2) * TILE];
+                }
+                const float cc0 = sigmoid_f(l0), cc1 = sigmoid_f(l1), cc2 = sigmoid_f(l2);
                 nct[3 * TILE] = cc0;
                 nct[4 * TILE] = cc1;
                 nct[5 * TILE] = cc2;
