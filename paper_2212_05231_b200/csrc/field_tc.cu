@@ -800,49 +800,21 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 // accumulate in TMEM across tiles while their operand exponents stay the same (sticky
 // predictions), and are folded into global memory every kFoldTiles tiles, when an
 // exponent changes, and at the end.
-constexpr int kFoldTiles = 32;
 enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, NACC };
 
-__global__ void __launch_bounds__(MLP_THREADS, 1)
-field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
-                 const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
-                 const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
-                 Workspace ws) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // [0] chain MMAs, [1] weight-gradient MMAs, [2..5] DMA into TW, TZ, TC, TE
-    __shared__ uint64_t bars[6];
-    __shared__ MlpShared sh;
-    uint64_t *mbar = bars, *mbarw = bars + 1, *mb_w = bars + 2, *mb_z = bars + 3, *mb_c = bars + 4,
-             *mb_e = bars + 5;
-    const Smem S{smem_raw};
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+// Fold one TMEM weight-gradient accumulator (scaled by 2^-e) into global memory.  All
+// threads call it; the accumulator's MMAs have completed.  Out of line: it runs only
+// every kFoldTiles tiles or on a scale change, and inlining its 18 call sites made the
+// backward kernel's code overflow the instruction cache.
+__device__ __noinline__ void fold_acc(int j, int e, uint32_t my, int E, const float *__restrict__ h2row0,
+                                      const float *__restrict__ sdf_w, float *__restrict__ g_sdf,
+                                      float *__restrict__ g_color) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qd = warp & 3, qt = warp >> 2;
-    const int r = 32 * qd + lane;
-    const int E = 3 + 2 * f.L;
-    const int NA = f.n_active;
-    mlp_setup<false>(S, f, sh, bars, 6);
-    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
-    const float *h2row0 = sh.h2row0;
-    const uint32_t tb = sh.tmem_base;
-    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0;
-    PredScale PS{sh.slot_mx, sh.slot_pred, 1};
-    const int P = *count;
-    const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
-    const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
+    const int jrow = 16 * qd + lane;
     const int b0 = qt, b1 = qt + 4;
-    const int nsdf = H * (E + 1) + NOUT * H;
-
-    // ---- weight-gradient accumulators (TMEM) and their folds into global memory
-    int acc_e[NACC];
-    bool acc_live[NACC];
-#pragma unroll
-    for (int j = 0; j < NACC; ++j) {
-        acc_e[j] = 0;
-        acc_live[j] = false;
-    }
-    auto fold = [&](int j) {  // all threads; the accumulator's MMAs have completed
-        const float sc = pow2i(-acc_e[j]);
+    {
+        const float sc = pow2i(-e);
         float d[8];
         switch (j) {
         case aC3:  // dC3^T: row = hidden unit, col = output (3)
@@ -899,7 +871,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                         const int rc = h1_col(8 * b + k, E);
                         if (rc >= 0) {
                             atomicAdd(g_sdf + jrow * (E + 1) + rc, h2j * d[k] * sc);
-                            dot = fmaf(f.sdf_w[jrow * (E + 1) + rc], d[k], dot);
+                            dot = fmaf(sdf_w[jrow * (E + 1) + rc], d[k], dot);
                         }
                     }
             }
@@ -907,6 +879,51 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             break;
         }
         }
+    }
+}
+
+constexpr int kFoldTiles = 32;
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
+                 const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
+                 const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
+                 Workspace ws) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // [0] chain MMAs, [1] weight-gradient MMAs, [2..5] DMA into TW, TZ, TC, TE
+    __shared__ uint64_t bars[6];
+    __shared__ MlpShared sh;
+    uint64_t *mbar = bars, *mbarw = bars + 1, *mb_w = bars + 2, *mb_z = bars + 3, *mb_c = bars + 4,
+             *mb_e = bars + 5;
+    const Smem S{smem_raw};
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int qd = warp & 3, qt = warp >> 2;
+    const int r = 32 * qd + lane;
+    const int E = 3 + 2 * f.L;
+    const int NA = f.n_active;
+    mlp_setup<false>(S, f, sh, bars, 6);
+    const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
+    const float *h2row0 = sh.h2row0;
+    const uint32_t tb = sh.tmem_base;
+    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0;
+    PredScale PS{sh.slot_mx, sh.slot_pred, 1};
+    const int P = *count;
+    const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
+    const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
+    const int b0 = qt, b1 = qt + 4;
+    const int nsdf = H * (E + 1) + NOUT * H;
+
+    // ---- weight-gradient accumulators (TMEM) and their folds into global memory
+    int acc_e[NACC];
+    bool acc_live[NACC];
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) {
+        acc_e[j] = 0;
+        acc_live[j] = false;
+    }
+    auto fold = [&](int j) {
+        fold_acc(j, acc_e[j], my, E, h2row0, f.sdf_w, g_sdf, g_color);
         acc_live[j] = false;
     };
     // before a weight-gradient GEMM into j with operand exponent sum e: fold on a scale
