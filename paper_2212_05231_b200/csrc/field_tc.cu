@@ -673,13 +673,13 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TZ, T64B, r, i ? b1 : b0, z[i], s);
             };
-            stg(eA1c);
-            publish();
-            PMARK(8);
-            if (!PS.check(kA1c, eA1c)) {
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 stg(eA1c);
                 publish();
-                PMARK(9);
+                if (pass) break;
+                PMARK(8);
+                if (PS.check(kA1c, eA1c)) break;
             }
         }
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
@@ -730,13 +730,13 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, z[i], s);
             };
-            stg(eA2c);  // into TY (the mask tile is dead): TX's A1 store may still be reading
-            publish();
-            PMARK(11);
-            if (!PS.check(kA2c, eA2c)) {
-                stg(eA2c);
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
+                stg(eA2c);  // into TY (the mask tile is dead): TX's A1 store may still be reading
                 publish();
-                PMARK(12);
+                if (pass) break;
+                PMARK(11);
+                if (PS.check(kA2c, eA2c)) break;
             }
         }
         if (t == 0) {
@@ -1069,14 +1069,14 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
             eD = PS.guess(kDlog);
             PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
-            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
-            publish();
-            PMARK(1);
-            if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;
-            if (!PS.check(kDlog, eD)) {
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
                 publish();
-                PMARK(2);
+                if (pass) break;
+                PMARK(1);
+                if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;
+                if (PS.check(kDlog, eD)) break;
             }
         }
         {
@@ -1112,13 +1112,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
             };
-            stg(eU2);
-            publish();
-            PMARK(4);
-            if (!PS.check(kU2, eU2)) {
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 stg(eU2);
                 publish();
-                PMARK(5);
+                if (pass) break;
+                PMARK(4);
+                if (PS.check(kU2, eU2)) break;
             }
         }
         {
@@ -1154,13 +1154,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
 #pragma unroll
                 for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
             };
-            stg(eU1);
-            publish();
-            PMARK(7);
-            if (!PS.check(kU1, eU1)) {
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 stg(eU1);
                 publish();
-                PMARK(8);
+                if (pass) break;
+                PMARK(7);
+                if (PS.check(kU1, eU1)) break;
             }
         }
         {
@@ -1210,13 +1210,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(blk[k]));
             eDLY = PS.guess(kDly);
             PS.contrib(kDly, m);
-            if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
-            publish();
-            PMARK(10);
-            if (!PS.check(kDly, eDLY)) {
+            #pragma unroll 1
+            for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
                 publish();
-                PMARK(11);
+                if (pass) break;
+                PMARK(10);
+                if (PS.check(kDly, eDLY)) break;
             }
         }
         {
