@@ -481,9 +481,13 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const int eE = eE_cur;  // loaded during the previous tile
         // ------------------------------------------------ P0: Z1 = E H1^T
         if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
-            if (lane == 0) umma::bulk_wait_read();  // the previous tile's tile stores have left smem
             umma::mbar_wait(mbare, phasee);
             umma::gemm3w<3>(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
+            // the previous tile's tile stores must have left smem before P1 restages it:
+            // wait for them while Z1 runs; committing afterwards orders every thread's
+            // P1 staging (which waits on this commit) after the drain
+            if (lane == 0) umma::bulk_wait_read();
+            __syncwarp();
             umma::commit_elect(mbar);
         }
         phasee ^= 1u;
