@@ -1233,26 +1233,11 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
             ph_w ^= 1u;
         }
-        wait_mma(mbar, phase);
-        PMARK(12);
-        // ------------------------------------------------ B4: u, mvec -> DE, PV, dH1
-        // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
-        if (t == 0 && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
-        int eU, eMV;
-        {
-            float u[2][8], mu = 0.f;
-            const float sc4 = pow2i(-(eDLY + eH2));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
-                    mu = fmaxf(mu, fabsf(u[i][k]));
-                }
-            }
-            // mvec = [J q (features), q, 0] (field.py:326-327); quarter k: block k
-            // (levels 4k..4k+3) and block k+4 (block 4 holds q)
+        // While U = DLY H2 runs: mvec = [J q (features), q, 0] (field.py:326-327) -> MV (TZ)
+        // and the ReLU mask M1 -> TY (exact in fp16: hi part only), both for B4's
+        // G = M1^T MV.  TZ / TY are free (A1c / U2 were last read by B1's GEMMs).
+        // Quarter k stages block k (levels 4k..4k+3) and block k+4 (block 4 holds q).
+        auto mv_stage = [&](int emv) -> float {
             float mv[2][8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -1277,34 +1262,55 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             float mm = 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
-            eU = PS.guess(kU);
-            eMV = PS.guess(kMv);
-            PS.contrib(kU, mu);
-            PS.contrib(kMv, mm);
-            auto stg = [&](int eu, int emv) {
-                const float su = pow2i(eu), sm = pow2i(emv);
+            const float sm = pow2i(emv);
+            stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
+            if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
+            return mm;
+        };
+        int eMV = PS.guess(kMv);
+        PS.contrib(kMv, mv_stage(eMV));
 #pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], su);
-                stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
-                if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
+            auto h2 = [&](int k) {
+                return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
             };
-            stg(eU, eMV);
-            // the ReLU mask M1 (exact in fp16: hi part only) for G = M1^T MV
+            *reinterpret_cast<uint4 *>(S.p(TY) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
+                make_uint4(h2(0), h2(2), h2(4), h2(6));
+        }
+        wait_mma(mbar, phase);
+        PMARK(12);
+        // ------------------------------------------------ B4: u -> DE, dH1, G
+        // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
+        if (t == 0 && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
+        int eU;
+        {
+            float u[2][8], mu = 0.f;
+            const float sc4 = pow2i(-(eDLY + eH2));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
-                auto h2 = [&](int k) {
-                    return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
-                };
-                *reinterpret_cast<uint4 *>(S.p(TY) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
-                    make_uint4(h2(0), h2(2), h2(4), h2(6));
+                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
+                    mu = fmaxf(mu, fabsf(u[i][k]));
+                }
             }
+            eU = PS.guess(kU);
+            PS.contrib(kU, mu);
+            auto stg = [&](int eu) {
+                const float su = pow2i(eu);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], su);
+            };
+            stg(eU);
             publish();
             PMARK(13);
             const bool oku = PS.check(kU, eU);
             const bool okm = PS.check(kMv, eMV);
-            if (!(oku && okm)) {
-                stg(eU, eMV);
+            if (!(oku && okm)) {  // (uniform) restage whichever missed its exponent window
+                if (!oku) stg(eU);
+                if (!okm) mv_stage(eMV);
                 publish();
                 PMARK(14);
             }
