@@ -317,6 +317,9 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
 // quarter k owns blocks k and k+4 of a tile.  Row scalars (the SDF value, the normal)
 // are combined through shared memory.  One elected thread issues all MMAs.
 constexpr int MLP_THREADS = 512;
+// The warp that issues every tcgen05.mma / commit (and the forward's tile stores): a
+// quarter-3 warp, whose epilogue share is the lightest (quarter 0 owns the row scalars).
+constexpr int kMmaWarp = 15;
 
 // Predicted staging exponents.  The exponent a tile is staged with only has to keep its
 // maximum inside fp16's range with the lo parts normal, so instead of a block-wide max
@@ -480,7 +483,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
         const int eE = eE_cur;  // loaded during the previous tile
         // ------------------------------------------------ P0: Z1 = E H1^T
-        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+        if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::mbar_wait(mbare, phasee);
             umma::gemm3w<3>(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
             // the previous tile's tile stores must have left smem before P1 restages it:
@@ -545,7 +548,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
         }
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
-        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+        if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<4>(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
             umma::gemm2a<4>(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1S, WH1B, 48), ID_KM(48), false);
             umma::commit_elect(mbar);
@@ -643,7 +646,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 PMARK(6);
             }
         }
-        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+        if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<2>(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), ID_KK(64), false);
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
@@ -686,7 +689,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 if (PS.check(kA1c, eA1c)) break;
             }
         }
-        if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+        if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<4>(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), ID_KK(64), false);
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
@@ -743,7 +746,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 if (PS.check(kA2c, eA2c)) break;
             }
         }
-        if (t == 0) {
+        if (t == kMmaWarp * 32) {  // the thread that issues (and drains) the tile stores
             umma::bulk_s2g(fwt + FW_A2C, S.p(TY), 2 * T64B);
             ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
@@ -784,7 +787,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         double v = warp_sum(static_cast<double>(eik));
         if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
     }
-    if (t == 0) umma::bulk_wait_all();
+    if (t == kMmaWarp * 32) umma::bulk_wait_all();
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tb, 512);
@@ -1085,7 +1088,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
         {
             const bool acc = acc_begin(aC3, eA2c + eD);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<1>(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_w, ph_w));
@@ -1127,7 +1130,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
         {
             const bool acc = acc_begin(aC2, eU2 + eA1c);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<4>(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_z, ph_z));
@@ -1169,7 +1172,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
         {
             const bool acc = acc_begin(aC1, eU1 + eCin);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), ID_KM(32), false);
                 umma::commit_elect(mbar);
                 // TW is free: dC3 (B0) completed before B1's chain GEMM did
@@ -1225,7 +1228,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
         {
             const bool acc = acc_begin(aH2, eA1 + eDLY);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<1>(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_w, ph_w));
@@ -1321,7 +1324,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             // (both applied when G is folded), so pvec = m1 . (H1 mvec) never materialises.
             const bool acca = acc_begin(aH1a, eU + eE);
             const bool accb = acc_begin(aH1b, eMV);
-            if (warp == 0) {  // converged warp 0; elect.sync picks the issuing lane
+            if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_e, ph_e));
