@@ -320,6 +320,8 @@ constexpr int MLP_THREADS = 512;
 // The warp that issues every tcgen05.mma / commit (and the forward's tile stores): a
 // quarter-3 warp, whose epilogue share is the lightest (quarter 0 owns the row scalars).
 constexpr int kMmaWarp = 15;
+// The thread that issues the bulk DMAs and L2 prefetches (another quarter-3 warp).
+constexpr int kDmaThread = 14 * 32;
 
 // Predicted staging exponents.  The exponent a tile is staged with only has to keep its
 // maximum inside fp16's range with the lo parts normal, so instead of a block-wide max
@@ -453,7 +455,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         umma::tmem_st_wait();
     };
     auto e_fetch = [&](int64_t tl) {
-        if (t == 0 && tl * TILE < P) umma::bulk_g2s(S.p(TE), ws.e_tiles + tl * 2 * TEB, 2 * TEB, mbare);
+        if (t == kDmaThread && tl * TILE < P) umma::bulk_g2s(S.p(TE), ws.e_tiles + tl * 2 * TEB, 2 * TEB, mbare);
     };
     e_fetch(blockIdx.x);
     if (static_cast<int64_t>(blockIdx.x) * TILE < P) {
@@ -477,7 +479,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         float *SBt = ws.sb + tile * SBROWS * TILE;
         uint8_t *fwt = ws.fw_tiles + tile * static_cast<int64_t>(FWB);
         float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
-        if (t == 0 && ntile * TILE < P) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
+        if (t == kDmaThread && ntile * TILE < P) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
         const float *xvt = ws.xv + tile * XVROWS * TILE + r;
         const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
         const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
@@ -975,7 +977,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     {
         const int64_t t0 = blockIdx.x;
         if (t0 * TILE < P) {
-            if (t == 0) {
+            if (t == kDmaThread) {
                 dma(TW, fwt(t0) + FW_A2C, 2 * T64B, mb_w);
                 dma(TZ, fwt(t0) + FW_A1C, 2 * T64B, mb_z);
                 dma(TC, fwt(t0) + FW_CIN, 2 * TCB, mb_c);
@@ -1029,7 +1031,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         const bool has_next = ntile * TILE < P;
         PS.par ^= 1;
         float *SBt = ws.sb + tile * SBROWS * TILE;
-        if (t == 0 && has_next) {  // next tile's inputs -> L2 while this one runs
+        if (t == kDmaThread && has_next) {  // next tile's inputs -> L2 while this one runs
             umma::prefetch_l2(fwt(ntile), FWB);
             umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
             umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, 2 * TEB);
@@ -1285,7 +1287,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         PMARK(12);
         // ------------------------------------------------ B4: u -> DE, dH1, G
         // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
-        if (t == 0 && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
+        if (t == kDmaThread && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
         int eU;
         {
             float u[2][8], mu = 0.f;
@@ -1338,7 +1340,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         PMARK(15);
         // ------------------------------------------------ B5: scatter inputs; next tile's DMAs
         // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
-        if (t == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
+        if (t == kDmaThread && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
         if (has_next) j_load(ntile);  // TMEM J is dead after B4
         {
             // dL/dfeature pairs (DE) and q for the scatter kernel
@@ -1355,7 +1357,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
             wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
             PMARK(16);
-            if (t == 0 && has_next) {
+            if (t == kDmaThread && has_next) {
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
             }
