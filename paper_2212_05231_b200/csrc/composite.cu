@@ -76,12 +76,21 @@ composite_kernel(const int32_t *__restrict__ offsets, int64_t nrays, const float
         double C0 = 0.0, C1 = 0.0, C2 = 0.0;
         if (kMode & kFwd) {
             double carry = 0.0;
+            // Phi of each sample is computed once: lane l holds sample b + l of the current
+            // 32-sample window; interval i's cj is the next lane's value (lane 31: the next
+            // window's first)
+            double phi = (nint > 0 && lane < n) ? logistic_cdf(s, static_cast<double>(sdf[start + lane])) : 0.0;
             for (int b = 0; b < nint; b += 32) {
                 const int i = b + lane;
+                const int nx = b + 32 + lane;
+                const double phi_next = nx < n ? logistic_cdf(s, static_cast<double>(sdf[start + nx])) : 0.0;
+                double up = __shfl_down_sync(0xffffffffu, phi, 1);
+                const double first_next = __shfl_sync(0xffffffffu, phi_next, 0);
+                if (lane == 31) up = first_next;
                 double a = 0.0, lg = 0.0;
                 if (i < nint) {
-                    const double ci = logistic_cdf(s, static_cast<double>(sdf[start + i]));
-                    const double cj = logistic_cdf(s, static_cast<double>(sdf[start + i + 1]));
+                    const double ci = phi;
+                    const double cj = up;
                     a = (ci - cj) / ci;
                     a = fmin(fmax(a, 0.0), kAlphaMax);
                     lg = log1p(-a);
@@ -99,6 +108,7 @@ composite_kernel(const int32_t *__restrict__ offsets, int64_t nrays, const float
                     tb[q] = T;
                 }
                 carry += __shfl_sync(0xffffffffu, incl, 31);
+                phi = phi_next;
             }
             C0 = warp_sum(C0);
             C1 = warp_sum(C1);
@@ -133,9 +143,21 @@ composite_kernel(const int32_t *__restrict__ offsets, int64_t nrays, const float
             double suffix = 0.0;   // sum over intervals of later chunks
             double next_ci = 0.0;  // interval (b+32)'s dalpha/df_i term, for lane 31
             const int nchunks = (nint + 31) >> 5;
+            // Phi once per sample again, windows walked back to front (phi_w: the window
+            // after the current chunk, whose lane 0 is lane 31's cj)
+            double phi_w = 0.0;
+            if (nint > 0) {
+                const int w0 = nchunks * 32 + lane;
+                phi_w = w0 < n ? logistic_cdf(s, static_cast<double>(sdf[start + w0])) : 0.0;
+            }
             for (int ch = nchunks - 1; ch >= 0; --ch) {
                 const int i = ch * 32 + lane;
                 const bool ok = i < nint;
+                const double phi_c = i < n ? logistic_cdf(s, static_cast<double>(sdf[start + i])) : 0.0;
+                double phi_up = __shfl_down_sync(0xffffffffu, phi_c, 1);
+                const double first_w = __shfl_sync(0xffffffffu, phi_w, 0);
+                if (lane == 31) phi_up = first_w;
+                phi_w = phi_c;
                 double wa = 0.0, a = 0.0, w = 0.0, T = 0.0, adot = 0.0;
                 if (ok) {
                     const int64_t q = start + i;
@@ -153,7 +175,7 @@ composite_kernel(const int32_t *__restrict__ offsets, int64_t nrays, const float
                     const double dl_da = T * adot - S / (1.0 - a);
                     const int64_t q = start + i;
                     const double fi = static_cast<double>(sdf[q]), fj = static_cast<double>(sdf[q + 1]);
-                    const double ci = logistic_cdf(s, fi), cj = logistic_cdf(s, fj);
+                    const double ci = phi_c, cj = phi_up;
                     const double raw = (ci - cj) / ci;
                     if (raw > 0.0 && raw < kAlphaMax) {
                         const double dpi = s * ci * (1.0 - ci);
