@@ -412,13 +412,26 @@ def run_ours(args, wl):
     red_ops = Pl * 8 * L
     kern["field_scatter"]["red_gops"] = red_ops / (per_kernel["field_scatter"] * 1e-3) / 1e9
     kern["field_scatter"]["red_frac_of_probe"] = kern["field_scatter"]["red_gops"] / l2["red_f32x2_gops"]
+    # DRAM traffic per launch from the committed ncu capture (bench.py cannot run ncu
+    # itself): bytes moved and the DRAM bandwidth that implies at this run's kernel time
+    traffic = {}
+    tp = ROOT / "profiles" / "r01_dram_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("kernels", {})
+    for k, v in kern.items():
+        if k in traffic:
+            v["dram_traffic_bytes"] = traffic[k]["traffic"]
+            v["dram_gbs"] = traffic[k]["traffic"] / (per_kernel[k] * 1e-3) / 1e9
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": d["unit"], "frac": d["frac"],
                 "peak_source": "MEASURED_PEAKS.json (" + peaks["source"] + "): "
                                + ("hbm_gbs" if d["unit"] == "GB/s" else "bf16_tflops_sustained"),
-                "traffic": None, "algorithmic_per_sample": d["per_sample"],
+                "traffic": d.get("dram_traffic_bytes"),
+                "traffic_source": "profiles/r01_dram_traffic.json (ncu dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum, one launch)" if "dram_traffic_bytes" in d else None,
+                "algorithmic_per_sample": d["per_sample"],
                 "step_share": d["ms"] / (ms_dev / args.steps), "kernels": kern,
                 "per_kernel_ms": per_kernel, "l2_probe": l2, "sampler": sampler}
     # CPU baseline on a bounded sample (the oracle, all host cores)
