@@ -85,6 +85,14 @@ NS2B_API int ns2b_interp_full(const float *xn, int64_t npts, const float *tables
                      float *cdw, void *stream);
 
 /* _kernels.scatter_first (_kernels.py:122-133): grad (L,T,2) += w * dL/dfeat. */
+/* _kernels.hessian_contract (_kernels.py:159-206; hash_encoding.py:240-254): out (P,3,3)
+ * fp32 = sum over active feature rows a of coeff[p,a] d2 e_a / dx dx, zero diagonal.
+ * coeff (P, nlev*nfeat) fp32; xn normalised positions as for interp_full. */
+NS2B_API int ns2b_hessian_contract(const float *xn, int64_t npts, const float *tables, int64_t nlev,
+                                   int64_t tsize, int64_t nfeat, const int64_t *resolutions,
+                                   int64_t n_active, const float *inv_extent, const float *coeff,
+                                   float *out, void *stream);
+
 NS2B_API int ns2b_scatter_first(float *grad, int64_t nlev, int64_t tsize, int64_t nfeat,
                        const int64_t *cidx, const float *cw, const float *dl_dfeat, int64_t npts,
                        int64_t n_active, void *stream);
@@ -180,6 +188,19 @@ NS2B_API int ns2b_field_scatter(const ns2b_field_t *field, const float *pos32, c
                                 int64_t capacity, float *grad_tables, void *workspace,
                                 void *stream);
 
+/* field_backward(need_input_grads=True) (field.py:332-349): per-sample position and
+ * view-direction cotangents for the dynamic-scene transform optimiser.  pos32/ray_ids/
+ * dirs are what the forward got; sdf (P), geo (P,15), normals (P,3), colors (P,3) are
+ * its outputs; dl_dc (P,3; NULL = no colour cotangent, then colors/ray_ids/dirs may be
+ * NULL), dl_dd (P), dl_dn (P,3) may be NULL.  dl_dx = colour-input x cotangent +
+ * de_aug[:E] J + q Hess (hessian_contract with the d-row Jacobian's feature columns);
+ * dl_dv = colour-input v cotangent.  Writes dl_dx, dl_dv (P,3) fp32. */
+NS2B_API int ns2b_field_input_grads(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                                    const double *dirs, int64_t npts, const float *sdf, const float *geo,
+                                    const float *normals, const float *colors, const float *dl_dc,
+                                    const float *dl_dd, const float *dl_dn, float *dl_dx, float *dl_dv,
+                                    void *stream);
+
 /* Lean SDF-only query (renderer.py:131-142) on fp32 positions; d (P). */
 NS2B_API int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,
                    void *stream);
@@ -188,6 +209,12 @@ NS2B_API int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64
  * ema = max(density, 0.95 ema), bits = ema*step > threshold.  ema fp64 (G^3). */
 NS2B_API int ns2b_occupancy_update(const ns2b_field_t *field, const ns2b_occ_t *occ, double sharpness,
                           double threshold, double *ema, uint8_t *bits, void *stream);
+
+/* The density / EMA / threshold half of update_occupancy from given per-cell SDF values
+ * (ncells = G^3, C order), for update_occupancy(point_transform=...) where the caller
+ * moves the cell centres and queries ns2b_field_sdf itself. */
+NS2B_API int ns2b_occupancy_from_sdf(const float *sdf, int64_t ncells, double sharpness, double step_size,
+                                     double threshold, double *ema, uint8_t *bits, void *stream);
 
 /* Per-ray compositing (renderer.py:234-291) fused with the Huber colour loss and
  * its cotangent (trainer.py:96-112,215-221) and the compositing backward

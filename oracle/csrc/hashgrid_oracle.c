@@ -12,6 +12,8 @@
  *   interp_full         _kernels.py:67-119
  *   scatter_first       _kernels.py:122-133
  *   scatter_second      _kernels.py:136-156
+ *   hessian_contract    _kernels.py:159-206 (cv = sum_f f32(coeff*table) in fp64,
+ *                                             per-level fp64 h, out re-rounded to fp32)
  *   adam_step           _kernels.py:209-218
  *
  * Numeric contract kept from numba's typing: positions are float32, t = x*n and the
@@ -161,6 +163,51 @@ void orc_scatter_second(float *grad, int64_t nlev, int64_t tsize, int64_t nfeat,
 }
 
 /* float ** int as numba lowers it: binary exponentiation in float64. */
+void orc_hessian_contract(const float *xn, int64_t npts, const float *tables, int64_t nlev,
+                          int64_t tsize, int64_t nfeat, const int64_t *res, int64_t n_active,
+                          const float *inv_extent, const float *coeff, float *out, int nthreads)
+{
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+    for (int64_t p = 0; p < npts; ++p) {
+        float *o = out + 9 * p;
+        for (int k = 0; k < 9; ++k)
+            o[k] = 0.0f;
+        for (int64_t l = 0; l < n_active; ++l) {
+            int64_t n = res[l];
+            double sx = (double)n * (double)inv_extent[0];
+            double sy = (double)n * (double)inv_extent[1];
+            double sz = (double)n * (double)inv_extent[2];
+            int64_t cx, cy, cz;
+            double fx, fy, fz;
+            cell_frac((double)xn[3 * p + 0] * (double)n, n, &cx, &fx);
+            cell_frac((double)xn[3 * p + 1] * (double)n, n, &cy, &fy);
+            cell_frac((double)xn[3 * p + 2] * (double)n, n, &cz, &fz);
+            const float *tab = tables + l * tsize * nfeat;
+            double hxy = 0.0, hxz = 0.0, hyz = 0.0;
+            for (int c = 0; c < 8; ++c) {
+                int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                double wx = ox ? fx : 1.0 - fx, wy = oy ? fy : 1.0 - fy, wz = oz ? fz : 1.0 - fz;
+                double gx = ox ? 1.0 : -1.0, gy = oy ? 1.0 : -1.0, gz = oz ? 1.0 : -1.0;
+                int64_t r = corner_row(cx + ox, cy + oy, cz + oz, n, tsize);
+                double cv = 0.0;
+                for (int64_t f = 0; f < nfeat; ++f) {
+                    float prod = coeff[(p * nlev + l) * nfeat + f] * tab[r * nfeat + f];
+                    cv += (double)prod;
+                }
+                hxy += cv * gx * gy * wz;
+                hxz += cv * gx * gz * wy;
+                hyz += cv * gy * gz * wx;
+            }
+            o[1] = (float)((double)o[1] + hxy * sx * sy);
+            o[3] = (float)((double)o[3] + hxy * sx * sy);
+            o[2] = (float)((double)o[2] + hxz * sx * sz);
+            o[6] = (float)((double)o[6] + hxz * sx * sz);
+            o[5] = (float)((double)o[5] + hyz * sy * sz);
+            o[7] = (float)((double)o[7] + hyz * sy * sz);
+        }
+    }
+}
+
 static double int_pow(double a, int64_t e)
 {
     int invert = e < 0;

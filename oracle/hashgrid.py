@@ -165,3 +165,12 @@ def backward_second(grid, point, u, out=None):
     kernels.scatter_second(out, rec.indices, rec.weight_gradients,
                            np.ascontiguousarray(u[:, 3:, :], grid.dtype), rec.active_levels)
     return out
+
+
+def hessian_contract(grid, x, max_level, coeff):
+    """`hash_encoding.py:240-254`: sum_a coeff[p,a] d2 e_a / dx dx, (P, 3, 3)."""
+    xb = np.ascontiguousarray(_batch(x), grid.dtype)
+    xn = grid.normalize(xb)
+    inv_extent = np.ascontiguousarray(1.0 / grid.aabb_extent, grid.dtype)
+    return kernels.hessian_contract(xn, grid.tables, grid.resolutions,
+                                    active_level_count(grid, max_level), inv_extent, coeff)

@@ -45,6 +45,8 @@ def lib():
                                          ctypes.c_int]
         _lib.orc_scatter_first.argtypes = [_P, _I, _I, _I, _P, _P, _P, _I, _I]
         _lib.orc_scatter_second.argtypes = [_P, _I, _I, _I, _P, _P, _P, _I, _I]
+        _lib.orc_hessian_contract.argtypes = [_P, _I, _P, _I, _I, _I, _P, _I, _P, _P, _P,
+                                              ctypes.c_int]
         _lib.orc_adam_step_f32.argtypes = [_P, _P, _P, _P, _I, _I, _D, _D, _D, _D]
         _lib.orc_adam_step_f64.argtypes = [_P, _P, _P, _P, _I, _I, _D, _D, _D, _D]
     return _lib
@@ -90,6 +92,22 @@ def interp_full(xn, tables, resolutions, n_active, inv_extent):
                           int(n_active), _ptr(inv), _ptr(feats), _ptr(jac), _ptr(cidx),
                           _ptr(cw), _ptr(cdw), NUM_THREADS)
     return feats, jac, cidx, cw, cdw
+
+
+def hessian_contract(xn, tables, resolutions, n_active, inv_extent, coeff):
+    """`_kernels.hessian_contract` (`hashsdf/_kernels.py:159-206`): (P, 3, 3)."""
+    xn = _c(xn, np.float32)
+    tables = _c(tables, np.float32)
+    res = _c(resolutions, np.int64)
+    inv = _c(inv_extent, np.float32)
+    coeff = _c(coeff, np.float32)
+    nlev, tsize, nfeat = tables.shape
+    if coeff.shape != (xn.shape[0], nlev * nfeat):
+        raise ValueError("coeff must be (P, L*F)")
+    out = np.zeros((xn.shape[0], 3, 3), np.float32)
+    lib().orc_hessian_contract(_ptr(xn), xn.shape[0], _ptr(tables), nlev, tsize, nfeat, _ptr(res),
+                               int(n_active), _ptr(inv), _ptr(coeff), _ptr(out), NUM_THREADS)
+    return out
 
 
 def _check_inplace(a, dtype):

@@ -1,4 +1,4 @@
-"""Drop-in for `hashsdf._kernels` (`_kernels.py:40-218`) backed by libns2b on the GPU.
+"""Drop-in for `hashsdf._kernels` (`_kernels.py:40-218`, incl. hessian_contract :159-206) backed by libns2b on the GPU.
 
 Same signatures and semantics: numpy arrays in; `interp_*` return new numpy arrays,
 `scatter_*` and `adam_step` mutate their first argument in place.  Each call copies
@@ -51,6 +51,20 @@ def interp_full(xn, tables, resolutions, n_active, inv_extent):
               int(n_active), _lib.ptr(inv), _lib.ptr(feats), _lib.ptr(jac), _lib.ptr(cidx),
               _lib.ptr(cw), _lib.ptr(cdw), _lib.stream_ptr())
     return tuple(t.cpu().numpy() for t in (feats, jac, cidx, cw, cdw))
+
+
+def hessian_contract(xn, tables, resolutions, n_active, inv_extent, coeff):
+    xd = _dev(xn, np.float32)
+    td = _dev(tables, np.float32)
+    rd = _dev(resolutions, np.int64)
+    inv = _dev(inv_extent, np.float32)
+    cf = _dev(coeff, np.float32)
+    nlev, tsize, nfeat = tables.shape
+    out = torch.empty((xd.shape[0], 3, 3), dtype=torch.float32, device=xd.device)
+    _lib.call("ns2b_hessian_contract", _lib.ptr(xd), xd.shape[0], _lib.ptr(td), nlev, tsize, nfeat,
+              _lib.ptr(rd), int(n_active), _lib.ptr(inv), _lib.ptr(cf), _lib.ptr(out),
+              _lib.stream_ptr())
+    return out.cpu().numpy()
 
 
 def _scatter(name, grad, cidx, w, d, n_active):

@@ -54,6 +54,7 @@ _SIGS = {
     "ns2b_launch_count": (ctypes.c_uint64, []),
     "ns2b_interp_features": (ctypes.c_int, [P, I64, P, I64, I64, I64, P, I64, P, P]),
     "ns2b_interp_full": (ctypes.c_int, [P, I64, P, I64, I64, I64, P, I64, P, P, P, P, P, P, P]),
+    "ns2b_hessian_contract": (ctypes.c_int, [P, I64, P, I64, I64, I64, P, I64, P, P, P, P]),
     "ns2b_scatter_first": (ctypes.c_int, [P, I64, I64, I64, P, P, P, I64, I64, P]),
     "ns2b_scatter_second": (ctypes.c_int, [P, I64, I64, I64, P, P, P, I64, I64, P]),
     "ns2b_adam_step_f32": (ctypes.c_int, [P, P, P, P, I64, I64, F64, F64, F64, F64, P]),
@@ -70,6 +71,9 @@ _SIGS = {
     "ns2b_field_mlp_backward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, F64,
                                                P, P, P, P, P]),
     "ns2b_field_scatter": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, I64, P, P, P]),
+    "ns2b_field_input_grads": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, I64, P, P, P, P, P, P,
+                                              P, P, P, P]),
+    "ns2b_occupancy_from_sdf": (ctypes.c_int, [P, I64, F64, F64, F64, P, P, P]),
     "ns2b_field_sdf": (ctypes.c_int, [ctypes.POINTER(FieldT), P, I64, P, P]),
     "ns2b_occupancy_update": (ctypes.c_int, [ctypes.POINTER(FieldT), ctypes.POINTER(OccT), F64,
                                              F64, P, P, P]),

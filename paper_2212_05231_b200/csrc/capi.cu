@@ -132,6 +132,39 @@ __global__ void interp_kernel(const float *__restrict__ xn, int64_t npts,
     }
 }
 
+// hessian_contract (_kernels.py:159-206): (P,3,3) fp32, zero diagonal.
+__global__ void hessian_kernel(const float *__restrict__ xn, int64_t npts, const float *__restrict__ tables,
+                               GridArgs g, double ix, double iy, double iz, const float *__restrict__ coeff,
+                               float *__restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npts;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const float u0 = xn[3 * p], u1 = xn[3 * p + 1], u2 = xn[3 * p + 2];
+        float oxy = 0.f, oxz = 0.f, oyz = 0.f;
+        for (int l = 0; l < g.n_active; ++l) {
+            const LevelInfo lv = g.lv[l];
+            const float2 *tab = reinterpret_cast<const float2 *>(tables + l * g.tsize * 2);
+            const float *cf = coeff + (p * g.nlev + l) * 2;
+            double hxy, hxz, hyz;
+            hess_level(tab, lv, u0, u1, u2, cf[0], cf[1], hxy, hxz, hyz);
+            const double n = static_cast<double>(lv.n);
+            const double sx = n * ix, sy = n * iy, sz = n * iz;
+            oxy = hess_acc(oxy, hxy, sx, sy);
+            oxz = hess_acc(oxz, hxz, sx, sz);
+            oyz = hess_acc(oyz, hyz, sy, sz);
+        }
+        float *o = out + 9 * p;
+        o[0] = 0.f;
+        o[1] = oxy;
+        o[2] = oxz;
+        o[3] = oxy;
+        o[4] = 0.f;
+        o[5] = oyz;
+        o[6] = oxz;
+        o[7] = oyz;
+        o[8] = 0.f;
+    }
+}
+
 __global__ void scatter_kernel(float *__restrict__ grad, int nlev, int64_t tsize,
                                const int64_t *__restrict__ cidx, const float *__restrict__ cw,
                                const float *__restrict__ cdw, const float *__restrict__ dl,
@@ -249,6 +282,26 @@ int ns2b_interp_full(const float *xn, int64_t npts, const float *tables, int64_t
     interp_kernel<true><<<grid_for(npts, 128), 128, 0, st>>>(xn, npts, tables, g, feats, jac, cidx,
                                                              cw, cdw);
     return check_launch("interp_full");
+}
+
+int ns2b_hessian_contract(const float *xn, int64_t npts, const float *tables, int64_t nlev, int64_t tsize,
+                          int64_t nfeat, const int64_t *resolutions, int64_t n_active, const float *inv_extent,
+                          const float *coeff, float *out, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    NS2B_REQUIRE(nlev >= 1 && nlev <= NS2B_MAX_LEVELS, "shape error: 1..16 levels supported");
+    int64_t res[NS2B_MAX_LEVELS];
+    float inv[3];
+    int rc = copy_res(resolutions, nlev, res, st);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(inv, inv_extent, sizeof(inv), cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(NS2B_ECUDA, "inv_extent copy: %s", cudaGetErrorString(e));
+    GridArgs g;
+    if ((rc = make_grid_args(g, nlev, tsize, nfeat, res, n_active, inv))) return rc;
+    if (npts == 0) return NS2B_OK;
+    hessian_kernel<<<grid_for(npts, 128), 128, 0, st>>>(xn, npts, tables, g, inv[0], inv[1], inv[2], coeff,
+                                                         out);
+    return check_launch("hessian_contract");
 }
 
 static int scatter_common(float *grad, int64_t nlev, int64_t tsize, int64_t nfeat,

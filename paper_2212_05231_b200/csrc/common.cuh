@@ -86,6 +86,51 @@ __device__ __forceinline__ float normalize_coord(float x, float lo, float ext) {
     return fminf(fmaxf(v, 0.0f), 1.0f);
 }
 
+// Interpolation curvature of one level (_kernels.py:159-206): trilinear interpolation
+// is linear per axis, so d2 feat/dx dx has a zero diagonal and mixed entries that are
+// constant per cell.  With cv = sum_f coeff_f * corner_f (fp32 products summed in
+// fp64, as numba types them), h_xy = sum_c cv * gx * gy * wz etc. in fp64 with fp64
+// fractions; the caller scales by n*inv_extent and rounds into its fp32 output.
+__device__ __forceinline__ void cell_frac_d(float xn, int n, int &c, double &frac) {
+    double t = static_cast<double>(xn) * static_cast<double>(n);
+    int ci = static_cast<int>(ceil(t)) - 1;
+    ci = ci < 0 ? 0 : (ci > n - 1 ? n - 1 : ci);
+    c = ci;
+    frac = t - static_cast<double>(ci);
+}
+
+__device__ __forceinline__ void hess_level(const float2 *__restrict__ tab, const LevelInfo &lv, float u0,
+                                           float u1, float u2, float c0, float c1, double &hxy,
+                                           double &hxz, double &hyz) {
+    int cx, cy, cz;
+    double fx, fy, fz;
+    cell_frac_d(u0, lv.n, cx, fx);
+    cell_frac_d(u1, lv.n, cy, fy);
+    cell_frac_d(u2, lv.n, cz, fz);
+    float2 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+    hxy = hxz = hyz = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+        const double wx = ox ? fx : 1.0 - fx, wy = oy ? fy : 1.0 - fy, wz = oz ? fz : 1.0 - fz;
+        const double cv = __dadd_rn(static_cast<double>(__fmul_rn(c0, v[c].x)),
+                                    static_cast<double>(__fmul_rn(c1, v[c].y)));
+        // gx*gy etc. are +-1: exact sign flips
+        const double sxy = (ox ^ oy) ? -cv : cv, sxz = (ox ^ oz) ? -cv : cv, syz = (oy ^ oz) ? -cv : cv;
+        hxy = __dadd_rn(hxy, __dmul_rn(sxy, wz));
+        hxz = __dadd_rn(hxz, __dmul_rn(sxz, wy));
+        hyz = __dadd_rn(hyz, __dmul_rn(syz, wx));
+    }
+}
+
+// out += h * s_a * s_b, the fp64 term rounded into the fp32 accumulator.
+__device__ __forceinline__ float hess_acc(float out, double h, double sa, double sb) {
+    return static_cast<float>(__dadd_rn(static_cast<double>(out), __dmul_rn(__dmul_rn(h, sa), sb)));
+}
+
 // ---------------------------------------------------------- misc device ----
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -7,11 +7,11 @@ range (MLPs first, then the active table levels).  `grid.tables`, `sdf_net.layer
 and `color_net.layers` are views into it; `sharpness_log` is a separate fp64 device
 scalar (`field.py:78`).
 
-`eval_field` / `field_backward` call the fused libns2b kernels (csrc/field.cu):
-the forward writes d, g, n, c per sample; the backward recomputes the forward per
-sample (nothing but positions and view directions is cached between the passes) and
-accumulates all parameter gradients, including the Eq. 9 table path and the
-Theorem-1 SDF path.
+`eval_field` / `field_backward` call the libns2b field kernels (csrc/field_tc.cu):
+the forward (gather + tcgen05 MLP forward) writes d, g, n, c per sample and leaves
+its staged operand tiles in the cache's workspace; the backward (tcgen05 MLP
+backward + table scatter) reads them back and accumulates all parameter gradients,
+including the Eq. 9 table path and the Theorem-1 SDF path.
 """
 
 from __future__ import annotations
@@ -316,12 +316,12 @@ def field_sdf_only(params, positions, max_level):
 
 def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input_grads=False,
                    grads=None):
-    """Parameter gradients from per-sample cotangents (`field.py:272-331`).
+    """Parameter gradients from per-sample cotangents (`field.py:272-350`).
 
-    Accumulates into `grads` (a FieldGrads from new_grads) when given."""
-    if need_input_grads:
-        raise NotImplementedError("input gradients belong to the dynamic-scene path "
-                                  "(field.py:332-349), not the static training step")
+    Accumulates into `grads` (a FieldGrads from new_grads) when given.  With
+    `need_input_grads` also sets grads.dl_dx / grads.dl_dv (P,3) fp32, the position
+    and view-direction cotangents of the transform optimiser (`field.py:332-349`,
+    csrc/field.cu field_input_grads_kernel)."""
     if cache is None or cache.x is None:
         raise ValueError("stale sample")
     if dl_dc is not None and not cache.has_color:
@@ -344,4 +344,14 @@ def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input
               _lib.ptr(gn), 0.0, None, _lib.ptr(grads.sdf_layers[0]),
               _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.tables), _lib.ptr(cache.workspace),
               _lib.stream_ptr())
+    if need_input_grads:
+        grads.dl_dx = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+        grads.dl_dv = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+        use_c = dl_dc is not None
+        _lib.call("ns2b_field_input_grads", ctypes.byref(f), _lib.ptr(cache.x),
+                  _lib.ptr(cache.ray_ids), _lib.ptr(cache.dirs), npts, _lib.ptr(cache.sdf),
+                  _lib.ptr(cache.geo), _lib.ptr(cache.normals),
+                  _lib.ptr(cache.colors) if use_c else None, _lib.ptr(gc) if use_c else None,
+                  _lib.ptr(gd), None if gn is None else _lib.ptr(gn), _lib.ptr(grads.dl_dx),
+                  _lib.ptr(grads.dl_dv), _lib.stream_ptr())
     return grads

@@ -223,3 +223,19 @@ def backward_second(grid, point, u, out=None):
               _lib.ptr(rec.indices), _lib.ptr(rec.weight_gradients), _lib.ptr(uu),
               rec.indices.shape[0], rec.active_levels, _lib.stream_ptr())
     return out
+
+
+def hessian_contract(grid, x, max_level, coeff):
+    """`hash_encoding.py:240-254` on the GPU: (P, 3, 3) fp32, the interpolation
+    curvature sum_a coeff[p, a] d2 e_a / dx dx (coeff (P, L*F), feature rows only)."""
+    xb = as_device(_batch(x), torch.float32)
+    xn = grid.normalize(xb)
+    npts = xb.shape[0]
+    L = grid.num_levels
+    cf = as_device(coeff, torch.float32).reshape(npts, 2 * L).contiguous()
+    inv = torch.from_numpy(grid.inv_extent_f32()).to(xb.device)
+    out = torch.empty((npts, 3, 3), dtype=torch.float32, device=xb.device)
+    _lib.call("ns2b_hessian_contract", _lib.ptr(xn), npts, _lib.ptr(grid.tables), L, grid.table_size,
+              2, _lib.ptr(grid.resolutions_device()), active_level_count(grid, max_level),
+              _lib.ptr(inv), _lib.ptr(cf), _lib.ptr(out), _lib.stream_ptr())
+    return out

@@ -102,12 +102,32 @@ class OccupancyGrid:
         return o
 
 
+def cell_centers_device(occ):
+    """`renderer.py:92-96` on the device: lo + (i + 0.5) * extent / G per axis (fp64,
+    same operation order as the reference, so the same bits), C-order (G^3, 3)."""
+    g = occ.resolution
+    dev = occ.ema.device
+    ax = [float(occ.lo[a]) + (torch.arange(g, dtype=torch.float64, device=dev) + 0.5)
+          * float(occ.hi[a] - occ.lo[a]) / g for a in range(3)]
+    xx, yy, zz = torch.meshgrid(*ax, indexing="ij")
+    return torch.stack([xx.reshape(-1), yy.reshape(-1), zz.reshape(-1)], dim=1)
+
+
 def update_occupancy(occ, params, max_level, rng=None, point_transform=None, chunk=1 << 18):
     """Refresh EMA / bits from the field (`renderer.py:108-128`), one kernel over all
-    G^3 cell centres.  `rng` and `chunk` are accepted for interface parity."""
+    G^3 cell centres.  `rng` and `chunk` are accepted for interface parity.
+
+    `point_transform` (dynamic scenes) maps the marching-space centres, an fp64 (N, 3)
+    device tensor, into the field's canonical space; the moved centres are queried
+    with ns2b_field_sdf and folded into the EMA by ns2b_occupancy_from_sdf."""
+    na = enc.active_level_count(params.grid, max_level)
     if point_transform is not None:
-        raise NotImplementedError("point_transform belongs to the dynamic-scene path")
-    f = params.field_struct(enc.active_level_count(params.grid, max_level))
+        pts = as_device(point_transform(cell_centers_device(occ)), torch.float64).reshape(-1, 3)
+        sdf = fieldmod.field_sdf_only(params, pts, max_level)
+        _lib.call("ns2b_occupancy_from_sdf", _lib.ptr(sdf), sdf.numel(), params.sharpness, occ.step_size,
+                  occ.threshold, _lib.ptr(occ.ema), _lib.ptr(occ.bits), _lib.stream_ptr())
+        return occ
+    f = params.field_struct(na)
     o = occ.struct()
     _lib.call("ns2b_occupancy_update", ctypes.byref(f), ctypes.byref(o), params.sharpness,
               occ.threshold, _lib.ptr(occ.ema), _lib.ptr(occ.bits), _lib.stream_ptr())
@@ -234,9 +254,12 @@ def composite_forward(offsets, m, sdf, colors, s, rendered, resid, alphas, weigh
 def render_rays(batch, params, occ, max_level, point_transform=None, dir_transform=None):
     """March, evaluate the field, composite (`renderer.py:234-291`).  Returns
     (colors (m,3) fp64 CUDA tensor, RenderRecords).  Like the reference, `params`
-    may be an analytic object with `.sharpness` and `.evaluate(pos, dirs)`."""
-    if point_transform is not None or dir_transform is not None:
-        raise NotImplementedError("point/dir transforms belong to the dynamic-scene path")
+    may be an analytic object with `.sharpness` and `.evaluate(pos, dirs)`.
+
+    `point_transform` / `dir_transform` (dynamic scenes, `renderer.py:257-264`) map
+    the marched samples' fp64 positions (P,3) / per-sample view directions (P,3),
+    device tensors, into the field's canonical space; marching and compositing stay
+    in the marching space."""
     o = as_device(batch.origins, torch.float64).reshape(-1, 3).contiguous()
     d = as_device(batch.directions, torch.float64).reshape(-1, 3).contiguous()
     m = o.shape[0]
@@ -245,8 +268,15 @@ def render_rays(batch, params, occ, max_level, point_transform=None, dir_transfo
     P = mr.sample_count
     if P == 0:
         return torch.zeros((m, 3), dtype=torch.float64, device=o.device), _empty_records(m, s, o.device)
+    pos32, fids, fdirs = mr.positions32, mr.ray_ids, d
+    if point_transform is not None:
+        pos32 = as_device(point_transform(mr.positions), torch.float64).reshape(-1, 3).float().contiguous()
+    if dir_transform is not None:
+        fdirs = as_device(dir_transform(d[mr.ray_ids.long()]), torch.float64).reshape(-1, 3).contiguous()
+        fids = torch.arange(P, dtype=torch.int32, device=o.device)
     if hasattr(params, "evaluate"):
-        sdf, cols = params.evaluate(mr.positions, d[mr.ray_ids.long()])
+        pos_f = mr.positions if point_transform is None else point_transform(mr.positions)
+        sdf, cols = params.evaluate(pos_f, fdirs[fids.long()])
         sdf = as_device(sdf, torch.float32).reshape(-1).contiguous()
         cols = as_device(cols, torch.float32).reshape(-1, 3).contiguous()
         cache = None
@@ -258,12 +288,11 @@ def render_rays(batch, params, occ, max_level, point_transform=None, dir_transfo
         geo = torch.empty((P, fieldmod.GEO_FEATURE_DIM), dtype=torch.float32, device=o.device)
         f = params.field_struct(na)
         ws = _lib.field_workspace(P, o.device)
-        _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(mr.positions32),
-                  _lib.ptr(mr.ray_ids), _lib.ptr(d), _lib.ptr(mr.count), P, _lib.ptr(sdf),
-                  _lib.ptr(cols), _lib.ptr(normals), _lib.ptr(geo), None, _lib.ptr(ws),
-                  _lib.stream_ptr())
-        cache = fieldmod.FieldCache(mr.positions32, max_level, na, mr.ray_ids, d, mr.count, sdf,
-                                    normals, cols, geo, True, ws)
+        _lib.call("ns2b_field_forward", ctypes.byref(f), _lib.ptr(pos32), _lib.ptr(fids),
+                  _lib.ptr(fdirs), _lib.ptr(mr.count), P, _lib.ptr(sdf), _lib.ptr(cols),
+                  _lib.ptr(normals), _lib.ptr(geo), None, _lib.ptr(ws), _lib.stream_ptr())
+        cache = fieldmod.FieldCache(pos32, max_level, na, fids, fdirs, mr.count, sdf, normals, cols,
+                                    geo, True, ws)
     rendered = torch.empty((m, 3), dtype=torch.float64, device=o.device)
     resid = torch.empty(m, dtype=torch.float64, device=o.device)
     a = torch.zeros(P, dtype=torch.float64, device=o.device)

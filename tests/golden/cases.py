@@ -70,3 +70,30 @@ def level_norms(g):
     """Per-level (L2 norm, sum, nnz) of a (L, T, F) table-shaped array (float64)."""
     g = g.astype(np.float64).reshape(g.shape[0], -1)
     return np.stack([np.sqrt((g * g).sum(1)), g.sum(1), (g != 0).sum(1)], axis=1)
+
+
+# Dynamic-scene hooks (SURVEY §8 f3): a fixed rigid transform x -> R (x + T) (Eq. 11),
+# evaluated elementwise in one fixed order so numpy (reference / oracle side) and
+# torch (device side) produce identical bits.
+RIGID_AXIS_ANGLE = (0.05, -0.12, 0.2)
+RIGID_T = (0.03, -0.02, 0.04)
+
+
+def rodrigues(w):
+    w = np.asarray(w, np.float64)
+    th = float(np.linalg.norm(w))
+    k = w / th
+    kx = np.array([[0, -k[2], k[1]], [k[2], 0, -k[0]], [-k[1], k[0], 0]])
+    return np.eye(3) + np.sin(th) * kx + (1 - np.cos(th)) * (kx @ kx)
+
+
+def rigid_apply(x, R, T=None):
+    """R (x + T) per row; x numpy (N,3) or torch (N,3)."""
+    cols = [x[:, k] + float(T[k]) if T is not None else x[:, k] for k in range(3)]
+    out = [(cols[0] * float(R[k][0]) + cols[1] * float(R[k][1])) + cols[2] * float(R[k][2])
+           for k in range(3)]
+    if type(x).__module__.startswith("torch"):
+        import torch
+
+        return torch.stack(out, dim=1)
+    return np.stack(out, axis=1)

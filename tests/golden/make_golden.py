@@ -252,7 +252,63 @@ def checkpoint_case():
     checkpoint.save_checkpoint(OUT / "ckpt_small.ns2c", st, extra_sections=[(b"XTRA", b"kept")])
 
 
+def dynamic_case():
+    """Dynamic-scene hooks: hessian_contract (_kernels.py:159-206),
+    field_backward(need_input_grads=True) (field.py:332-349), and update_occupancy /
+    render_rays with point/dir transforms (renderer.py:108-128, 234-264)."""
+    res = {}
+    for name in ("c1", "np2"):
+        spec = cases.GRIDS[name]
+        L, T = spec["num_levels"], spec["table_size"]
+        grid = hash_encoding.MultiResHashGrid(**spec)
+        tables = cases.trained_tables(L, T)
+        xn = cases.grid_points(seed=3)
+        inv = np.ascontiguousarray(1.0 / grid.aabb_extent, np.float32)
+        coeff = np.random.default_rng(17).standard_normal((xn.shape[0], 2 * L)).astype(np.float32)
+        for na in (L, 3):
+            res[f"hess_{name}_na{na}"] = _kernels.hessian_contract(xn, tables, grid.resolutions, na,
+                                                                   inv, coeff)
+    for name in ("c1", "c2"):
+        p = _field_params(name)
+        x = cases.world_points(seed=5)
+        rng = np.random.default_rng(9)
+        v = rng.standard_normal((x.shape[0], 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        for lam in (p.grid.num_levels, 3):
+            cache = field.eval_field(p, x, v, lam)
+            dl_dc = rng.standard_normal((x.shape[0], 3))
+            dl_dd = rng.standard_normal(x.shape[0])
+            dl_dn = rng.standard_normal((x.shape[0], 3)).astype(np.float32)
+            k = f"ig_{name}_lam{lam}_"
+            gr = field.field_backward(p, cache, dl_dc=dl_dc, dl_dd=dl_dd, dl_dn=dl_dn,
+                                      need_input_grads=True)
+            res.update({k + "dl_dc": dl_dc, k + "dl_dd": dl_dd, k + "dl_dn": dl_dn,
+                        k + "dl_dx": gr.dl_dx, k + "dl_dv": gr.dl_dv})
+            gr = field.field_backward(p, cache, dl_dd=dl_dd, dl_dn=dl_dn, need_input_grads=True)
+            res[k + "nocolor_dl_dx"] = gr.dl_dx
+    # transforms: c1 scene, SAL init, occupancy refreshed in the moved frame
+    R = cases.rodrigues(cases.RIGID_AXIS_ANGLE)
+    pt = lambda x: cases.rigid_apply(x, R, cases.RIGID_T)  # noqa: E731
+    dt = lambda v: cases.rigid_apply(v, R)  # noqa: E731
+    with tempfile.TemporaryDirectory() as td:
+        ds = scene_io.make_synthetic("sphere", td, views=8, image_size=64, seed=0)
+    cfg = trainer.TrainConfig(batch_size=512, num_levels=8, table_size=2**14, seed=0, level_init=8)
+    st = trainer.TrainState.create(cfg, aabb=ds.scene_aabb)
+    renderer.update_occupancy(st.occ, st.params, 8, point_transform=pt)
+    res["occ_bits"] = np.packbits(st.occ.bits.reshape(-1))
+    res["occ_ema_sum"] = st.occ.ema.sum()
+    batch = scene_io.sample_ray_batch(ds, 0, cfg.batch_size, cfg.fg_fraction, st.rng)
+    rendered, rec = renderer.render_rays(batch, st.params, st.occ, 8, point_transform=pt,
+                                         dir_transform=dt)
+    res.update({"rt_origins": batch.origins, "rt_dirs": batch.directions, "rt_rendered": rendered,
+                "rt_count": rec.sample_count, "rt_R": R})
+    np.savez_compressed(OUT / "dynamic_c1.npz", **res)
+
+
 def main():
+    if sys.argv[1:] == ["dynamic"]:
+        dynamic_case()
+        return
     checkpoint_case()
     kat()
     mlp_case()
