@@ -1,0 +1,331 @@
+"""Dynamic sequences: global rigid transforms, their accumulation into the canonical
+space, and incremental per-frame training (paper §5.1-5.2, Eqs. 11-12; the
+reference's SPEC `dynamic` module — the reference package ships only the hooks it
+calls: `render_rays(point_transform, dir_transform)` `renderer.py:234-264`,
+`update_occupancy(point_transform)` `renderer.py:108-128`,
+`field_backward(need_input_grads)` `field.py:332-349` and `hessian_contract`
+`_kernels.py:159-206`, so there is no reference driver to be bit-compatible with).
+
+Device path per step (frames > 0): march in the frame's own space, evaluate the
+field at x_c = M (x + o) (M = R^c_{i-1} R_i, o = T_i + R_i^T T^c_{i-1}: Eq. 11 then
+Eq. 12 in one affine map), composite, backward through the compositing, then ONE
+input-gradient kernel (`ns2b_field_input_grads`, dl/dx_c incl. the encoding
+curvature term, dl/dv_c) whose per-sample outputs are reduced to the 6 transform
+parameters' gradient; in the joint phase the usual field backward + fused Adam run
+as well.  The transform's own 6-parameter Adam is host arithmetic on 21 reduced
+numbers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import field as fieldmod
+from . import hash_encoding as enc
+from . import renderer, scene_io, trainer
+from .hash_encoding import as_device
+
+
+def _skew(w):
+    return np.array([[0.0, -w[2], w[1]], [w[2], 0.0, -w[0]], [-w[1], w[0], 0.0]])
+
+
+def rodrigues(w):
+    """exp([w]x) for an axis-angle 3-vector (closed form)."""
+    w = np.asarray(w, np.float64)
+    th = float(np.linalg.norm(w))
+    if th < 1e-12:
+        return np.eye(3) + _skew(w)
+    k = _skew(w / th)
+    return np.eye(3) + np.sin(th) * k + (1.0 - np.cos(th)) * (k @ k)
+
+
+def rodrigues_jacobian(w):
+    """[dR/dw_k] for k = 0..2: ((w_k [w]x + [w x ((I - R) e_k)]x) / |w|^2) R
+    (the standard differential of the exponential map); [e_k]x at w = 0."""
+    w = np.asarray(w, np.float64)
+    th2 = float(w @ w)
+    eye = np.eye(3)
+    if th2 < 1e-16:
+        return [_skew(eye[k]) for k in range(3)]
+    R = rodrigues(w)
+    W = _skew(w)
+    return [((w[k] * W + _skew(np.cross(w, (eye - R)[:, k]))) / th2) @ R for k in range(3)]
+
+
+def polar_orthonormalize(R):
+    """Nearest rotation (polar decomposition via SVD, det +1)."""
+    u, _, vt = np.linalg.svd(R)
+    d = np.sign(np.linalg.det(u @ vt))
+    return u @ np.diag([1.0, 1.0, d]) @ vt
+
+
+def _affine(x, M, o):
+    """M (x + o) row-wise for numpy or torch (N, 3)."""
+    if isinstance(x, torch.Tensor):
+        Mt = torch.as_tensor(M, dtype=x.dtype, device=x.device)
+        ot = torch.as_tensor(o, dtype=x.dtype, device=x.device)
+        return (x + ot) @ Mt.T
+    return (np.asarray(x, np.float64) + o) @ M.T
+
+
+@dataclass
+class GlobalTransform:
+    """Per-frame rigid transform (Eq. 11): x_{i-1} = R_i (x_i + T_i), R_i = exp([w]x)."""
+
+    w: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    t: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    @classmethod
+    def identity(cls):
+        return cls()
+
+    @property
+    def rotation(self):
+        return rodrigues(self.w)
+
+    @property
+    def params(self):
+        return np.concatenate([self.w, self.t])
+
+    def to_previous_frame(self, x):
+        return _affine(x, self.rotation, np.asarray(self.t, np.float64))
+
+
+@dataclass
+class TransformChain:
+    """Accumulated transform to the canonical (first-frame) space (Eq. 12):
+    x_c = R^c_i (x_i + T^c_i)."""
+
+    R: np.ndarray = field(default_factory=lambda: np.eye(3))
+    T: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    frame: int = 0
+
+    def accumulate(self, gt):
+        """R^c_i = R^c_{i-1} R_i, T^c_i = T_i + R_i^{-1} T^c_{i-1}; re-orthonormalised."""
+        Ri = gt.rotation
+        return TransformChain(polar_orthonormalize(self.R @ Ri), np.asarray(gt.t, np.float64) + Ri.T @ self.T,
+                              self.frame + 1)
+
+    def canonicalize(self, x):
+        return _affine(x, self.R, self.T)
+
+    def frame_transform(self, gt):
+        return FrameTransform(self, gt)
+
+
+class FrameTransform:
+    """The point / direction maps render_rays and update_occupancy take for frame i
+    while gt_i is being optimised: x_c = R^c_{i-1} (R_i (x + T_i) + T^c_{i-1})
+    = M (x + o), v_c = M v."""
+
+    def __init__(self, chain, gt):
+        self.chain, self.gt = chain, gt
+        Ri = gt.rotation
+        self.Ri = Ri
+        self.M = chain.R @ Ri
+        self.o = np.asarray(gt.t, np.float64) + Ri.T @ chain.T
+
+    def point(self, x):
+        return _affine(x, self.M, self.o)
+
+    def direction(self, v):
+        return _affine(v, self.M, np.zeros(3))
+
+    def param_gradient(self, x, v, dl_dxc, dl_dvc):
+        """d loss / d (w, T_i) from per-sample canonical-space cotangents.
+
+        x (P,3) frame-space positions, v (P,3) frame-space directions, dl_dxc / dl_dvc
+        (P,3) cotangents of x_c / v_c.  dL/dT = M^T sum g; dL/dR_i = R^c^T (sum g (x+T)^T
+        + sum h v^T); dL/dw_k = <dL/dR_i, dR_i/dw_k>."""
+        t = torch.as_tensor(np.asarray(self.gt.t, np.float64), device=x.device)
+        g = dl_dxc.double()
+        h = dl_dvc.double()
+        a = x.double() + t
+        red = torch.cat([g.sum(0), (g.T @ a).reshape(-1), (h.T @ v.double()).reshape(-1)]).cpu().numpy()
+        gsum, Sx, Sv = red[:3], red[3:12].reshape(3, 3), red[12:21].reshape(3, 3)
+        dT = self.M.T @ gsum
+        dR = self.chain.R.T @ (Sx + Sv)
+        dw = np.array([np.sum(dR * J) for J in rodrigues_jacobian(self.gt.w)])
+        return np.concatenate([dw, dT])
+
+
+class TransformAdam:
+    """Adam over the 6 transform parameters (host fp64; β and ε as the field's)."""
+
+    def __init__(self, beta1=0.9, beta2=0.99, eps=1e-15):
+        self.b1, self.b2, self.eps = beta1, beta2, eps
+        self.m = np.zeros(6)
+        self.v = np.zeros(6)
+        self.t = 0
+
+    def step(self, gt, grad, lr):
+        if not np.all(np.isfinite(grad)):
+            raise FloatingPointError("divergence: non-finite gradient for global_transform")
+        self.t += 1
+        self.m = self.b1 * self.m + (1 - self.b1) * grad
+        self.v = self.b2 * self.v + (1 - self.b2) * grad * grad
+        mh = self.m / (1 - self.b1**self.t)
+        vh = self.v / (1 - self.b2**self.t)
+        p = gt.params - lr * mh / (np.sqrt(vh) + self.eps)
+        gt.w, gt.t = p[:3].copy(), p[3:].copy()
+
+
+@dataclass
+class DynamicConfig:
+    """SPEC `dynamic` design decisions (Supp. §F.3)."""
+
+    first_frame_steps: int = 2000
+    transform_steps: int = 100
+    frame_steps: int = 1100
+    lr_transform: float = 1e-3
+    lr_transform_joint: float = 1e-4
+
+
+@dataclass
+class SequenceState:
+    train: trainer.TrainState
+    chain: TransformChain = field(default_factory=TransformChain)
+    transforms: list = field(default_factory=list)   # per-frame GlobalTransform (frame 0: identity)
+    frame: int = -1
+
+
+def field_input_grads(params, cache, dl_dc=None, dl_dd=None, dl_dn=None):
+    """Only the position / view cotangents of field_backward(need_input_grads=True)
+    (`field.py:332-349`), without the parameter gradients: (dl_dx, dl_dv) (P,3) fp32."""
+    npts = cache.x.shape[0]
+    dev = cache.x.device
+
+    def _cot(a, shape):
+        return None if a is None else as_device(a, torch.float32).reshape(shape).contiguous()
+
+    gc, gd, gn = _cot(dl_dc, (npts, 3)), _cot(dl_dd, (npts,)), _cot(dl_dn, (npts, 3))
+    dl_dx = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+    dl_dv = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+    f = params.field_struct(cache.n_active)
+    _lib.call("ns2b_field_input_grads", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.ray_ids),
+              _lib.ptr(cache.dirs), npts, _lib.ptr(cache.sdf), _lib.ptr(cache.geo), _lib.ptr(cache.normals),
+              _lib.ptr(cache.colors) if gc is not None else None, _lib.ptr(gc), _lib.ptr(gd), _lib.ptr(gn),
+              _lib.ptr(dl_dx), _lib.ptr(dl_dv), _lib.stream_ptr())
+    return dl_dx, dl_dv
+
+
+def _cotangents(state, batch, rendered, rec):
+    """Huber colour loss + Eikonal (`trainer.py:96-120, 215-240`) on the device."""
+    cfg = state.config
+    m = batch.count
+    P = rec.sample_count
+    tgt = as_device(batch.target_colors, torch.float64).reshape(-1, 3)
+    r = rendered - tgt
+    a = r.abs()
+    d = cfg.huber_delta
+    hub = torch.where(a <= d, 0.5 * r * r, d * (a - 0.5 * d))
+    color = float(hub.sum()) / m
+    dl_dray = torch.where(a <= d, r, d * torch.sign(r)) / m
+    dl_dc, dl_dsdf, dslog = renderer.backward_cotangents(rec, dl_dray)
+    n = rec.cache.normals
+    nn = n.norm(dim=1)
+    eik = float(((nn - 1.0) ** 2).sum()) / max(P, 1)
+    dl_dn = (cfg.eikonal_weight * 2.0 * (nn - 1.0) / nn.clamp_min(1e-12))[:, None] * n / max(P, 1)
+    mse = float((r * r).sum()) / (3.0 * m)
+    return color, eik, mse, dl_dc, dl_dsdf, dslog, dl_dn.float()
+
+
+def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform):
+    """One step of frame `frame` > 0: transform-only (joint=False: field frozen, only
+    the input-gradient kernel runs) or joint (field backward + Adam as well)."""
+    st = seq.train
+    cfg, params = st.config, st.params
+    level = trainer.level_schedule(st.step, cfg)
+    ft = seq.chain.frame_transform(gt)
+    if st.step % cfg.occupancy_update_every == 0:
+        renderer.update_occupancy(st.occ, params, level, point_transform=ft.point)
+    batch = scene_io.sample_ray_batch(dataset, frame, cfg.batch_size, cfg.fg_fraction, st.rng)
+    rendered, rec = renderer.render_rays(batch, params, st.occ, level, point_transform=ft.point,
+                                         dir_transform=ft.direction)
+    P = rec.sample_count
+    rep = trainer.LossReport(step=st.step, color=0.0, eikonal=0.0, total=0.0, level=level, psnr=0.0,
+                             sample_count=P)
+    if P > 0:
+        color, eik, mse, dl_dc, dl_dsdf, dslog, dl_dn = _cotangents(st, batch, rendered, rec)
+        rep.color, rep.eikonal, rep.total = color, eik, color + cfg.eikonal_weight * eik
+        rep.psnr = trainer.psnr_from_mse(mse)
+        v = as_device(batch.directions, torch.float64).reshape(-1, 3)[rec.ray_ids.long()]
+        if joint:
+            ws = st.ws
+            lay = params.layout
+            na = enc.active_level_count(params.grid, level)
+            ws.grads[:lay.active_end(na)].zero_()
+            sdf_g, col_g, tab_g = lay.views(ws.grads)
+            grads = fieldmod.FieldGrads(tab_g, sdf_g, col_g, ws.grads)
+            fieldmod.field_backward(params, rec.cache, dl_dc, dl_dsdf, dl_dn, need_input_grads=True,
+                                    grads=grads)
+            dl_dx, dl_dv = grads.dl_dx, grads.dl_dv
+        else:
+            dl_dx, dl_dv = field_input_grads(params, rec.cache, dl_dc, dl_dsdf, dl_dn)
+        opt.step(gt, ft.param_gradient(rec.frame_positions, v, dl_dx, dl_dv), lr_transform)
+        if joint:
+            ws.flag.zero_()
+            ws.sums[1].fill_(dslog / params.sharpness)
+            trainer._apply_gradients(st, na, params.sharpness)
+            if int(ws.flag.item()) != 0:
+                raise FloatingPointError("divergence: non-finite gradient")
+            params.refresh_host_mirror()
+    st.step += 1
+    return rep
+
+
+def train_frame(seq, dataset, frame, config=None, on_step=None):
+    """SPEC `train_frame`: frame 0 trains from scratch (the static step); frame i > 0
+    starts gt_i at identity, optimises it alone for `transform_steps` (field frozen),
+    then jointly with the field up to `frame_steps`, and accumulates it into the chain."""
+    dc = config or DynamicConfig()
+    if frame != seq.frame + 1:
+        raise ValueError("sequence order violation")
+    reports = []
+    if frame == 0:
+        for _ in range(dc.first_frame_steps):
+            r = trainer.train_step(seq.train, dataset, time_index=0)
+            reports.append(r)
+            if on_step:
+                on_step(r)
+        seq.transforms.append(GlobalTransform.identity())
+    else:
+        gt = GlobalTransform.identity()
+        opt = TransformAdam(seq.train.config.adam_beta1, seq.train.config.adam_beta2, seq.train.config.adam_eps)
+        for k in range(dc.frame_steps):
+            joint = k >= dc.transform_steps
+            r = dynamic_step(seq, dataset, frame, gt, opt, joint,
+                             dc.lr_transform_joint if joint else dc.lr_transform)
+            reports.append(r)
+            if on_step:
+                on_step(r)
+        seq.chain = seq.chain.accumulate(gt)
+        seq.transforms.append(gt)
+    seq.frame = frame
+    return reports
+
+
+def train_sequence(dataset, train_config, config=None, checkpoint_dir=None, on_step=None):
+    """SPEC `train_sequence`: frames in order; optional per-frame NS2C checkpoints
+    (`frame_%05d.ns2c`) and the chain as JSON-ready rows."""
+    from . import checkpoint as ck
+
+    seq = SequenceState(trainer.TrainState.create(train_config, aabb=dataset.scene_aabb))
+    rows = []
+    for i in range(dataset.num_time_steps):
+        train_frame(seq, dataset, i, config, on_step)
+        gt = seq.transforms[-1]
+        rows.append({"frame": i, "rotation": gt.rotation.tolist(), "translation": list(map(float, gt.t)),
+                     "chain_rotation": seq.chain.R.tolist(), "chain_translation": seq.chain.T.tolist()})
+        if checkpoint_dir is not None:
+            from pathlib import Path
+
+            Path(checkpoint_dir).mkdir(parents=True, exist_ok=True)
+            ck.save_checkpoint(Path(checkpoint_dir) / f"frame_{i:05d}.ns2c", seq.train)
+    return seq, rows

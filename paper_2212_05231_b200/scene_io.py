@@ -129,16 +129,28 @@ def sample_ray_batch(dataset, time_index, count, fg_fraction, rng):
     return RayBatch(o, d, tgt, flags)
 
 
+def _rot_z(angle):
+    c, s = np.cos(angle), np.sin(angle)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
 def preset_scene(name, num_frames=1):
-    """Static presets of `scene_io.py:229-263`."""
+    """Presets of `scene_io.py:230-257`: (spheres, per-frame motion), motion (R, T)
+    mapping canonical -> frame coordinates, x_frame = R x_canonical + T."""
+    static = [(np.eye(3), np.zeros(3))] * num_frames
     if name == "sphere":
-        spheres = [(np.zeros(3), 0.5, np.array([0.85, 0.35, 0.25]))]
-    elif name == "two-spheres":
-        spheres = [(np.array([0.32, 0.0, 0.0]), 0.30, np.array([0.85, 0.35, 0.25])),
-                   (np.array([-0.30, 0.05, 0.10]), 0.25, np.array([0.25, 0.45, 0.85]))]
-    else:
-        raise ValueError("unknown preset")
-    return spheres, [(np.eye(3), np.zeros(3))] * num_frames
+        return [(np.zeros(3), 0.5, np.array([0.85, 0.35, 0.25]))], static
+    if name == "two-spheres":
+        return [(np.array([0.32, 0.0, 0.0]), 0.30, np.array([0.85, 0.35, 0.25])),
+                (np.array([-0.30, 0.05, 0.10]), 0.25, np.array([0.25, 0.45, 0.85]))], static
+    if name == "translating-sphere":
+        return ([(np.zeros(3), 0.25, np.array([0.85, 0.35, 0.25]))],
+                [(np.eye(3), np.array([0.05 * t, 0.0, 0.0])) for t in range(num_frames)])
+    if name == "rotating-blob":
+        return ([(np.array([0.25, 0.0, 0.0]), 0.28, np.array([0.85, 0.35, 0.25])),
+                 (np.array([-0.18, 0.12, 0.14]), 0.20, np.array([0.25, 0.45, 0.85]))],
+                [(_rot_z(np.deg2rad(6.0) * t), np.zeros(3)) for t in range(num_frames)])
+    raise ValueError("unknown preset")
 
 
 def trace_spheres(origins, dirs, spheres, rot, trans):
@@ -183,21 +195,33 @@ def orbit_pose(azimuth, elevation, distance):
 
 
 def make_synthetic(preset, views=16, seed=0, image_size=128, width=None, height=None,
-                   focal=None, distance=2.6, chunk=1 << 20):
+                   focal=None, distance=2.6, chunk=1 << 20, frames=1):
     """In-memory `make_synthetic` (`scene_io.py:319-378`); with width/height/focal it
-    builds a rectangular variant.  Images are uint8-quantised like the PNG round trip."""
-    spheres, motion = preset_scene(preset)
+    builds a rectangular variant, with `frames` > 1 a dynamic sequence (the same
+    cameras every frame, time_index t, the preset's per-frame rigid motion).  Images
+    are uint8-quantised like the PNG round trip; the ground-truth motion is kept on
+    the dataset as `.motion` (evaluation only, like ground_truth.json)."""
+    spheres, motion = preset_scene(preset, frames)
     w = int(width or image_size)
     h = int(height or image_size)
     f = float(focal) if focal is not None else image_size * 1.4
     rng = np.random.default_rng(seed)
     elev = np.deg2rad(np.where(np.arange(views) % 2 == 0, 18.0, -12.0))
     azim = 2 * np.pi * np.arange(views) / views + rng.uniform(0, 2 * np.pi / views)
-    rot, trans = motion[0]
+    out = []
+    for t in range(frames):
+        rot, trans = motion[t]
+        out += _render_views(views, azim, elev, distance, f, w, h, spheres, rot, trans, t, chunk)
+    ds = MultiViewDataset(out, num_time_steps=frames)
+    ds.motion = motion
+    return ds
+
+
+def _render_views(views, azim, elev, distance, f, w, h, spheres, rot, trans, t, chunk):
     frames = []
     for v in range(views):
         pose = orbit_pose(azim[v], elev[v], distance)
-        fr = CameraFrame(f, f, w / 2.0, h / 2.0, w, h, pose, None, None, 0)
+        fr = CameraFrame(f, f, w / 2.0, h / 2.0, w, h, pose, None, None, t)
         img = np.empty((h * w, 3), np.uint8)
         msk = np.empty(h * w, np.float64)
         ys, xs = np.mgrid[0:h, 0:w]
@@ -210,7 +234,7 @@ def make_synthetic(preset, views=16, seed=0, image_size=128, width=None, height=
         fr.image = img.reshape(h, w, 3).astype(np.float64) / 255.0
         fr.mask = msk.reshape(h, w)
         frames.append(fr)
-    return MultiViewDataset(frames)
+    return frames
 
 
 def make_dtu_shaped(views=49, width=1600, height=1200, seed=0, preset="two-spheres"):
