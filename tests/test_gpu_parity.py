@@ -370,3 +370,34 @@ def test_divergence_raises(sphere64):
     with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for"):
         ptrain.train_step(pst, sphere64, batch=b)
     assert np.array_equal(np_(pst.params.grid.tables), before)
+
+
+@pytest.mark.parametrize("case", ["empty_occupancy", "rays_miss_box", "single_ray"])
+def test_edge_batches_match_oracle(sphere64, case):
+    """Edge cases of `train_step` (`trainer.py:281-310`): no kept samples (empty grid, or
+    every ray misses the aabb) -> colour loss of a black render, Adam skipped, parameters
+    and Adam step counts untouched; a one-ray batch -> the normal path at m = 1."""
+    cfg = otrain.TrainConfig(batch_size=1 if case == "single_ray" else 512, num_levels=8,
+                             table_size=2**14, seed=0, level_init=8)
+    ost = otrain.TrainState.create(cfg)
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    if case == "empty_occupancy":
+        ost.occ.bits[...] = False
+    ost.step = 1  # no occupancy refresh on either side
+    pst = product_state_from_oracle(ost)
+    b = oscene.sample_ray_batch(sphere64, 0, cfg.batch_size, cfg.fg_fraction, np.random.default_rng(3))
+    if case == "rays_miss_box":
+        b = oscene.RayBatch(b.origins + 10.0, b.directions, b.target_colors, b.foreground_flags)
+    before = np_(pst.params.flat).copy()
+    t_before = pst.adam["tables"].t
+    ro = otrain.train_step(ost, sphere64, batch=b)
+    rp = ptrain.train_step(pst, sphere64, batch=b)
+    assert rp.sample_count == ro.sample_count
+    for k in ("color", "eikonal", "total"):
+        a, r = getattr(rp, k), getattr(ro, k)
+        assert abs(a - r) <= TOL * max(abs(r), 1e-9), f"{k}: {a} vs {r}"
+    if case != "single_ray":
+        assert ro.sample_count == 0
+        assert np.array_equal(np_(pst.params.flat), before), "Adam must be skipped when P = 0"
+        assert pst.adam["tables"].t == t_before == ost.adam["tables"].t
+    assert pst.step == ost.step == 2
