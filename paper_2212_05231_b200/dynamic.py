@@ -66,12 +66,13 @@ def polar_orthonormalize(R):
 
 
 def _affine(x, M, o):
-    """M (x + o) row-wise for numpy or torch (N, 3)."""
-    if isinstance(x, torch.Tensor):
-        Mt = torch.as_tensor(M, dtype=x.dtype, device=x.device)
-        ot = torch.as_tensor(o, dtype=x.dtype, device=x.device)
-        return (x + ot) @ Mt.T
-    return (np.asarray(x, np.float64) + o) @ M.T
+    """M (x + o) row-wise for numpy or torch (N, 3), as elementwise fp64 arithmetic
+    (a K = 3 matmul would go to a GEMM kernel for nothing)."""
+    if not isinstance(x, torch.Tensor):
+        x = np.asarray(x, np.float64)
+    c = [x[:, k] + float(o[k]) for k in range(3)]
+    rows = [(c[0] * float(M[k][0]) + c[1] * float(M[k][1])) + c[2] * float(M[k][2]) for k in range(3)]
+    return torch.stack(rows, dim=1) if isinstance(x, torch.Tensor) else np.stack(rows, axis=1)
 
 
 @dataclass
@@ -147,7 +148,11 @@ class FrameTransform:
         g = dl_dxc.double()
         h = dl_dvc.double()
         a = x.double() + t
-        red = torch.cat([g.sum(0), (g.T @ a).reshape(-1), (h.T @ v.double()).reshape(-1)]).cpu().numpy()
+        vd = v.double()
+        # the 21 sums as one reduction over a (P, 21) product (no K = P GEMMs)
+        prods = torch.cat([g, (g[:, :, None] * a[:, None, :]).reshape(-1, 9),
+                           (h[:, :, None] * vd[:, None, :]).reshape(-1, 9)], dim=1)
+        red = prods.sum(0).cpu().numpy()
         gsum, Sx, Sv = red[:3], red[3:12].reshape(3, 3), red[12:21].reshape(3, 3)
         dT = self.M.T @ gsum
         dR = self.chain.R.T @ (Sx + Sv)
