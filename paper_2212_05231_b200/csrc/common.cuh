@@ -99,18 +99,8 @@ __device__ __forceinline__ void cell_frac_d(float xn, int n, int &c, double &fra
     frac = t - static_cast<double>(ci);
 }
 
-__device__ __forceinline__ void hess_level(const float2 *__restrict__ tab, const LevelInfo &lv, float u0,
-                                           float u1, float u2, float c0, float c1, double &hxy,
-                                           double &hxz, double &hyz) {
-    int cx, cy, cz;
-    double fx, fy, fz;
-    cell_frac_d(u0, lv.n, cx, fx);
-    cell_frac_d(u1, lv.n, cy, fy);
-    cell_frac_d(u2, lv.n, cz, fz);
-    float2 v[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-        v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+__device__ __forceinline__ void hess_from_corners(const float2 (&v)[8], double fx, double fy, double fz, float c0,
+                                                  float c1, double &hxy, double &hxz, double &hyz) {
     hxy = hxz = hyz = 0.0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -124,6 +114,21 @@ __device__ __forceinline__ void hess_level(const float2 *__restrict__ tab, const
         hxz = __dadd_rn(hxz, __dmul_rn(sxz, wy));
         hyz = __dadd_rn(hyz, __dmul_rn(syz, wx));
     }
+}
+
+__device__ __forceinline__ void hess_level(const float2 *__restrict__ tab, const LevelInfo &lv, float u0,
+                                           float u1, float u2, float c0, float c1, double &hxy,
+                                           double &hxz, double &hyz) {
+    int cx, cy, cz;
+    double fx, fy, fz;
+    cell_frac_d(u0, lv.n, cx, fx);
+    cell_frac_d(u1, lv.n, cy, fy);
+    cell_frac_d(u2, lv.n, cz, fz);
+    float2 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+    hess_from_corners(v, fx, fy, fz, c0, c1, hxy, hxz, hyz);
 }
 
 // out += h * s_a * s_b, the fp64 term rounded into the fp32 accumulator.

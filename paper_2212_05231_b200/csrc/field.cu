@@ -216,12 +216,55 @@ field_input_grads_kernel(FieldDev f, const float *__restrict__ pos, const int32_
         }
         dy[0] = dd;
         // SDF forward (features, mask, j_d), then de = H1^T (m . H2^T dy)
+        const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+        const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+        const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+        // features, 4 levels (32 independent loads) in flight per thread, via shared memory
+        float *fs = sw + W_FLOATS + threadIdx.x;
+#pragma unroll 1
+        for (int g = 0; g < f.n_active; g += 4) {
+            float2 v[4][8];
+            float fr[4][3];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < f.n_active) {
+                    const LevelInfo lv = f.lv[l];
+                    int cx, cy, cz;
+                    cell_frac(u0, lv.n, cx, fr[i][0]);
+                    cell_frac(u1, lv.n, cy, fr[i][1]);
+                    cell_frac(u2, lv.n, cz, fr[i][2]);
+                    const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < f.n_active) {
+                    float f0 = 0.f, f1 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                        const float w = (ox ? fr[i][0] : 1.f - fr[i][0]) * (oy ? fr[i][1] : 1.f - fr[i][1]) *
+                                        (oz ? fr[i][2] : 1.f - fr[i][2]);
+                        f0 = fmaf(w, v[i][c].x, f0);
+                        f1 = fmaf(w, v[i][c].y, f1);
+                    }
+                    fs[(2 * l) * FWD_BLOCK] = f0;
+                    fs[(2 * l + 1) * FWD_BLOCK] = f1;
+                }
+            }
+        }
         float e[EP];
         e[0] = x0;
         e[1] = x1;
         e[2] = x2;
         e[EC] = 1.f;
-        gather_features(f, x0, x1, x2, e);
+#pragma unroll
+        for (int a = 0; a < 2 * NS2B_MAX_LEVELS; ++a) e[3 + a] = a < 2 * f.n_active ? fs[a * FWD_BLOCK] : 0.f;
         float y[NOUT], jd[EP];
         uint32_t mlo, mhi;
         sdf_forward<true>(sw, e, y, jd, mlo, mhi);
@@ -247,40 +290,54 @@ field_input_grads_kernel(FieldDev f, const float *__restrict__ pos, const int32_
         gx0 += e[0];
         gx1 += e[1];
         gx2 += e[2];
-        // per level: de . d feat/dx and the curvature term q Hess(j_d features)
-        const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
-        const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
-        const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+        // per level: de . d feat/dx and the curvature term q Hess(j_d features); two levels
+        // (16 independent loads) per iteration, one set of corner values for both terms
         float hxy = 0.f, hxz = 0.f, hyz = 0.f;
 #pragma unroll 1
-        for (int l = 0; l < f.n_active; ++l) {
-            {
-                const LevelInfo lv = f.lv[l];
-                const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
-                int cx, cy, cz;
-                float fx, fy, fz;
-                cell_frac(u0, lv.n, cx, fx);
-                cell_frac(u1, lv.n, cy, fy);
-                cell_frac(u2, lv.n, cz, fz);
-                const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
-                const float d0 = e[3 + 2 * l], d1 = e[4 + 2 * l];
+        for (int g = 0; g < f.n_active; g += 2) {
+            float2 v[2][8];
+            double fr[2][3];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-                    const float2 v = __ldg(tab + corner_row(lv, cx + ox, cy + oy, cz + oz));
-                    const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                    const float t = fmaf(d0, v.x, d1 * v.y);
-                    gx0 = fmaf((ox ? sx : -sx) * (wy * wz), t, gx0);
-                    gx1 = fmaf((oy ? sy : -sy) * (wx * wz), t, gx1);
-                    gx2 = fmaf((oz ? sz : -sz) * (wx * wy), t, gx2);
+            for (int i = 0; i < 2; ++i) {
+                const int l = g + i;
+                if (l < f.n_active) {
+                    const LevelInfo lv = f.lv[l];
+                    int cx, cy, cz;
+                    cell_frac_d(u0, lv.n, cx, fr[i][0]);
+                    cell_frac_d(u1, lv.n, cy, fr[i][1]);
+                    cell_frac_d(u2, lv.n, cz, fr[i][2]);
+                    const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
                 }
-                double h01, h02, h12;
-                hess_level(tab, lv, u0, u1, u2, jd[3 + 2 * l], jd[4 + 2 * l], h01, h02, h12);
-                const double n = static_cast<double>(lv.n);
-                const double dsx = n * ix, dsy = n * iy, dsz = n * iz;
-                hxy = hess_acc(hxy, h01, dsx, dsy);
-                hxz = hess_acc(hxz, h02, dsx, dsz);
-                hyz = hess_acc(hyz, h12, dsy, dsz);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int l = g + i;
+                if (l < f.n_active) {
+                    const float fx = static_cast<float>(fr[i][0]), fy = static_cast<float>(fr[i][1]),
+                                fz = static_cast<float>(fr[i][2]);
+                    const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
+                    const float d0 = e[3 + 2 * l], d1 = e[4 + 2 * l];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                        const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                        const float t = fmaf(d0, v[i][c].x, d1 * v[i][c].y);
+                        gx0 = fmaf((ox ? sx : -sx) * (wy * wz), t, gx0);
+                        gx1 = fmaf((oy ? sy : -sy) * (wx * wz), t, gx1);
+                        gx2 = fmaf((oz ? sz : -sz) * (wx * wy), t, gx2);
+                    }
+                    double h01, h02, h12;
+                    hess_from_corners(v[i], fr[i][0], fr[i][1], fr[i][2], jd[3 + 2 * l], jd[4 + 2 * l], h01, h02,
+                                      h12);
+                    const double n = static_cast<double>(f.lv[l].n);
+                    const double dsx = n * ix, dsy = n * iy, dsz = n * iz;
+                    hxy = hess_acc(hxy, h01, dsx, dsy);
+                    hxz = hess_acc(hxz, h02, dsx, dsz);
+                    hyz = hess_acc(hyz, h12, dsy, dsz);
+                }
             }
         }
         dl_dx[3 * p] = gx0 + (q1 * hxy + q2 * hxz);
@@ -293,6 +350,7 @@ field_input_grads_kernel(FieldDev f, const float *__restrict__ pos, const int32_
 }
 
 constexpr size_t SDF_SMEM = W_FLOATS * sizeof(float);
+constexpr size_t IG_SMEM = SDF_SMEM + 2 * NS2B_MAX_LEVELS * FWD_BLOCK * sizeof(float);  // + per-thread features
 
 static int g_attr_done = 0;
 static int ensure_attrs() {
@@ -301,7 +359,7 @@ static int ensure_attrs() {
                                          static_cast<int>(SDF_SMEM));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(field_input_grads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(SDF_SMEM));
+                                 static_cast<int>(IG_SMEM));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(occupancy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SDF_SMEM));
@@ -426,7 +484,7 @@ int ns2b_field_input_grads(const ns2b_field_t *field, const float *pos32, const 
     NS2B_REQUIRE(pos32 && sdf && geo && normals && dl_dx && dl_dv, "field_input_grads: null argument");
     NS2B_REQUIRE(!dl_dc || (colors && ray_ids && dirs), "stale sample");
     if (npts <= 0) return NS2B_OK;
-    field_input_grads_kernel<<<grid_for(npts, FWD_BLOCK, kNumSMs * 8), FWD_BLOCK, SDF_SMEM,
+    field_input_grads_kernel<<<grid_for(npts, FWD_BLOCK, kNumSMs * 8), FWD_BLOCK, IG_SMEM,
                                as_stream(stream)>>>(f, pos32, ray_ids, dirs, npts, sdf, geo, normals, colors, dl_dc,
                                                     dl_dd, dl_dn, field->inv_extent[0], field->inv_extent[1],
                                                     field->inv_extent[2], dl_dx, dl_dv);
