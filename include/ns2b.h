@@ -188,18 +188,18 @@ NS2B_API int ns2b_field_scatter(const ns2b_field_t *field, const float *pos32, c
                                 int64_t capacity, float *grad_tables, void *workspace,
                                 void *stream);
 
-/* field_backward(need_input_grads=True) (field.py:332-349): per-sample position and
- * view-direction cotangents for the dynamic-scene transform optimiser.  pos32/ray_ids/
- * dirs are what the forward got; sdf (P), geo (P,15), normals (P,3), colors (P,3) are
- * its outputs; dl_dc (P,3; NULL = no colour cotangent, then colors/ray_ids/dirs may be
- * NULL), dl_dd (P), dl_dn (P,3) may be NULL.  dl_dx = colour-input x cotangent +
- * de_aug[:E] J + q Hess (hessian_contract with the d-row Jacobian's feature columns);
- * dl_dv = colour-input v cotangent.  Writes dl_dx, dl_dv (P,3) fp32. */
-NS2B_API int ns2b_field_input_grads(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
-                                    const double *dirs, int64_t npts, const float *sdf, const float *geo,
-                                    const float *normals, const float *colors, const float *dl_dc,
-                                    const float *dl_dd, const float *dl_dn, float *dl_dx, float *dl_dv,
-                                    void *stream);
+/* field_backward(need_input_grads=True) (field.py:332-349) on the forward's workspace:
+ * the tcgen05 MLP backward (weight gradients accumulated into grad_sdf / grad_color, as
+ * ns2b_field_mlp_backward) additionally leaves each sample's colour-input x / v
+ * cotangents and de_aug's position rows in the workspace, then one pass over the levels
+ * gives dl_dx = dcin_x + de_x + sum_a de_a J_a + q Hess(j_d) (hessian_contract's
+ * curvature) and dl_dv = dcin_v, (P,3) fp32 each.  No table gradients: run
+ * ns2b_field_scatter on the same workspace for those. */
+NS2B_API int ns2b_field_backward_inputs(const ns2b_field_t *field, const int32_t *count, int64_t capacity,
+                                        const float *dl_dc, const float *dl_dsdf, const float *dl_dn_extra,
+                                        double eik_weight, const int64_t *eik_count, float *grad_sdf,
+                                        float *grad_color, float *dl_dx, float *dl_dv, void *workspace,
+                                        void *stream);
 
 /* Lean SDF-only query (renderer.py:131-142) on fp32 positions; d (P). */
 NS2B_API int ns2b_field_sdf(const ns2b_field_t *field, const float *pos32, int64_t npts, float *sdf,

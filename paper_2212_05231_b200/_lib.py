@@ -71,8 +71,8 @@ _SIGS = {
     "ns2b_field_mlp_backward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, F64,
                                                P, P, P, P, P]),
     "ns2b_field_scatter": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, I64, P, P, P]),
-    "ns2b_field_input_grads": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, I64, P, P, P, P, P, P,
-                                              P, P, P, P]),
+    "ns2b_field_backward_inputs": (ctypes.c_int, [ctypes.POINTER(FieldT), P, I64, P, P, P, F64, P, P, P, P,
+                                                  P, P, P]),
     "ns2b_occupancy_from_sdf": (ctypes.c_int, [P, I64, F64, F64, F64, P, P, P]),
     "ns2b_field_sdf": (ctypes.c_int, [ctypes.POINTER(FieldT), P, I64, P, P]),
     "ns2b_occupancy_update": (ctypes.c_int, [ctypes.POINTER(FieldT), ctypes.POINTER(OccT), F64,

@@ -269,7 +269,8 @@ struct LevelSm {
 //              normal | colour [tile][6][128] fp32, j_d feature rows (into the sb block);
 //   MLP bwd -> scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d rows (32) | q (3).
 // The backward therefore never recomputes the forward: it DMAs the forward's tiles.
-constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6, NCROWS = 6;
+//   MLP bwd (input cotangents requested) -> [tile][9][128] fp32 = dcin_x (3) | dcin_v (3) | de_x (3).
+constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6, NCROWS = 6, XINROWS = 9;
 constexpr uint32_t FW_A1 = 0, FW_CIN = 2 * T64B, FW_A1C = FW_CIN + 2 * TCB, FW_A2C = FW_A1C + 2 * T64B,
                    FWB = FW_A2C + 2 * T64B;
 struct Workspace {
@@ -282,10 +283,11 @@ struct Workspace {
     int4 *fw_exp;
     uint2 *fw_mask;
     float *fw_nc;
+    float *xin;
 };
 __host__ __device__ inline size_t ws_tile_bytes() {
     return 2 * static_cast<size_t>(TEB) + FWB + sizeof(int4) + sizeof(int) + 4 * TILE * sizeof(uint2) +
-           (JROWS + SBROWS + XVROWS + NCROWS) * TILE * sizeof(float);
+           (JROWS + SBROWS + XVROWS + NCROWS + XINROWS) * TILE * sizeof(float);
 }
 __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     uint8_t *b = static_cast<uint8_t *>(base);
@@ -306,6 +308,8 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     b += ntiles * SBROWS * TILE * sizeof(float);
     w.xv = reinterpret_cast<float *>(b);
     b += ntiles * XVROWS * TILE * sizeof(float);
+    w.xin = reinterpret_cast<float *>(b);
+    b += ntiles * XINROWS * TILE * sizeof(float);
     w.e_exp = reinterpret_cast<int *>(b);
     return w;
 }
@@ -897,7 +901,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
                  const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
                  const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
-                 Workspace ws) {
+                 Workspace ws, int want_xin) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // [0] chain MMAs, [1] weight-gradient MMAs, [2..5] DMA into TW, TZ, TC, TE
     __shared__ uint64_t bars[6];
@@ -1199,6 +1203,15 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             q0 = gn0 + c0[3] * sc3;  // field.py:308-312
             q1 = gn1 + c0[4] * sc3;
             q2 = gn2 + c0[5] * sc3;
+            if (want_xin && qt == 2 && valid) {  // dl_dx / dl_dv colour-input parts (field.py:307,309)
+                float *xi = ws.xin + tile * XINROWS * TILE + r;
+                xi[0] = c0[0] * sc3;
+                xi[TILE] = c0[1] * sc3;
+                xi[2 * TILE] = c0[2] * sc3;
+                xi[3 * TILE] = c0[6] * sc3;
+                xi[4 * TILE] = c0[7] * sc3;
+                xi[5 * TILE] = c1[0] * sc3;
+            }
             // dly = [dd + dcin[9], dcin[10..24]]: block 0 (quarter 0), block 1 (quarter 1)
             float blk[8];
             if (qt == 0) {
@@ -1354,6 +1367,16 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 SBt[64 * TILE + r] = q0;
                 SBt[65 * TILE + r] = q1;
                 SBt[66 * TILE + r] = q2;
+            }
+            if (want_xin && qt == 3) {  // de_aug's position rows (E columns 32..34)
+                float dx[8];
+                umma::tmem_ld8(my + TB_SA + 32, dx);
+                if (valid) {
+                    float *xi = ws.xin + tile * XINROWS * TILE + r;
+                    xi[6 * TILE] = dx[0] * sde;
+                    xi[7 * TILE] = dx[1] * sde;
+                    xi[8 * TILE] = dx[2] * sde;
+                }
             }
             wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
             PMARK(16);
@@ -1523,6 +1546,88 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
         umma::stage_row<0, 48>(et, et + TEB, t, row);
         if (t == 0) ws.e_exp[tile] = eE;
         __syncthreads();  // raw[] reuse
+    }
+}
+
+// ---------------------------------------------------------------------------
+// field_backward(need_input_grads=True) (field.py:332-349) from the backward's outputs:
+//   dl_dx = dcin_x + de_x + sum_a de_a J_a + q Hess(j_d features),  dl_dv = dcin_v,
+// with de = dL/de_aug (= dd j_d + dg jg, so de J = dd n + dg (jg J)), J from the gather,
+// and the encoding curvature (hessian_contract, _kernels.py:159-206) from a fresh corner
+// gather, 4 levels (32 loads) in flight per thread.
+__global__ void __launch_bounds__(TILE)
+field_input_levels_kernel(FieldDev f, const int32_t *__restrict__ count, const Workspace ws, double ix,
+                          double iy, double iz, float *__restrict__ dl_dx, float *__restrict__ dl_dv) {
+    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
+    const int t = threadIdx.x;
+    if (t < NS2B_MAX_LEVELS) {
+        lvs[t].lv = f.lv[t];
+        lvs[t].sx = f.sx[t];
+        lvs[t].sy = f.sy[t];
+        lvs[t].sz = f.sz[t];
+    }
+    __syncthreads();
+    const int NA = f.n_active;
+    const int P = *count;
+    const int64_t ntiles = (static_cast<int64_t>(P) + TILE - 1) / TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p = tile * TILE + t;
+        if (p >= P) continue;
+        const float *SBt = ws.sb + tile * SBROWS * TILE + t;
+        const float *Jt = ws.jac + tile * JROWS * TILE + t;
+        const float *xi = ws.xin + tile * XINROWS * TILE + t;
+        const float *xv = ws.xv + tile * XVROWS * TILE + t;
+        const float u0 = normalize_coord(xv[0], f.lo[0], f.ext[0]);
+        const float u1 = normalize_coord(xv[TILE], f.lo[1], f.ext[1]);
+        const float u2 = normalize_coord(xv[2 * TILE], f.lo[2], f.ext[2]);
+        const float q0 = SBt[64 * TILE], q1 = SBt[65 * TILE], q2 = SBt[66 * TILE];
+        float gx0 = xi[0] + xi[6 * TILE], gx1 = xi[TILE] + xi[7 * TILE], gx2 = xi[2 * TILE] + xi[8 * TILE];
+        float hxy = 0.f, hxz = 0.f, hyz = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < NA; g += 4) {
+            float2 v[4][8];
+            double fr[4][3];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < NA) {
+                    const LevelInfo lv = lvs[l].lv;
+                    int cx, cy, cz;
+                    cell_frac_d(u0, lv.n, cx, fr[i][0]);
+                    cell_frac_d(u1, lv.n, cy, fr[i][1]);
+                    cell_frac_d(u2, lv.n, cz, fr[i][2]);
+                    const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int l = g + i;
+                if (l < NA) {
+                    const float de0 = SBt[(2 * l) * TILE], de1 = SBt[(2 * l + 1) * TILE];
+                    const float jd0 = SBt[(32 + 2 * l) * TILE], jd1 = SBt[(33 + 2 * l) * TILE];
+                    const float *jr = Jt + 6 * l * TILE;
+                    gx0 = fmaf(de0, jr[0], fmaf(de1, jr[3 * TILE], gx0));
+                    gx1 = fmaf(de0, jr[TILE], fmaf(de1, jr[4 * TILE], gx1));
+                    gx2 = fmaf(de0, jr[2 * TILE], fmaf(de1, jr[5 * TILE], gx2));
+                    double h01, h02, h12;
+                    hess_from_corners(v[i], fr[i][0], fr[i][1], fr[i][2], jd0, jd1, h01, h02, h12);
+                    const double n = static_cast<double>(lvs[l].lv.n);
+                    const double dsx = n * ix, dsy = n * iy, dsz = n * iz;
+                    hxy = hess_acc(hxy, h01, dsx, dsy);
+                    hxz = hess_acc(hxz, h02, dsx, dsz);
+                    hyz = hess_acc(hyz, h12, dsy, dsz);
+                }
+            }
+        }
+        dl_dx[3 * p] = gx0 + (q1 * hxy + q2 * hxz);
+        dl_dx[3 * p + 1] = gx1 + (q0 * hxy + q2 * hyz);
+        dl_dx[3 * p + 2] = gx2 + (q0 * hxz + q1 * hyz);
+        dl_dv[3 * p] = xi[3 * TILE];
+        dl_dv[3 * p + 1] = xi[4 * TILE];
+        dl_dv[3 * p + 2] = xi[5 * TILE];
     }
 }
 
@@ -1713,7 +1818,8 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
         tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-            f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+            f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws,
+            0);
         return check_launch("field_mlp_backward");
     default:
         tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
@@ -1744,7 +1850,8 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
 int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids, const double *dirs,
                       const int32_t *count, int64_t capacity, const float *dl_dc, const float *dl_dsdf,
                       const float *dl_dn_extra, double eik_weight, const int64_t *eik_count, float *grad_sdf,
-                      float *grad_color, float *grad_tables, void *workspace, cudaStream_t st) {
+                      float *grad_color, float *grad_tables, void *workspace, cudaStream_t st, float *dl_dx,
+                      float *dl_dv) {
     FieldDev f;
     int rc = make_field_dev(field, f);
     if (rc) return rc;
@@ -1755,8 +1862,15 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
     tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-        f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws);
+        f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws,
+        dl_dx != nullptr);
     if ((rc = check_launch("field_backward_tc"))) return rc;
+    if (dl_dx != nullptr) {
+        tc::field_input_levels_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::TILE, 0, st>>>(
+            f, count, ws, field->inv_extent[0], field->inv_extent[1], field->inv_extent[2], dl_dx, dl_dv);
+        if ((rc = check_launch("field_input_levels"))) return rc;
+    }
+    if (grad_tables == nullptr) return NS2B_OK;
     tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 16), tc::TILE, 0, st>>>(f, pos32, count, ws,
                                                                                    grad_tables, tc::agg_levels_env());
     return check_launch("field_scatter");

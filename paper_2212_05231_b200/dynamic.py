@@ -8,10 +8,10 @@ calls: `render_rays(point_transform, dir_transform)` `renderer.py:234-264`,
 
 Device path per step (frames > 0): march in the frame's own space, evaluate the
 field at x_c = M (x + o) (M = R^c_{i-1} R_i, o = T_i + R_i^T T^c_{i-1}: Eq. 11 then
-Eq. 12 in one affine map), composite, backward through the compositing, then ONE
-input-gradient kernel (`ns2b_field_input_grads`, dl/dx_c incl. the encoding
-curvature term, dl/dv_c) whose per-sample outputs are reduced to the 6 transform
-parameters' gradient; in the joint phase the usual field backward + fused Adam run
+Eq. 12 in one affine map), composite, backward through the compositing, then the
+tcgen05 MLP backward + one per-level pass (`ns2b_field_backward_inputs`: dl/dx_c incl.
+the encoding curvature term, dl/dv_c) whose per-sample outputs are reduced to the 6
+transform parameters' gradient; in the joint phase the usual field backward + fused Adam run
 as well.  The transform's own 6-parameter Adam is host arithmetic on 21 reduced
 numbers.
 """
@@ -202,21 +202,27 @@ class SequenceState:
 
 def field_input_grads(params, cache, dl_dc=None, dl_dd=None, dl_dn=None):
     """Only the position / view cotangents of field_backward(need_input_grads=True)
-    (`field.py:332-349`), without the parameter gradients: (dl_dx, dl_dv) (P,3) fp32."""
+    (`field.py:332-349`): the tcgen05 backward (its weight gradients go to a scratch
+    buffer) + the per-level pass, no table scatter.  (dl_dx, dl_dv) (P,3) fp32."""
     npts = cache.x.shape[0]
     dev = cache.x.device
 
     def _cot(a, shape):
-        return None if a is None else as_device(a, torch.float32).reshape(shape).contiguous()
+        if a is None:
+            return torch.zeros(shape, dtype=torch.float32, device=dev)
+        return as_device(a, torch.float32).reshape(shape).contiguous()
 
-    gc, gd, gn = _cot(dl_dc, (npts, 3)), _cot(dl_dd, (npts,)), _cot(dl_dn, (npts, 3))
+    gc, gd = _cot(dl_dc, (npts, 3)), _cot(dl_dd, (npts,))
+    gn = None if dl_dn is None else _cot(dl_dn, (npts, 3))
+    lay = params.layout
+    scratch = torch.empty(lay.mlp_floats, dtype=torch.float32, device=dev)
     dl_dx = torch.empty((npts, 3), dtype=torch.float32, device=dev)
     dl_dv = torch.empty((npts, 3), dtype=torch.float32, device=dev)
     f = params.field_struct(cache.n_active)
-    _lib.call("ns2b_field_input_grads", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.ray_ids),
-              _lib.ptr(cache.dirs), npts, _lib.ptr(cache.sdf), _lib.ptr(cache.geo), _lib.ptr(cache.normals),
-              _lib.ptr(cache.colors) if gc is not None else None, _lib.ptr(gc), _lib.ptr(gd), _lib.ptr(gn),
-              _lib.ptr(dl_dx), _lib.ptr(dl_dv), _lib.stream_ptr())
+    _lib.call("ns2b_field_backward_inputs", ctypes.byref(f), _lib.ptr(cache.count), npts, _lib.ptr(gc),
+              _lib.ptr(gd), _lib.ptr(gn), 0.0, None, _lib.ptr(scratch),
+              _lib.ptr(scratch[lay.color_offs[0]:]), _lib.ptr(dl_dx), _lib.ptr(dl_dv),
+              _lib.ptr(cache.workspace), _lib.stream_ptr())
     return dl_dx, dl_dv
 
 

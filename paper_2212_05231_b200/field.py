@@ -320,8 +320,9 @@ def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input
 
     Accumulates into `grads` (a FieldGrads from new_grads) when given.  With
     `need_input_grads` also sets grads.dl_dx / grads.dl_dv (P,3) fp32, the position
-    and view-direction cotangents of the transform optimiser (`field.py:332-349`,
-    csrc/field.cu field_input_grads_kernel)."""
+    and view-direction cotangents of the transform optimiser (`field.py:332-349`:
+    the tcgen05 backward leaves the colour-input and de_aug position cotangents in the
+    workspace, `field_input_levels_kernel` adds de.J and the encoding curvature)."""
     if cache is None or cache.x is None:
         raise ValueError("stale sample")
     if dl_dc is not None and not cache.has_color:
@@ -339,19 +340,19 @@ def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input
     gn = None if dl_dn is None else _cot(dl_dn, (npts, 3))
     grads = new_grads(params) if grads is None else grads
     f = params.field_struct(cache.n_active)
-    _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.ray_ids),
-              _lib.ptr(cache.dirs), _lib.ptr(cache.count), npts, _lib.ptr(gc), _lib.ptr(gd),
-              _lib.ptr(gn), 0.0, None, _lib.ptr(grads.sdf_layers[0]),
-              _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.tables), _lib.ptr(cache.workspace),
-              _lib.stream_ptr())
-    if need_input_grads:
-        grads.dl_dx = torch.empty((npts, 3), dtype=torch.float32, device=dev)
-        grads.dl_dv = torch.empty((npts, 3), dtype=torch.float32, device=dev)
-        use_c = dl_dc is not None
-        _lib.call("ns2b_field_input_grads", ctypes.byref(f), _lib.ptr(cache.x),
-                  _lib.ptr(cache.ray_ids), _lib.ptr(cache.dirs), npts, _lib.ptr(cache.sdf),
-                  _lib.ptr(cache.geo), _lib.ptr(cache.normals),
-                  _lib.ptr(cache.colors) if use_c else None, _lib.ptr(gc) if use_c else None,
-                  _lib.ptr(gd), None if gn is None else _lib.ptr(gn), _lib.ptr(grads.dl_dx),
-                  _lib.ptr(grads.dl_dv), _lib.stream_ptr())
+    if not need_input_grads:
+        _lib.call("ns2b_field_backward", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.ray_ids),
+                  _lib.ptr(cache.dirs), _lib.ptr(cache.count), npts, _lib.ptr(gc), _lib.ptr(gd),
+                  _lib.ptr(gn), 0.0, None, _lib.ptr(grads.sdf_layers[0]),
+                  _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.tables), _lib.ptr(cache.workspace),
+                  _lib.stream_ptr())
+        return grads
+    grads.dl_dx = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+    grads.dl_dv = torch.empty((npts, 3), dtype=torch.float32, device=dev)
+    _lib.call("ns2b_field_backward_inputs", ctypes.byref(f), _lib.ptr(cache.count), npts, _lib.ptr(gc),
+              _lib.ptr(gd), _lib.ptr(gn), 0.0, None, _lib.ptr(grads.sdf_layers[0]),
+              _lib.ptr(grads.color_layers[0]), _lib.ptr(grads.dl_dx), _lib.ptr(grads.dl_dv),
+              _lib.ptr(cache.workspace), _lib.stream_ptr())
+    _lib.call("ns2b_field_scatter", ctypes.byref(f), _lib.ptr(cache.x), _lib.ptr(cache.count), npts,
+              _lib.ptr(grads.tables), _lib.ptr(cache.workspace), _lib.stream_ptr())
     return grads
