@@ -183,13 +183,23 @@ class TransformAdam:
 
 @dataclass
 class DynamicConfig:
-    """SPEC `dynamic` design decisions (Supp. §F.3)."""
+    """Per-frame schedule (Supp. §F.3; the reference's `TrainConfig` dynamic fields,
+    `trainer.py:62-68`, are the defaults — `from_train_config` copies them)."""
 
     first_frame_steps: int = 2000
     transform_steps: int = 100
     frame_steps: int = 1100
     lr_transform: float = 1e-3
     lr_transform_joint: float = 1e-4
+    frame_lr_scale: float = 0.3   # field learning-rate scale while fine-tuning frames > 0
+
+    @classmethod
+    def from_train_config(cls, cfg, **kw):
+        d = dict(first_frame_steps=cfg.first_frame_steps, transform_steps=cfg.transform_only_steps,
+                 frame_steps=cfg.frame_steps, lr_transform=cfg.transform_lr,
+                 lr_transform_joint=cfg.transform_joint_lr, frame_lr_scale=cfg.frame_lr_scale)
+        d.update(kw)
+        return cls(**d)
 
 
 @dataclass
@@ -247,9 +257,10 @@ def _cotangents(state, batch, rendered, rec):
     return color, eik, mse, dl_dc, dl_dsdf, dslog, dl_dn.float()
 
 
-def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform):
+def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform, field_lr_scale=1.0):
     """One step of frame `frame` > 0: transform-only (joint=False: field frozen, only
-    the input-gradient kernel runs) or joint (field backward + Adam as well)."""
+    the input-gradient kernel runs) or joint (field backward + Adam as well, the field's
+    learning rates scaled by `field_lr_scale`)."""
     st = seq.train
     cfg, params = st.config, st.params
     level = trainer.level_schedule(st.step, cfg)
@@ -283,7 +294,7 @@ def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform):
         if joint:
             ws.flag.zero_()
             ws.sums[1].fill_(dslog / params.sharpness)
-            trainer._apply_gradients(st, na, params.sharpness)
+            trainer._apply_gradients(st, na, params.sharpness, field_lr_scale)
             if int(ws.flag.item()) != 0:
                 raise FloatingPointError("divergence: non-finite gradient")
             params.refresh_host_mirror()
@@ -295,9 +306,9 @@ def train_frame(seq, dataset, frame, config=None, on_step=None):
     """SPEC `train_frame`: frame 0 trains from scratch (the static step); frame i > 0
     starts gt_i at identity, optimises it alone for `transform_steps` (field frozen),
     then jointly with the field up to `frame_steps`, and accumulates it into the chain."""
-    dc = config or DynamicConfig()
     if frame != seq.frame + 1:
         raise ValueError("sequence order violation")
+    dc = config or DynamicConfig.from_train_config(seq.train.config)
     reports = []
     if frame == 0:
         for _ in range(dc.first_frame_steps):
@@ -312,7 +323,7 @@ def train_frame(seq, dataset, frame, config=None, on_step=None):
         for k in range(dc.frame_steps):
             joint = k >= dc.transform_steps
             r = dynamic_step(seq, dataset, frame, gt, opt, joint,
-                             dc.lr_transform_joint if joint else dc.lr_transform)
+                             dc.lr_transform_joint if joint else dc.lr_transform, dc.frame_lr_scale)
             reports.append(r)
             if on_step:
                 on_step(r)

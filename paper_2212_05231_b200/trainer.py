@@ -345,14 +345,16 @@ def train_step(state, dataset, time_index=0, batch=None):
     return report
 
 
-def _apply_gradients(state, n_active, sharpness):
+def _apply_gradients(state, n_active, sharpness, lr_scale=1.0):
     """Divergence check, s_log Adam, then one multi-group Adam launch over
-    [sdf_0 | sdf_1 | color_0..2 | tables[:n_active]] (`trainer.py:243-278`)."""
+    [sdf_0 | sdf_1 | color_0..2 | tables[:n_active]] (`trainer.py:243-278`).
+    `lr_scale` multiplies every group's learning rate (dynamic frames > 0 fine-tune
+    with `frame_lr_scale`, `trainer.py:62-68`)."""
     cfg = state.config
     params, ws = state.params, state.ws
     lay = params.layout
     sp = _lib.stream_ptr()
-    scale = lr_factor(state.step, cfg.total_steps, cfg.lr_final_fraction)
+    scale = lr_factor(state.step, cfg.total_steps, cfg.lr_final_fraction) * lr_scale
     lr_t, lr_m = cfg.lr_tables * scale, cfg.lr_mlp * scale
     names = ["sdf_0", "sdf_1", "color_0", "color_1", "color_2", "tables"]
     offs = lay.sdf_offs + lay.color_offs + [lay.tables_off]

@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--transform-steps", type=int, default=100)
     ap.add_argument("--frame-steps", type=int, default=1100)
     ap.add_argument("--lr-joint", type=float, default=1e-4, help="transform lr in the joint phase")
+    ap.add_argument("--frame-lr-scale", type=float, default=0.3, help="field lr scale for frames > 0")
     a = ap.parse_args()
     ds = scene_io.make_synthetic("translating-sphere", views=a.views, image_size=a.image, seed=0, frames=a.frames)
     ds_eval = scene_io.make_synthetic("translating-sphere", views=2, image_size=a.image, seed=99, frames=a.frames)
@@ -58,7 +59,8 @@ def main():
     cfg = trainer.TrainConfig(batch_size=4096, num_levels=8, table_size=2**14, seed=0, level_init=8,
                               max_resolution=128, init_radius=0.25, total_steps=2 * a.frame0_steps)
     dc = dyn.DynamicConfig(first_frame_steps=a.frame0_steps, transform_steps=a.transform_steps,
-                           frame_steps=a.frame_steps, lr_transform_joint=a.lr_joint)
+                           frame_steps=a.frame_steps, lr_transform_joint=a.lr_joint,
+                           frame_lr_scale=a.frame_lr_scale)
     seq = dyn.SequenceState(trainer.TrainState.create(cfg, aabb=ds.scene_aabb))
     rows = []
     for i in range(a.frames):
@@ -84,7 +86,7 @@ def main():
         "frames": a.frames, "max_T_err": max(r["T_err"] for r in rows[1:]) if a.frames > 1 else 0.0,
         "psnr_frame0": rows[0]["psnr_heldout"], "min_psnr": min(r["psnr_heldout"] for r in rows),
         "chain_identity_max_err": chain_err, "steps_per_frame": a.frame_steps,
-        "transform_steps": a.transform_steps, "lr_joint": a.lr_joint,
+        "transform_steps": a.transform_steps, "lr_joint": a.lr_joint, "frame_lr_scale": a.frame_lr_scale,
         "mean_frame_seconds": float(np.mean([r["seconds"] for r in rows[1:]])) if a.frames > 1 else None}}))
 
 
