@@ -1,4 +1,4 @@
-// Shared device code of the field kernels (SIMT: field.cu, tcgen05: field_tc.cu).
+// Shared device code of the field kernels (SIMT SDF queries: field.cu, tcgen05: field_tc.cu).
 #pragma once
 
 #include "common.cuh"
@@ -9,25 +9,13 @@ constexpr int H = 64;        // hidden width
 constexpr int EP = 36;       // padded e_aug width (3 + 32 + 1)
 constexpr int EC = 35;       // const-channel column in the padded layout
 constexpr int CIN = 25;      // colour-net input
-constexpr int CINP = 28;     // padded
 constexpr int NOUT = 16;     // sdf-net outputs (d + 15 geometry features)
 
-// shared-memory weight block (floats)
+// shared-memory weight block of the SIMT SDF kernels (floats)
 constexpr int OFF_H1 = 0;                       // 64 x 36
 constexpr int OFF_H2 = OFF_H1 + H * EP;         // 16 x 64
 constexpr int OFF_H2T = OFF_H2 + NOUT * H;      // 64 x 16
-constexpr int OFF_C1 = OFF_H2T + H * NOUT;      // 64 x 28
-constexpr int OFF_C2 = OFF_C1 + H * CINP;       // 64 x 64
-constexpr int OFF_C3 = OFF_C2 + H * H;          // 4 x 64
-constexpr int W_FLOATS = OFF_C3 + 4 * H;        // 10496
-
-// weight-gradient accumulators (padded layouts, floats)
-constexpr int G_H1 = 0;                          // 64 x 36
-constexpr int G_H2 = G_H1 + H * EP;              // 16 x 64
-constexpr int G_C1 = G_H2 + NOUT * H;            // 64 x 28
-constexpr int G_C2 = G_C1 + H * CINP;            // 64 x 64
-constexpr int G_C3 = G_C2 + H * H;               // 4 x 64
-constexpr int G_FLOATS = G_C3 + 4 * H;           // 9472
+constexpr int W_FLOATS = OFF_H2T + H * NOUT;    // 4352
 
 struct FieldDev {
     int L, n_active;
@@ -80,17 +68,9 @@ static __device__ void load_weights(float *sw, const FieldDev &f) {
             if (src >= 0) v = f.sdf_w[j * (E + 1) + src];
         } else if (i < OFF_H2T) {
             v = f.sdf_w[H * (E + 1) + (i - OFF_H2)];
-        } else if (i < OFF_C1) {
+        } else {
             int r = i - OFF_H2T, j = r / NOUT, o = r % NOUT;  // H2T[j][o] = H2[o][j]
             v = f.sdf_w[H * (E + 1) + o * H + j];
-        } else if (i < OFF_C2) {
-            int r = i - OFF_C1, j = r / CINP, c = r % CINP;
-            if (c < CIN) v = f.color_w[j * CIN + c];
-        } else if (i < OFF_C3) {
-            v = f.color_w[H * CIN + (i - OFF_C2)];
-        } else {
-            int r = i - OFF_C3;
-            if (r < 3 * H) v = f.color_w[H * CIN + H * H + r];
         }
         sw[i] = v;
     }
@@ -106,62 +86,7 @@ __device__ __forceinline__ float sigmoid_f(float z) {
 }
 
 // ------------------------------------------------------------- gather -----
-// Trilinear features + d feature / d x for all active levels (_kernels.py:67-119,
-// without corner records).  e[3..34] receives the features; the Jacobian rows go to
-// shared memory at Js[(a*3+k)*stride].
-__device__ __forceinline__ void gather_full(const FieldDev &f, float x0, float x1, float x2,
-                                            float (&e)[EP], float *Js, int stride) {
-    const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
-    const float u1 = normalize_coord(x1, f.lo[1], f.ext[1]);
-    const float u2 = normalize_coord(x2, f.lo[2], f.ext[2]);
-#pragma unroll
-    for (int l = 0; l < NS2B_MAX_LEVELS; ++l) {
-        float f0 = 0.f, f1 = 0.f, j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
-        if (l < f.n_active) {
-            const LevelInfo lv = f.lv[l];
-            int cx, cy, cz;
-            float fx, fy, fz;
-            cell_frac(u0, lv.n, cx, fx);
-            cell_frac(u1, lv.n, cy, fy);
-            cell_frac(u2, lv.n, cz, fz);
-            const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
-            float2 v[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                v[c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
-            const float sx = f.sx[l], sy = f.sy[l], sz = f.sz[l];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
-                const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
-                const float w = wx * wy * wz;
-                const float dwx = (ox ? sx : -sx) * (wy * wz);
-                const float dwy = (oy ? sy : -sy) * (wx * wz);
-                const float dwz = (oz ? sz : -sz) * (wx * wy);
-                f0 = fmaf(w, v[c].x, f0);
-                f1 = fmaf(w, v[c].y, f1);
-                j00 = fmaf(dwx, v[c].x, j00);
-                j01 = fmaf(dwy, v[c].x, j01);
-                j02 = fmaf(dwz, v[c].x, j02);
-                j10 = fmaf(dwx, v[c].y, j10);
-                j11 = fmaf(dwy, v[c].y, j11);
-                j12 = fmaf(dwz, v[c].y, j12);
-            }
-        }
-        e[3 + 2 * l] = f0;
-        e[4 + 2 * l] = f1;
-        if (Js) {
-            float *jr = Js + (2 * l) * 3 * stride;
-            jr[0 * stride] = j00;
-            jr[1 * stride] = j01;
-            jr[2 * stride] = j02;
-            jr[3 * stride] = j10;
-            jr[4 * stride] = j11;
-            jr[5 * stride] = j12;
-        }
-    }
-}
-
+// Trilinear features of all active levels (_kernels.py:40-64); e[3..34] receives them.
 __device__ __forceinline__ void gather_features(const FieldDev &f, float x0, float x1, float x2,
                                                 float (&e)[EP]) {
     const float u0 = normalize_coord(x0, f.lo[0], f.ext[0]);
@@ -247,70 +172,6 @@ __device__ __forceinline__ void sdf_forward(const float *sw, const float (&e)[EP
             }
         }
     }
-}
-
-__device__ __forceinline__ bool mask_bit(uint32_t lo, uint32_t hi, int j) {
-    return j < 32 ? ((lo >> j) & 1u) : ((hi >> (j - 32)) & 1u);
-}
-
-// n = j_d[:E] @ J with J rows 0..2 = I (field.py:220-221).
-__device__ __forceinline__ void normal_from(const float (&jd)[EP], const float *Js, int stride,
-                                            int n_active, float &n0, float &n1, float &n2) {
-    n0 = jd[0];
-    n1 = jd[1];
-    n2 = jd[2];
-#pragma unroll
-    for (int a = 0; a < 2 * NS2B_MAX_LEVELS; ++a) {
-        if (a < 2 * n_active) {
-            const float s = jd[3 + a];
-            const float *jr = Js + a * 3 * stride;
-            n0 = fmaf(s, jr[0], n0);
-            n1 = fmaf(s, jr[stride], n1);
-            n2 = fmaf(s, jr[2 * stride], n2);
-        }
-    }
-}
-
-// colour net first layer: a1c = relu(C1 cin)
-__device__ __forceinline__ void color_layer1(const float *sw, const float (&cin)[CINP], float (&a1)[H],
-                                             uint32_t &mlo, uint32_t &mhi) {
-    mlo = mhi = 0u;
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-        const float *c1 = sw + OFF_C1 + j * CINP;
-        float z = 0.f;
-#pragma unroll
-        for (int i = 0; i < CINP; i += 4) {
-            float4 w = lds4(c1 + i);
-            z = fmaf(w.x, cin[i], z);
-            z = fmaf(w.y, cin[i + 1], z);
-            z = fmaf(w.z, cin[i + 2], z);
-            z = fmaf(w.w, cin[i + 3], z);
-        }
-        const bool on = z > 0.f;
-        a1[j] = on ? z : 0.f;
-        if (on) {
-            if (j < 32) mlo |= 1u << j;
-            else mhi |= 1u << (j - 32);
-        }
-    }
-}
-
-__device__ __forceinline__ float dot64(const float *w, const float (&a)[H]) {
-    float z0 = 0.f, z1 = 0.f;
-#pragma unroll
-    for (int i = 0; i < H; i += 8) {
-        float4 p = lds4(w + i), q = lds4(w + i + 4);
-        z0 = fmaf(p.x, a[i], z0);
-        z0 = fmaf(p.y, a[i + 1], z0);
-        z0 = fmaf(p.z, a[i + 2], z0);
-        z0 = fmaf(p.w, a[i + 3], z0);
-        z1 = fmaf(q.x, a[i + 4], z1);
-        z1 = fmaf(q.y, a[i + 5], z1);
-        z1 = fmaf(q.z, a[i + 6], z1);
-        z1 = fmaf(q.w, a[i + 7], z1);
-    }
-    return z0 + z1;
 }
 
 }  // namespace ns2b
