@@ -591,8 +591,8 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 d1 *= scd;
                 float jl[8];
                 umma::tmem_ld8(my + TM_J + 8 * l, jl);
-                SBt[(32 + 2 * l) * TILE + r] = d0;  // j_d feature rows for the scatter (Eq. 9)
-                SBt[(33 + 2 * l) * TILE + r] = d1;
+                __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
+                __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
                 p0 = fmaf(d0, jl[0], fmaf(d1, jl[3], p0));
                 p1 = fmaf(d0, jl[1], fmaf(d1, jl[4], p1));
                 p2 = fmaf(d0, jl[2], fmaf(d1, jl[5], p2));
@@ -1362,11 +1362,11 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             umma::tmem_ld8(my + TB_SA + 8 * qt, de);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (8 * qt + k < 2 * NA) SBt[(8 * qt + k) * TILE + r] = de[k] * sde;
+                if (8 * qt + k < 2 * NA) __stcs(SBt + (8 * qt + k) * TILE + r, de[k] * sde);
             if (qt == 0) {
-                SBt[64 * TILE + r] = q0;
-                SBt[65 * TILE + r] = q1;
-                SBt[66 * TILE + r] = q2;
+                __stcs(SBt + 64 * TILE + r, q0);
+                __stcs(SBt + 65 * TILE + r, q1);
+                __stcs(SBt + 66 * TILE + r, q2);
             }
             if (want_xin && qt == 3) {  // de_aug's position rows (E columns 32..34)
                 float dx[8];
@@ -1510,24 +1510,24 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
                     fmax_ = fmaxf(fmax_, fmaxf(fabsf(f0), fabsf(f1)));
                     raw[2 * l][t] = f0;
                     raw[2 * l + 1][t] = f1;
-                    float *jr = Jt + 6 * l * TILE + t;
-                    jr[0] = j00;
-                    jr[TILE] = j01;
-                    jr[2 * TILE] = j02;
-                    jr[3 * TILE] = j10;
-                    jr[4 * TILE] = j11;
-                    jr[5 * TILE] = j12;
+                    float *jr = Jt + 6 * l * TILE + t;  // streaming stores: keep the tables in L2
+                    __stcs(jr, j00);
+                    __stcs(jr + TILE, j01);
+                    __stcs(jr + 2 * TILE, j02);
+                    __stcs(jr + 3 * TILE, j10);
+                    __stcs(jr + 4 * TILE, j11);
+                    __stcs(jr + 5 * TILE, j12);
                 }
             }
         }
         {  // (view-dir loads issued before the level loop)
             float *xvt = ws.xv + tile * XVROWS * TILE + t;
-            xvt[0] = x0;
-            xvt[TILE] = x1;
-            xvt[2 * TILE] = x2;
-            xvt[3 * TILE] = v0;
-            xvt[4 * TILE] = v1;
-            xvt[5 * TILE] = v2;
+            __stcs(xvt, x0);
+            __stcs(xvt + TILE, x1);
+            __stcs(xvt + 2 * TILE, x2);
+            __stcs(xvt + 3 * TILE, v0);
+            __stcs(xvt + 4 * TILE, v1);
+            __stcs(xvt + 5 * TILE, v2);
         }
         const int eE = R.one(fmax_);
         float row[48];
@@ -1543,7 +1543,7 @@ field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__
 #pragma unroll
         for (int i = 0; i < 48; ++i) row[i] *= sc;
         uint8_t *et = ws.e_tiles + tile * 2 * TEB;
-        umma::stage_row<0, 48>(et, et + TEB, t, row);
+        umma::stage_row<0, 48, true>(et, et + TEB, t, row);
         if (t == 0) ws.e_exp[tile] = eE;
         __syncthreads();  // raw[] reuse
     }

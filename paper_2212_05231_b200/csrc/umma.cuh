@@ -234,8 +234,12 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
 // One-thread bulk DMA shared -> global (bulk-group completion; the source buffer may be
 // rewritten after bulk_wait_read() returns in the issuing thread).
 __device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-                 "r"(bytes)
+    // evict-first in L2: the tiles are read back by a later kernel, long after this one
+    // has streamed far more than L2 through; keep L2 for the prefetched next-tile inputs
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -268,7 +272,7 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t &hi, uint32_t 
 }
 
 // Write row r (C values, C % 8 == 0) of a tile as hi and lo parts: 16-B stores.
-template <int kFmt, int C>
+template <int kFmt, int C, bool kStream = false>
 __device__ __forceinline__ void stage_row(uint8_t *hi_tile, uint8_t *lo_tile, int r, const float *v) {
 #pragma unroll
     for (int cb = 0; cb < C; cb += 8) {
@@ -278,8 +282,13 @@ __device__ __forceinline__ void stage_row(uint8_t *hi_tile, uint8_t *lo_tile, in
         split2<kFmt>(v[cb + 4], v[cb + 5], h.z, l.z);
         split2<kFmt>(v[cb + 6], v[cb + 7], h.w, l.w);
         const uint32_t off = tile_off(r, cb, C);
-        *reinterpret_cast<uint4 *>(hi_tile + off) = h;
-        *reinterpret_cast<uint4 *>(lo_tile + off) = l;
+        if (kStream) {  // global destination written once, read by a later kernel
+            __stcs(reinterpret_cast<uint4 *>(hi_tile + off), h);
+            __stcs(reinterpret_cast<uint4 *>(lo_tile + off), l);
+        } else {
+            *reinterpret_cast<uint4 *>(hi_tile + off) = h;
+            *reinterpret_cast<uint4 *>(lo_tile + off) = l;
+        }
     }
 }
 
