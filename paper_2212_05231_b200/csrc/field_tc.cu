@@ -961,7 +961,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             if (4 * qt + i < NA) {
                 const float *jr = jt + 6 * (4 * qt + i) * TILE + r;
 #pragma unroll
-                for (int k = 0; k < 6; ++k) jv[i][k] = jr[k * TILE];
+                for (int k = 0; k < 6; ++k) jv[i][k] = __ldcs(jr + k * TILE);
             }
     };
     auto j_store = [&]() {
@@ -976,7 +976,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     };
     auto fwt = [&](int64_t tl) { return ws.fw_tiles + tl * static_cast<int64_t>(FWB); };
     auto dma = [&](uint32_t soff, const uint8_t *g, uint32_t bytes, uint64_t *mb) {
-        umma::bulk_g2s(S.p(soff), g, bytes, mb);
+        umma::bulk_g2s<true>(S.p(soff), g, bytes, mb);
     };
     {
         const int64_t t0 = blockIdx.x;

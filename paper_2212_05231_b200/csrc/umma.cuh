@@ -221,14 +221,25 @@ __device__ __forceinline__ void prefetch_l2(const void *gptr, uint32_t bytes) {
 
 // One-thread bulk DMA global -> shared (TMA engine, no registers); completion is
 // signalled as transaction bytes on `mbar` (arrive + expect_tx by the same thread).
+template <bool kEvictFirst = false>
 __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *mbar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(sdst)),
-        "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
-        : "memory");
+    if (kEvictFirst) {  // data read exactly once: leave L2 to the prefetched next-tile inputs
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+            "%4;" ::"r"(smem_u32(sdst)),
+            "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar)), "l"(pol)
+            : "memory");
+    } else {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sdst)),
+            "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
+            : "memory");
+    }
 }
 
 // One-thread bulk DMA shared -> global (bulk-group completion; the source buffer may be
