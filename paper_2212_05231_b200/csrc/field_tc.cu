@@ -657,13 +657,13 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
         }
+        const bool jnext = ntile * TILE < P;
+        if (jnext) j_load(ntile);  // next tile's d feature/dx: its latency hides under the Zc1 GEMM
         wait_mma(mbar, phase);
         PMARK(7);
         // ------------------------------------------------ P3: a1c -> Zc2
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
-        const bool jnext = ntile * TILE < P;
-        if (jnext) j_load(ntile);
         {
             float z[2][8], m = 0.f;
             const float sc = pow2i(-(eCin + eC1));
