@@ -1349,12 +1349,12 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
             ph_e ^= 1u;
         }
+        if (has_next) j_load(ntile);  // registers only (TMEM J is rewritten in B5): hides under B4's GEMM
         wait_mma(mbar, phase);
         PMARK(15);
         // ------------------------------------------------ B5: scatter inputs; next tile's DMAs
         // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
         if (t == kDmaThread && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
-        if (has_next) j_load(ntile);  // TMEM J is dead after B4
         {
             // dL/dfeature pairs (DE) and q for the scatter kernel
             const float sde = pow2i(-(eU + eH1));
