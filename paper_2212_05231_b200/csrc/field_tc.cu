@@ -895,7 +895,7 @@ __device__ __noinline__ void fold_acc(int j, int e, uint32_t my, int E, const fl
     }
 }
 
-constexpr int kFoldTiles = 32;
+constexpr int kFoldTiles = 128;
 
 __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
