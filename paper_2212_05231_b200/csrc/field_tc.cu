@@ -492,10 +492,11 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::mbar_wait(mbare, phasee);
             umma::gemm3w<3>(tb + TM_Z1, S.K(TE, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
-            // the previous tile's tile stores must have left smem before P1 restages it:
-            // wait for them while Z1 runs; committing afterwards orders every thread's
-            // P1 staging (which waits on this commit) after the drain
-            if (lane == 0) umma::bulk_wait_read();
+            // the previous tile's A1 (TX), CIN (TC) and A1c (TZ) stores must have left smem
+            // before P1 / P2 / P3 restage those buffers: wait for them while Z1 runs (its
+            // A2c store from TY may still be reading; P3 waits for that one); committing
+            // afterwards orders every thread's P1 staging (which waits on this commit)
+            if (lane == 0) umma::bulk_wait_read_n<1>();
             __syncwarp();
             umma::commit_elect(mbar);
         }
@@ -541,7 +542,9 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 auto h2 = [&](int k) {
                     return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
                 };
-                *reinterpret_cast<uint4 *>(S.p(TY) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
+                // M1 goes to TC (free until P2 stages CIN): TY may still be draining the
+                // previous tile's A2c store
+                *reinterpret_cast<uint4 *>(S.p(TC) + umma::tile_off(r, 8 * (i ? b1 : b0), 64)) =
                     make_uint4(h2(0), h2(2), h2(4), h2(6));
             }
             publish();
@@ -556,7 +559,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         const float d_sdf = xch[r] + xch[TILE + r] + xch[2 * TILE + r] + xch[3 * TILE + r];
         if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<4>(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
-            umma::gemm2a<4>(tb + TM_SA, S.K(TY, T64B, 64), S.MN(WH1S, WH1B, 48), ID_KM(48), false);
+            umma::gemm2a<4>(tb + TM_SA, S.K(TC, T64B, 64), S.MN(WH1S, WH1B, 48), ID_KM(48), false);
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
         }
@@ -697,6 +700,10 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         }
         if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<4>(tb + TM_SB, S.K(TZ, T64B, 64), S.K(WC2, WC2B, 64), ID_KK(64), false);
+            // the previous tile's A2c store (TY) must be done before P4 restages TY: all but
+            // this tile's A1 and CIN stores; the commit orders P4's staging after it
+            if (lane == 0) umma::bulk_wait_read_n<2>();
+            __syncwarp();
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
         }
