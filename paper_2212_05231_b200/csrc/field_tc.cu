@@ -600,14 +600,16 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
                 p1 = fmaf(d0, jl[1], fmaf(d1, jl[4], p1));
                 p2 = fmaf(d0, jl[2], fmaf(d1, jl[5], p2));
             }
-            __syncthreads();  // xch reads of P1 are done
-            xch[(3 * qt + 0) * TILE + r] = p0;
-            xch[(3 * qt + 1) * TILE + r] = p1;
-            xch[(3 * qt + 2) * TILE + r] = p2;
+            // normal partials in rows 4..15 of the scratch (P1's d partials, rows 0..3, may
+            // still be being read: no barrier needed before these writes)
+            float *xn = xch + 4 * TILE;
+            xn[(3 * qt + 0) * TILE + r] = p0;
+            xn[(3 * qt + 1) * TILE + r] = p1;
+            xn[(3 * qt + 2) * TILE + r] = p2;
             __syncthreads();
-            const float n0 = xch[r] + xch[3 * TILE + r] + xch[6 * TILE + r] + xch[9 * TILE + r];
-            const float n1 = xch[TILE + r] + xch[4 * TILE + r] + xch[7 * TILE + r] + xch[10 * TILE + r];
-            const float n2 = xch[2 * TILE + r] + xch[5 * TILE + r] + xch[8 * TILE + r] + xch[11 * TILE + r];
+            const float n0 = xn[r] + xn[3 * TILE + r] + xn[6 * TILE + r] + xn[9 * TILE + r];
+            const float n1 = xn[TILE + r] + xn[4 * TILE + r] + xn[7 * TILE + r] + xn[10 * TILE + r];
+            const float n2 = xn[2 * TILE + r] + xn[5 * TILE + r] + xn[8 * TILE + r] + xn[11 * TILE + r];
             const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
             if (valid && qt == 0) eik += (nn - 1.f) * (nn - 1.f);
             // cin = [x, n, v, y] (field.py:237-239); quarter k stages block k of the 32
