@@ -1763,20 +1763,19 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
                         }
                     }
                 }
-                if (lane == 31 || ((heads >> (lane + 1)) & 1u))
+                if (!(lane == 31 || ((heads >> (lane + 1)) & 1u))) continue;  // not a run's last lane
+            } else if (!valid) {
+                continue;
+            }
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) red_add_f32x2(gt + 2 * row[c], a[c], b[c]);
-            } else if (valid) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {  // x-pairs (c, c + 4): one 16-B RED when adjacent
-                    if ((row[c] ^ row[c + 4]) == 1u) {
-                        const bool sw = row[c] & 1u;
-                        red_add_f32x4(gt + 2 * (row[c] & ~1u), sw ? a[c + 4] : a[c], sw ? b[c + 4] : b[c],
-                                      sw ? a[c] : a[c + 4], sw ? b[c] : b[c + 4]);
-                    } else {
-                        red_add_f32x2(gt + 2 * row[c], a[c], b[c]);
-                        red_add_f32x2(gt + 2 * row[c + 4], a[c + 4], b[c + 4]);
-                    }
+            for (int c = 0; c < 4; ++c) {  // x-pairs (c, c + 4): one 16-B RED when adjacent
+                if ((row[c] ^ row[c + 4]) == 1u) {
+                    const bool sw = row[c] & 1u;
+                    red_add_f32x4(gt + 2 * (row[c] & ~1u), sw ? a[c + 4] : a[c], sw ? b[c + 4] : b[c],
+                                  sw ? a[c] : a[c + 4], sw ? b[c] : b[c + 4]);
+                } else {
+                    red_add_f32x2(gt + 2 * row[c], a[c], b[c]);
+                    red_add_f32x2(gt + 2 * row[c + 4], a[c + 4], b[c + 4]);
                 }
             }
         }
