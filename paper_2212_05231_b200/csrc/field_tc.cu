@@ -1664,7 +1664,7 @@ __device__ __forceinline__ void red_add_f32x4(float *addr, float a, float b, flo
     atomicAdd(reinterpret_cast<float4 *>(addr), make_float4(a, b, c, d));
 }
 
-__global__ void __launch_bounds__(TILE)
+__global__ void __launch_bounds__(TILE, 6)
 field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count,
                      const Workspace ws, float *__restrict__ g_tab, int agg_levels) {
     __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
