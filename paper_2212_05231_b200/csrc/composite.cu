@@ -238,7 +238,7 @@ int ns2b_composite(const int32_t *offsets, int64_t nrays, const float *sdf, cons
                    double *sums, void *stream) {
     NS2B_REQUIRE(rendered && alphas && weights && trans_before, "composite: output buffers required");
     if (nrays == 0) return NS2B_OK;
-    const int blocks = grid_for(nrays * 32, CBLOCK, kNumSMs * 8);
+    const int blocks = grid_for(nrays * 32, CBLOCK, kNumSMs * 16);
     cudaStream_t st = as_stream(stream);
     if (targets) {
         NS2B_REQUIRE(dl_dc && dl_dsdf && sums, "composite: cotangent buffers required with targets");
@@ -262,7 +262,7 @@ int ns2b_composite_backward(const int32_t *offsets, int64_t nrays, const float *
     NS2B_REQUIRE(alphas && weights && trans_before && dl_dray && dl_dc && dl_dsdf,
                  "composite_backward: null buffer");
     if (nrays == 0) return NS2B_OK;
-    const int blocks = grid_for(nrays * 32, CBLOCK, kNumSMs * 8);
+    const int blocks = grid_for(nrays * 32, CBLOCK, kNumSMs * 16);
     composite_kernel<kBwd><<<blocks, CBLOCK, 0, as_stream(stream)>>>(
         offsets, nrays, sdf, colors, sharpness, nullptr, 0.0, 1.0, dl_dray, nullptr, nullptr,
         const_cast<double *>(alphas), const_cast<double *>(weights), const_cast<double *>(trans_before),

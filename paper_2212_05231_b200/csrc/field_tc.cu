@@ -1820,7 +1820,7 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
     switch (which) {
     case 0:
-        tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 1024), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
+        tc::field_gather_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
                                                                                          count, ws);
         return check_launch("field_gather");
     case 1:
@@ -1834,7 +1834,7 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
             0);
         return check_launch("field_mlp_backward");
     default:
-        tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 1024), tc::TILE, 0, st>>>(f, pos32, count, ws,
+        tc::field_scatter_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::TILE, 0, st>>>(f, pos32, count, ws,
                                                                                        grad_tables, tc::agg_levels_env());
         return check_launch("field_scatter");
     }
@@ -1851,7 +1851,7 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
-    tc::field_gather_kernel<<<grid_for(ntiles, 1, kNumSMs * 1024), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
+    tc::field_gather_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
                                                                                          count, ws);
     if ((rc = check_launch("field_gather"))) return rc;
     tc::field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
@@ -1883,7 +1883,7 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
         if ((rc = check_launch("field_input_levels"))) return rc;
     }
     if (grad_tables == nullptr) return NS2B_OK;
-    tc::field_scatter_kernel<<<grid_for(ntiles, 1, kNumSMs * 1024), tc::TILE, 0, st>>>(f, pos32, count, ws,
+    tc::field_scatter_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::TILE, 0, st>>>(f, pos32, count, ws,
                                                                                    grad_tables, tc::agg_levels_env());
     return check_launch("field_scatter");
 }
