@@ -1,13 +1,18 @@
 """Bias-free ReLU MLP weights on the GPU (container API of `hashsdf/relu_mlp.py`).
 
-The per-sample MLP arithmetic (forward, input-Jacobian row, first-order backward
-and the Theorem-1 row contraction, `relu_mlp.py:94-216`) is fused into the field
-kernels of libns2b (csrc/field.cu); this module only holds the layer matrices as
-CUDA tensors (views into the flat parameter buffer) and mirrors the reference's
-shape validation and seeded initialisation.
+On the training path the per-sample MLP arithmetic (forward, input-Jacobian row,
+first-order backward and the Theorem-1 row contraction, `relu_mlp.py:94-216`) is fused
+into the tcgen05 field kernels of libns2b (csrc/field_tc.cu).  This module holds the
+layer matrices as CUDA tensors (views into the flat parameter buffer), mirrors the
+reference's shape validation and seeded initialisation, and keeps the reference's
+standalone array functions (`forward`, `input_jacobian_rows`, `backward_first`,
+`backward_second_row`) for callers outside the step: those are plain batched GEMMs
+(cuBLAS through torch) on device tensors, fp32, same masks (strict z > 0), same errors.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -15,7 +20,8 @@ import torch
 from . import _lib
 from ._lib import ShapeError
 
-__all__ = ["ShapeError", "MlpWeights"]
+__all__ = ["ShapeError", "MlpWeights", "ForwardTrace", "forward", "input_jacobian_rows",
+           "backward_first", "backward_second_row"]
 
 
 class MlpWeights:
@@ -76,3 +82,76 @@ def _to_device(h):
             h = h.to(device=_lib.device(), dtype=torch.float32)
         return h
     return torch.from_numpy(np.ascontiguousarray(h, dtype=np.float32)).to(_lib.device())
+
+
+@dataclass
+class ForwardTrace:
+    """`relu_mlp.py:80-91`: batched input, post-ReLU activations and 0/1 masks per
+    hidden layer, and the output (all (P, n) fp32 CUDA tensors)."""
+    x: torch.Tensor
+    activations: list
+    masks: list
+    y: torch.Tensor
+
+
+def _as_batch(a):
+    t = _to_device(a)
+    return (t[None, :] if t.dim() == 1 else t), t.dim() == 1
+
+
+def forward(weights, x):
+    """`relu_mlp.py:94-111`: returns (y, trace); x may be (n_0,) or (P, n_0)."""
+    xb, single = _as_batch(x)
+    if xb.shape[1] != weights.in_dim:
+        raise ShapeError("shape error: input dim mismatch")
+    acts, masks = [], []
+    a = xb
+    for h in weights.layers[:-1]:
+        z = a @ h.T
+        m = (z > 0).to(torch.float32)
+        a = z * m
+        masks.append(m)
+        acts.append(a)
+    y = a @ weights.layers[-1].T
+    return (y[0] if single else y), ForwardTrace(xb, acts, masks, y)
+
+
+def input_jacobian_rows(weights, trace, rows):
+    """`relu_mlp.py:123-129`: selected rows of dy/dx, (P, len(rows), n_0)."""
+    rows = list(rows)
+    jac = weights.layers[-1][rows].expand(trace.x.shape[0], -1, -1)
+    for h, m in zip(weights.layers[-2::-1], trace.masks[::-1]):
+        jac = (jac * m[:, None, :]) @ h
+    return jac
+
+
+def backward_first(weights, trace, dl_dy):
+    """`relu_mlp.py:132-147`: ([dL/dH_l], dL/dx)."""
+    g, single = _as_batch(dl_dy)
+    if tuple(g.shape) != tuple(trace.y.shape):
+        raise ShapeError("shape error: cotangent does not match output")
+    grads = [None] * weights.depth
+    up = g
+    for l in range(weights.depth - 1, 0, -1):
+        grads[l] = up.T @ trace.activations[l - 1]
+        up = (up @ weights.layers[l]) * trace.masks[l - 1]
+    grads[0] = up.T @ trace.x
+    dl_dx = up @ weights.layers[0]
+    return grads, (dl_dx[0] if single else dl_dx)
+
+
+def backward_second_row(weights, trace, row, row_cotangent):
+    """`relu_mlp.py:191-216` (Theorem 1 for one Jacobian row): dH_l = svec_l^T pvec_l."""
+    mvec, _ = _as_batch(row_cotangent)
+    depth = weights.depth
+    svec = [None] * depth
+    svec[-1] = torch.zeros((mvec.shape[0], weights.out_dim), dtype=torch.float32, device=mvec.device)
+    svec[-1][:, row] = 1.0
+    for l in range(depth - 2, -1, -1):
+        svec[l] = (svec[l + 1] @ weights.layers[l + 1]) * trace.masks[l]
+    grads, pvec = [], mvec
+    for l in range(depth):
+        grads.append(svec[l].T @ pvec)
+        if l < depth - 1:
+            pvec = (pvec @ weights.layers[l].T) * trace.masks[l]
+    return grads

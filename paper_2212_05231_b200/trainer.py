@@ -119,6 +119,23 @@ def huber_grad(residual, delta):
     return np.where(np.abs(r) <= delta, r / delta, np.sign(r))
 
 
+def color_loss(rendered, targets, delta):
+    """`trainer.py:108-112`: mean over rays of the channel-summed Huber (host arrays)."""
+    r = np.asarray(rendered)
+    if r.shape[0] < 1:
+        raise ValueError("need at least one ray")
+    return float(huber(r - np.asarray(targets), delta).sum(axis=1).mean())
+
+
+def eikonal_loss(normals):
+    """`trainer.py:115-120`: mean (||n|| - 1)^2 (host arrays)."""
+    n = np.asarray(normals)
+    if n.shape[0] < 1:
+        raise ValueError("need at least one normal")
+    nn = np.linalg.norm(np.atleast_2d(n), axis=1)
+    return float(((nn - 1.0) ** 2).mean())
+
+
 def psnr_from_mse(mse):
     return 100.0 if mse < 1e-10 else float(10.0 * np.log10(1.0 / mse))
 
