@@ -399,3 +399,78 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0):
               _lib.f64_array(lrs), _lib.i64_array(ts), len(names), cfg.adam_beta1,
               cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
 
+
+
+def masked_psnr(image_a, image_b, mask):
+    """`trainer.py:145-149` (host helper)."""
+    sel = np.asarray(mask) > 0.5
+    if not np.any(sel):
+        return 100.0
+    return psnr(np.asarray(image_a)[sel], np.asarray(image_b)[sel])
+
+
+@dataclass
+class TrainResult:
+    """`trainer.py:313-318`."""
+    state: TrainState
+    reports: list
+    checkpoint_path: object = None
+    wall_seconds: float = 0.0
+
+
+def train_static(dataset, config, out_path=None, time_index=0, state=None, log_every=100):
+    """Static training loop (`trainer.py:321-347`): `train_step` until
+    `config.total_steps`, reports every `log_every` steps and at the last step, then the
+    NS2C checkpoint at `out_path` plus the `.loss.csv` log next to it."""
+    import time
+    from pathlib import Path
+
+    from . import checkpoint
+
+    if state is None:
+        state = TrainState.create(config, aabb=dataset.scene_aabb)
+    reports = []
+    t0 = time.perf_counter()
+    while state.step < config.total_steps:
+        rep = train_step(state, dataset, time_index)
+        if rep.step % log_every == 0 or rep.step == config.total_steps - 1:
+            reports.append(rep)
+    wall = time.perf_counter() - t0
+    ckpt = None
+    if out_path is not None:
+        ckpt = Path(out_path)
+        checkpoint.save_checkpoint(ckpt, state)
+        lines = ["step,color,eikonal,total,lambda,psnr"]
+        lines += [f"{r.step},{r.color:.6f},{r.eikonal:.6f},{r.total:.6f},{r.level},{r.psnr:.3f}"
+                  for r in reports]
+        ckpt.with_suffix(ckpt.suffix + ".loss.csv").write_text("\n".join(lines) + "\n")
+    return TrainResult(state, reports, ckpt, wall)
+
+
+def render_frame(params, occ, frame, level=None, chunk=1 << 18, point_transform=None,
+                 dir_transform=None):
+    """Full camera view (`trainer.py:350-370`) through `render_rays` in ray chunks
+    (rays are independent, so the chunk size does not change the result; the
+    reference's 8192 is a host-memory bound).  Returns host (H,W,3) image and (H,W)
+    expected depth, fp64 like the reference."""
+    level = level if level is not None else params.grid.num_levels
+    origins, dirs = scene_io.generate_rays_grid(frame)
+    n = origins.shape[0]
+    img = np.zeros((n, 3))
+    depth = np.zeros(n)
+    for s in range(0, n, chunk):
+        e = min(s + chunk, n)
+        batch = scene_io.RayBatch(origins[s:e], dirs[s:e], np.zeros((e - s, 3)), np.ones(e - s, bool))
+        cols, rec = renderer.render_rays(batch, params, occ, level, point_transform=point_transform,
+                                         dir_transform=dir_transform)
+        img[s:e] = cols.cpu().numpy()
+        depth[s:e] = renderer.expected_depth(rec).cpu().numpy()
+    return img.reshape(frame.height, frame.width, 3), depth.reshape(frame.height, frame.width)
+
+
+def evaluate_view(params, occ, frame, level=None, point_transform=None, dir_transform=None):
+    """Masked and full-frame PSNR of a rendered view (`trainer.py:373-382`)."""
+    img, _ = render_frame(params, occ, frame, level, point_transform=point_transform,
+                          dir_transform=dir_transform)
+    target = frame.image * frame.mask[:, :, None]
+    return {"psnr_masked": masked_psnr(img, target, frame.mask), "psnr_full": psnr(img, target)}

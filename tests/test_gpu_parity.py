@@ -401,3 +401,45 @@ def test_edge_batches_match_oracle(sphere64, case):
         assert np.array_equal(np_(pst.params.flat), before), "Adam must be skipped when P = 0"
         assert pst.adam["tables"].t == t_before == ost.adam["tables"].t
     assert pst.step == ost.step == 2
+
+
+def test_render_frame_and_evaluate_view(sphere64):
+    """Evaluation rendering (`trainer.py:350-382`): a full 64x64 view through
+    `render_frame` (chunked, so chunk boundaries fall inside the image) vs the oracle's
+    `render_rays` + `expected_depth` on the same pixel-grid rays."""
+    ost = _c1_state()
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    ost.params.grid.tables[:] = cases.trained_tables(8, 2**14, scale=0.05)
+    pp = product_params_from_oracle(ost.params)
+    pocc = prender.OccupancyGrid(128)
+    pocc.set_bits(ost.occ.bits)
+    frame = sphere64.frames[0]
+    o, d = oscene.generate_rays_grid(frame)
+    b = oscene.RayBatch(o, d, np.zeros((o.shape[0], 3)), np.ones(o.shape[0], bool))
+    oc, orec = orender.render_rays(b, ost.params, ost.occ, 8)
+    img, depth = ptrain.render_frame(pp, pocc, frame, 8, chunk=1000)
+    assert img.shape == (frame.height, frame.width, 3) and depth.shape == (frame.height, frame.width)
+    assert_close(img.reshape(-1, 3), oc, TOL, "image")
+    assert_close(depth.reshape(-1), orender.expected_depth(orec), TOL, "depth")
+    ev = ptrain.evaluate_view(pp, pocc, frame, 8)
+    target = frame.image * frame.mask[:, :, None]
+    assert ev["psnr_full"] == pytest.approx(otrain.psnr(oc.reshape(img.shape), target), abs=1e-3)
+    assert ev["psnr_masked"] == pytest.approx(
+        ptrain.masked_psnr(oc.reshape(img.shape), target, frame.mask), abs=1e-3)
+
+
+def test_train_static_writes_checkpoint_and_log(tmp_path):
+    """`trainer.train_static` (`trainer.py:321-347`): loop to total_steps, NS2C
+    checkpoint + loss CSV, resumable through `checkpoint.load_checkpoint`."""
+    from paper_2212_05231_b200 import checkpoint as pckpt
+    from paper_2212_05231_b200 import scene_io as pscene
+
+    ds = pscene.make_synthetic("sphere", views=4, seed=0, image_size=32)
+    cfg = ptrain.TrainConfig(batch_size=512, num_levels=8, table_size=2**14, total_steps=3)
+    res = ptrain.train_static(ds, cfg, out_path=tmp_path / "run.ns2c", log_every=2)
+    assert res.state.step == 3 and [r.step for r in res.reports] == [0, 2]
+    assert res.checkpoint_path.exists()
+    csv = (tmp_path / "run.ns2c.loss.csv").read_text().splitlines()
+    assert csv[0] == "step,color,eikonal,total,lambda,psnr" and len(csv) == 3
+    st, _ = pckpt.load_checkpoint(res.checkpoint_path)
+    assert st.step == 3
