@@ -314,6 +314,30 @@ def field_sdf_only(params, positions, max_level):
     return out
 
 
+def sigmoid(z):
+    """Stable logistic (`field.py:40-46`) on host arrays or device tensors."""
+    if isinstance(z, torch.Tensor):
+        return torch.sigmoid(z)
+    z = np.asarray(z)
+    out = np.empty_like(z)
+    pos = z >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-z[pos]))
+    ez = np.exp(z[~pos])
+    out[~pos] = ez / (1.0 + ez)
+    return out
+
+
+def eval_color(params, cache, view_dirs):
+    """Colour of an evaluated batch for new view directions (`field.py:258-269`).  The
+    colour net is fused into the field forward kernel, so this re-runs the forward at the
+    cached positions and level cutoff with the new directions and refreshes the cache
+    (the SDF outputs are unchanged, so field_backward sees a consistent cache)."""
+    fresh = eval_field(params, cache.x, view_dirs, cache.max_level, need_color=True)
+    for k in ("ray_ids", "dirs", "count", "sdf", "normals", "colors", "geo", "has_color", "workspace"):
+        setattr(cache, k, getattr(fresh, k))
+    return cache.colors
+
+
 def field_backward(params, cache, dl_dc=None, dl_dd=None, dl_dn=None, need_input_grads=False,
                    grads=None):
     """Parameter gradients from per-sample cotangents (`field.py:272-350`).

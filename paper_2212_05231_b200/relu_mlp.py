@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import ShapeError
 
 __all__ = ["ShapeError", "MlpWeights", "ForwardTrace", "forward", "input_jacobian_rows",
-           "backward_first", "backward_second_row"]
+           "backward_first", "backward_second", "backward_second_row", "input_jacobian"]
 
 
 class MlpWeights:
@@ -155,3 +155,28 @@ def backward_second_row(weights, trace, row, row_cotangent):
         if l < depth - 1:
             pvec = (pvec @ weights.layers[l].T) * trace.masks[l]
     return grads
+
+
+def input_jacobian(weights, trace):
+    """`relu_mlp.py:114-120`: full dy/dx per sample, (P, n_L, n_0)."""
+    return input_jacobian_rows(weights, trace, range(weights.out_dim))
+
+
+def backward_second(weights, trace, jac_cotangent):
+    """`relu_mlp.py:150-188`: gradients of sum_p <M_p, (dy/dx)_p> w.r.t. each layer
+    (masks constant), from the per-sample partial products S_l (output side) and P_l
+    (input side): dH_l = sum_p S_l^T M_p P_l^T."""
+    m = _to_device(jac_cotangent)
+    if m.dim() == 2:
+        m = m[None]
+    npts, depth = m.shape[0], weights.depth
+    back = [None] * depth
+    back[-1] = torch.eye(weights.out_dim, device=m.device).expand(npts, -1, -1)
+    for l in range(depth - 2, -1, -1):
+        back[l] = (back[l + 1] @ weights.layers[l + 1]) * trace.masks[l][:, None, :]
+    fwd = [None] * depth
+    fwd[0] = torch.eye(weights.in_dim, device=m.device).expand(npts, -1, -1)
+    for l in range(1, depth):
+        fwd[l] = trace.masks[l - 1][:, :, None] * (weights.layers[l - 1] @ fwd[l - 1])
+    return [torch.tensordot(back[l].transpose(1, 2) @ m, fwd[l], dims=([0, 2], [0, 2]))
+            for l in range(depth)]

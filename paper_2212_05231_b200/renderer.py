@@ -179,6 +179,27 @@ def march_count_and_scan(o, d, occ, counts, offsets, stream=None):
               ctypes.byref(need), st)
 
 
+def intersect_aabb(origins, dirs, lo, hi):
+    """Slab test (`renderer.py:153-168`) as fp64 device tensor ops with the reference's
+    operation order (1/d, then (lo-o)*inv), so the entry/exit values are bit-identical;
+    the marcher (`ns2b_march_*`) runs the same arithmetic inline.  Returns device
+    (t_enter, t_exit); exit < enter on a miss."""
+    o = as_device(origins, torch.float64).reshape(-1, 3)
+    d = as_device(dirs, torch.float64).reshape(-1, 3)
+    lo_t = torch.as_tensor(np.asarray(lo, np.float64), device=o.device)
+    hi_t = torch.as_tensor(np.asarray(hi, np.float64), device=o.device)
+    inv = 1.0 / d
+    t1 = (lo_t - o) * inv
+    t2 = (hi_t - o) * inv
+    near, far = torch.minimum(t1, t2), torch.maximum(t1, t2)
+    par = d.abs() < 1e-12
+    inside = (o >= lo_t) & (o <= hi_t)
+    inf = torch.tensor(float("inf"), dtype=torch.float64, device=o.device)
+    near = torch.where(par, torch.where(inside, -inf, inf), near)
+    far = torch.where(par, torch.where(inside, inf, -inf), far)
+    return torch.clamp(near.amax(dim=1), min=0.0), far.amin(dim=1)
+
+
 def march_rays(origins, dirs, occ, need_t=True, need_pos64=True):
     """Fixed-stride marching with empty-space skipping (`renderer.py:171-192`)."""
     o = as_device(origins, torch.float64).reshape(-1, 3).contiguous()

@@ -122,3 +122,56 @@ def test_reference_error_contract():
         pfield.SdfFieldParams(grid, pmlp.MlpWeights([np.ones((64, grid.encoding_dim + 1), np.float32),
                                                      np.ones((15, 64), np.float32)]),
                               params.color_net, 0.0)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_mlp_full_jacobian_and_backward_second_golden(depth):
+    """`relu_mlp.input_jacobian` / `backward_second` (full cotangent M) vs the golden
+    vectors (`relu_mlp.py:114-188`)."""
+    gold = dict(np.load(GOLD / "mlp.npz", allow_pickle=False))
+    k = f"d{depth}_"
+    w = pmlp.MlpWeights([gold[k + f"w{i}"] for i in range(depth)])
+    _, tr = pmlp.forward(w, gold[k + "x"])
+    ow = omlp.MlpWeights([gold[k + f"w{i}"] for i in range(depth)])
+    _, otr = omlp.forward(ow, gold[k + "x"])
+    assert_close(_np(pmlp.input_jacobian(w, tr)),
+                 omlp.input_jacobian_rows(ow, otr, list(range(ow.out_dim))), TOL, "jac")
+    g2 = pmlp.backward_second(w, tr, gold[k + "m"])
+    for i in range(depth):
+        assert_close(_np(g2[i]), gold[k + f"g2_{i}"], TOL, f"g2_{i}")
+
+
+def test_intersect_aabb_bit_exact():
+    from oracle import render as orender
+    from paper_2212_05231_b200 import renderer as prender
+
+    rng = np.random.default_rng(4)
+    o = rng.uniform(-3, 3, (4096, 3))
+    d = rng.standard_normal((4096, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d[:8, 1] = 0.0  # axis-parallel rays, inside and outside the slab
+    o[:4, 1] = 0.5
+    lo, hi = np.array([-1.0, -1.0, -1.0]), np.array([1.0, 1.0, 1.0])
+    te, tx = prender.intersect_aabb(o, d, lo, hi)
+    re, rx = orender.intersect_aabb(o, d, lo, hi)
+    assert np.array_equal(_np(te), re) and np.array_equal(_np(tx), rx)
+
+
+def test_eval_color_and_sigmoid():
+    from helpers import product_params_from_oracle
+    from oracle import field as ofield
+    from paper_2212_05231_b200 import field as pfield
+    from test_oracle_golden import oracle_field_params
+
+    z = np.linspace(-50, 50, 101)
+    assert np.array_equal(pfield.sigmoid(z), ofield.sigmoid(z))
+    op = oracle_field_params("c1")
+    pp = product_params_from_oracle(op)
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-0.9, 0.9, (2048, 3)).astype(np.float32)
+    v1, v2 = (rng.standard_normal((2048, 3)) for _ in range(2))
+    v1 /= np.linalg.norm(v1, axis=1, keepdims=True)
+    v2 /= np.linalg.norm(v2, axis=1, keepdims=True)
+    cache = pfield.eval_field(pp, x, v1, 8)
+    cols = pfield.eval_color(pp, cache, v2)
+    assert_close(_np(cols), ofield.eval_field(op, x, v2, 8).colors, TOL, "colors")
