@@ -32,6 +32,7 @@ from . import _lib
 from . import field as fieldmod
 from . import hash_encoding as enc
 from . import renderer, scene_io
+from .hash_encoding import as_device
 from .parallel import DataParallel
 
 
@@ -362,7 +363,7 @@ def train_step(state, dataset, time_index=0, batch=None):
     return report
 
 
-def _apply_gradients(state, n_active, sharpness, lr_scale=1.0):
+def _apply_gradients(state, n_active, sharpness, lr_scale=1.0, schedule=True):
     """Divergence check, s_log Adam, then one multi-group Adam launch over
     [sdf_0 | sdf_1 | color_0..2 | tables[:n_active]] (`trainer.py:243-278`).
     `lr_scale` multiplies every group's learning rate (dynamic frames > 0 fine-tune
@@ -371,7 +372,7 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0):
     params, ws = state.params, state.ws
     lay = params.layout
     sp = _lib.stream_ptr()
-    scale = lr_factor(state.step, cfg.total_steps, cfg.lr_final_fraction) * lr_scale
+    scale = (lr_factor(state.step, cfg.total_steps, cfg.lr_final_fraction) if schedule else 1.0) * lr_scale
     lr_t, lr_m = cfg.lr_tables * scale, cfg.lr_mlp * scale
     names = ["sdf_0", "sdf_1", "color_0", "color_1", "color_2", "tables"]
     offs = lay.sdf_offs + lay.color_offs + [lay.tables_off]
@@ -399,6 +400,32 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0):
               _lib.f64_array(lrs), _lib.i64_array(ts), len(names), cfg.adam_beta1,
               cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
 
+
+def apply_gradients(state, grads, dl_dslog, lr_scale=1.0, max_active_level=None):
+    """Module-API Adam step (`trainer.py:243-278`) for callers that assemble their own
+    FieldGrads (train_step applies the same kernels to its fused gradient buffer):
+    `lr_scale` is the full learning-rate factor as in the reference (train_step passes
+    the cosine `lr_factor`), levels >= `max_active_level` are skipped, and a
+    non-finite gradient raises FloatingPointError("divergence: ...") naming the first
+    bad group in the reference's order (here no group has been stepped when it raises;
+    the reference has already stepped the groups it checked before the bad one)."""
+    params, ws = state.params, state.ws
+    na = params.grid.num_levels if max_active_level is None else int(max_active_level)
+    if grads.flat is not None:
+        ws.grads.copy_(grads.flat)
+    else:
+        sdf, col, tab = params.layout.views(ws.grads)
+        for dst, src in zip(sdf + col + [tab], list(grads.sdf_layers) + list(grads.color_layers)
+                            + [grads.tables]):
+            dst.copy_(as_device(src, torch.float32).reshape(dst.shape))
+    ws.sums[1:2].fill_(float(dl_dslog))
+    ws.flag.zero_()
+    _apply_gradients(state, na, 1.0, lr_scale, schedule=False)
+    bits = int(ws.flag.item())
+    if bits:
+        name = next(n for n in _CHECK_ORDER if bits & (1 << _CHECK_ORDER.index(n)))
+        raise FloatingPointError(f"divergence: non-finite gradient for {name}")
+    params.refresh_host_mirror(float(params.sharpness_log.item()))
 
 
 def masked_psnr(image_a, image_b, mask):

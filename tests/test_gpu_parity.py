@@ -7,6 +7,8 @@ max|ref|) in fp32 arithmetic with fp32 table storage.
 
 from __future__ import annotations
 
+from types import SimpleNamespace
+
 import numpy as np
 import pytest
 
@@ -443,3 +445,26 @@ def test_train_static_writes_checkpoint_and_log(tmp_path):
     assert csv[0] == "step,color,eikonal,total,lambda,psnr" and len(csv) == 3
     st, _ = pckpt.load_checkpoint(res.checkpoint_path)
     assert st.step == 3
+
+
+def test_apply_gradients_module_api():
+    """`trainer.apply_gradients` (`trainer.py:243-278`) on caller-built FieldGrads vs the
+    oracle: two steps, lr_scale 0.7, levels >= 5 skipped; then the divergence error."""
+    ost = _c1_state()
+    pst = product_state_from_oracle(ost)
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        tab = rng.standard_normal(ost.params.grid.tables.shape).astype(np.float32) * 1e-3
+        sdf = [rng.standard_normal(h.shape).astype(np.float32) * 1e-2 for h in ost.params.sdf_net.layers]
+        col = [rng.standard_normal(h.shape).astype(np.float32) * 1e-2 for h in ost.params.color_net.layers]
+        dslog = float(rng.standard_normal())
+        otrain.apply_gradients(ost, SimpleNamespace(tables=tab, sdf_layers=sdf, color_layers=col), dslog, 0.7, 5)
+        ptrain.apply_gradients(pst, pfield.FieldGrads(torch.from_numpy(tab), sdf, col), dslog, 0.7, 5)
+    assert_close(np_(pst.params.grid.tables), ost.params.grid.tables, 1e-6, "tables")
+    for a, b in zip(pst.params.sdf_net.layers + pst.params.color_net.layers,
+                    ost.params.sdf_net.layers + ost.params.color_net.layers):
+        assert_close(np_(a), b, 1e-6, "mlp")
+    assert abs(float(pst.params.sharpness_log.item()) - float(np.asarray(ost.params.sharpness_log).ravel()[0])) <= 1e-12
+    sdf[1][0, 0] = np.nan
+    with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for sdf_1"):
+        ptrain.apply_gradients(pst, pfield.FieldGrads(torch.from_numpy(tab), sdf, col), 0.0)
