@@ -401,6 +401,35 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0, schedule=True):
               cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
 
 
+def compute_cotangents(state, batch, rendered, records):
+    """Module-API loss + cotangents (`trainer.py:215-240`) for a rendered batch, on the
+    device (train_step fuses the same arithmetic into ns2b_composite and the MLP
+    kernels): Huber colour loss and its ray cotangent /m, `renderer.backward_cotangents`,
+    and the Eikonal loss/cotangent over all P samples.  Returns (color_loss,
+    eikonal_loss, total, dl_dcolors (P,3), dl_dsdf (P,), dl_dslog, dl_dn (P,3) or None)."""
+    cfg = state.config
+    m = batch.count
+    r = as_device(rendered, torch.float64).reshape(-1, 3)
+    resid = r - as_device(batch.target_colors, torch.float64).reshape(-1, 3)
+    if m < 1:
+        raise ValueError("need at least one ray")
+    delta = cfg.huber_delta
+    a = resid.abs()
+    c_loss = float(torch.where(a <= delta, 0.5 * resid * resid / delta, a - 0.5 * delta).sum(1).mean())
+    dl_dray = torch.where(a <= delta, resid / delta, torch.sign(resid)) / m
+    dl_dcolors, dl_dsdf, dl_dslog = renderer.backward_cotangents(records, dl_dray)
+    nsamp = records.sample_count
+    if nsamp > 0:
+        n = records.cache.normals
+        norms = torch.linalg.vector_norm(n, dim=1)
+        e_loss = float(((norms - 1.0) ** 2).mean())
+        dl_dn = (cfg.eikonal_weight * (2.0 * (norms - 1.0) / torch.clamp(norms, min=1e-12))[:, None]
+                 * n / nsamp)
+    else:
+        e_loss, dl_dn = 0.0, None
+    return c_loss, e_loss, c_loss + cfg.eikonal_weight * e_loss, dl_dcolors, dl_dsdf, dl_dslog, dl_dn
+
+
 def apply_gradients(state, grads, dl_dslog, lr_scale=1.0, max_active_level=None):
     """Module-API Adam step (`trainer.py:243-278`) for callers that assemble their own
     FieldGrads (train_step applies the same kernels to its fused gradient buffer):

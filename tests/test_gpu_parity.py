@@ -468,3 +468,23 @@ def test_apply_gradients_module_api():
     sdf[1][0, 0] = np.nan
     with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for sdf_1"):
         ptrain.apply_gradients(pst, pfield.FieldGrads(torch.from_numpy(tab), sdf, col), 0.0)
+
+
+def test_compute_cotangents_module_api(sphere64):
+    """`trainer.compute_cotangents` (`trainer.py:215-240`) on the device vs the oracle,
+    on the same rendered batch."""
+    ost = _c1_state()
+    orender.update_occupancy(ost.occ, ost.params, 8)
+    ost.params.grid.tables[:] = cases.trained_tables(8, 2**14, scale=0.05)
+    pst = product_state_from_oracle(ost)
+    b = oscene.sample_ray_batch(sphere64, 0, 4096, 0.9, np.random.default_rng(2))
+    oc, orec = orender.render_rays(b, ost.params, ost.occ, 8)
+    pc, prec = prender.render_rays(b, pst.params, pst.occ, 8)
+    o = otrain.compute_cotangents(ost, b, oc, orec)
+    p = ptrain.compute_cotangents(pst, b, pc, prec)
+    for i in range(3):
+        assert abs(p[i] - o[i]) <= TOL * abs(o[i]), i
+    assert_close(np_(p[3]), o[3], TOL, "dl_dcolors")
+    assert_close(np_(p[4]), o[4], TOL, "dl_dsdf")
+    assert abs(p[5] - o[5]) <= TOL * max(abs(o[5]), 1e-12)
+    assert_close(np_(p[6]), o[6], TOL, "dl_dn")
