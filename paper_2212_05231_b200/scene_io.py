@@ -16,6 +16,9 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+# pose orthonormality tolerance of CameraFrame.validate (`scene_io.py:26`)
+POSE_ORTHO_TOL = 1e-4
+
 LIGHT = np.array([0.35, 0.45, 0.82]) / np.linalg.norm([0.35, 0.45, 0.82])
 AMBIENT = 0.3
 
@@ -32,6 +35,17 @@ class CameraFrame:
     image: np.ndarray
     mask: np.ndarray
     time_index: int = 0
+
+    def validate(self):
+        """`scene_io.py:44-57`."""
+        rot = self.pose[:3, :3]
+        if (np.abs(rot @ rot.T - np.eye(3)).max() > POSE_ORTHO_TOL
+                or abs(np.linalg.det(rot) - 1.0) > POSE_ORTHO_TOL):
+            raise ValueError("invalid pose")
+        if self.image.shape[:2] != (self.height, self.width) or self.mask.shape != (self.height, self.width):
+            raise ValueError("inconsistent frame")
+        if self.image.min() < 0 or self.image.max() > 1:
+            raise ValueError("inconsistent frame: pixel values outside [0,1]")
 
 
 @dataclass
@@ -79,6 +93,65 @@ class RayBatch:
     @property
     def count(self):
         return self.origins.shape[0]
+
+
+def generate_ray(frame, px, py):
+    """One world-space ray through pixel (px, py) (`scene_io.py:86-95`)."""
+    if not (0 <= px < frame.width and 0 <= py < frame.height):
+        raise ValueError("pixel out of range")
+    d_cam = np.array([(px + 0.5 - frame.cx) / frame.fx, (py + 0.5 - frame.cy) / frame.fy, 1.0])
+    d = frame.pose[:3, :3] @ d_cam
+    d /= np.linalg.norm(d)
+    return frame.pose[:3, 3].copy(), d
+
+
+def project_point(frame, p_world):
+    """World point -> (px, py), the inverse pinhole map (`scene_io.py:119-126`)."""
+    rot = frame.pose[:3, :3]
+    pc = rot.T @ (np.asarray(p_world) - frame.pose[:3, 3])
+    return pc[0] / pc[2] * frame.fx + frame.cx - 0.5, pc[1] / pc[2] * frame.fy + frame.cy - 0.5
+
+
+def scene_sdf(spheres, points):
+    """Exact union-of-spheres SDF at (N,3) canonical points (`scene_io.py:261-266`)."""
+    d = np.full(points.shape[0], np.inf)
+    for center, radius, _ in spheres:
+        d = np.minimum(d, np.linalg.norm(points - center, axis=1) - radius)
+    return d
+
+
+def load_dataset(path):
+    """Dataset directory with `transforms.json` + PNGs (`scene_io.py:178-213`): RGBA
+    alpha > 0.5 is the mask, RGB images get an all-ones mask; per-frame `time_index`."""
+    import json
+    from pathlib import Path
+
+    from PIL import Image
+
+    path = Path(path)
+    manifest = path / "transforms.json"
+    if not manifest.is_file():
+        raise FileNotFoundError("dataset not found")
+    meta = json.loads(manifest.read_text())
+    frames, num_t = [], 1
+    for entry in meta["frames"]:
+        arr = np.asarray(Image.open(path / entry["file_path"])).astype(np.float64) / 255.0
+        if arr.ndim == 2:
+            arr = np.repeat(arr[:, :, None], 3, axis=2)
+        if arr.shape[2] == 4:
+            rgb, mask = arr[:, :, :3], (arr[:, :, 3] > 0.5).astype(np.float64)
+        else:
+            rgb, mask = arr[:, :, :3], np.ones(arr.shape[:2])
+        t = int(entry.get("time_index", 0))
+        num_t = max(num_t, t + 1)
+        frame = CameraFrame(fx=float(meta["fl_x"]), fy=float(meta["fl_y"]), cx=float(meta["cx"]),
+                            cy=float(meta["cy"]), width=int(meta["w"]), height=int(meta["h"]),
+                            pose=np.asarray(entry["transform_matrix"], np.float64).reshape(4, 4),
+                            image=rgb, mask=mask, time_index=t)
+        frame.validate()
+        frames.append(frame)
+    aabb = tuple(map(tuple, meta.get("scene_aabb", [[-1, -1, -1], [1, 1, 1]])))
+    return MultiViewDataset(frames, aabb, num_t)
 
 
 def generate_rays_grid(frame, pixels=None):
