@@ -21,7 +21,8 @@ from . import _lib
 from ._lib import ShapeError
 
 __all__ = ["ShapeError", "MlpWeights", "ForwardTrace", "forward", "input_jacobian_rows",
-           "backward_first", "backward_second", "backward_second_row", "input_jacobian"]
+           "backward_first", "backward_second", "backward_second_row", "input_jacobian",
+           "second_order_input_residual"]
 
 
 class MlpWeights:
@@ -180,3 +181,24 @@ def backward_second(weights, trace, jac_cotangent):
         fwd[l] = trace.masks[l - 1][:, :, None] * (weights.layers[l - 1] @ fwd[l - 1])
     return [torch.tensordot(back[l].transpose(1, 2) @ m, fwd[l], dims=([0, 2], [0, 2]))
             for l in range(depth)]
+
+
+def second_order_input_residual(weights, x, rng, h=1e-3, margin=1e-3, num_directions=8):
+    """Largest |f(x+hd) + f(x-hd) - 2f(x)| / h^2 over random unit directions
+    (`relu_mlp.py:219-250`): zero for a ReLU net unless a mask flips, which the margin
+    precondition on every pre-activation rules out ("near activation boundary")."""
+    x = np.asarray(x, np.float32)
+    worst = 0.0
+    for _ in range(num_directions):
+        d = rng.standard_normal(x.shape[0])
+        d = (d / np.linalg.norm(d)).astype(np.float32)
+        pts = np.stack([x, x + h * d, x - h * d])
+        a = _to_device(pts)
+        for hl in weights.layers[:-1]:
+            z = a @ hl.T
+            if float(z.abs().min()) <= margin:
+                raise ValueError("near activation boundary")
+            a = torch.clamp(z, min=0)
+        y, _ = forward(weights, pts)
+        worst = max(worst, float((y[1] + y[2] - 2.0 * y[0]).abs().max()) / h**2)
+    return worst

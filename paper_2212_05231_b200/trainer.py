@@ -401,6 +401,27 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0, schedule=True):
               cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
 
 
+def adam_update(state, param, grad, lr, config, name="param", m=None, v=None):
+    """One bias-corrected Adam step in place on a contiguous CUDA tensor
+    (`trainer.py:152-172`) through `ns2b_adam_step_f32/_f64`; `m`/`v` default to the
+    AdamState's buffers (callers updating a leading slice, e.g. the active table levels,
+    pass matching views).  Raises FloatingPointError("divergence: ...") on a non-finite
+    gradient before touching anything."""
+    g = as_device(grad, param.dtype).reshape(-1).contiguous()
+    if not bool(torch.isfinite(g).all()):
+        raise FloatingPointError(f"divergence: non-finite gradient for {name}")
+    m = state.m if m is None else m
+    v = state.v if v is None else v
+    for t in (param, m, v):
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("adam_update: param and moments must be contiguous CUDA tensors")
+    state.t += 1
+    fn = "ns2b_adam_step_f64" if param.dtype == torch.float64 else "ns2b_adam_step_f32"
+    _lib.call(fn, _lib.ptr(param), _lib.ptr(g), _lib.ptr(m), _lib.ptr(v), param.numel(), int(state.t),
+              float(lr), float(config.adam_beta1), float(config.adam_beta2), float(config.adam_eps),
+              _lib.stream_ptr())
+
+
 def compute_cotangents(state, batch, rendered, records):
     """Module-API loss + cotangents (`trainer.py:215-240`) for a rendered batch, on the
     device (train_step fuses the same arithmetic into ns2b_composite and the MLP

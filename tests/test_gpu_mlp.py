@@ -175,3 +175,26 @@ def test_eval_color_and_sigmoid():
     cache = pfield.eval_field(pp, x, v1, 8)
     cols = pfield.eval_color(pp, cache, v2)
     assert_close(_np(cols), ofield.eval_field(op, x, v2, 8).colors, TOL, "colors")
+
+
+def test_second_order_input_residual():
+    """`relu_mlp.second_order_input_residual` (`relu_mlp.py:219-250`): a ReLU net is
+    piecewise linear, so away from mask boundaries the residual is fp32 rounding only;
+    a point on a boundary raises."""
+    rng = np.random.default_rng(0)
+    w = pmlp.MlpWeights([0.25 * rng.standard_normal((16, 5)).astype(np.float32),
+                         0.25 * rng.standard_normal((3, 16)).astype(np.float32)])
+    for _ in range(20):
+        x = rng.standard_normal(5).astype(np.float32)
+        try:
+            # margin 0.05 > h |row of H1| excludes a flip between x and x +- h d
+            r = pmlp.second_order_input_residual(w, x, np.random.default_rng(1), h=1e-2, margin=0.05)
+        except ValueError:
+            continue
+        assert r < 5e-2  # fp32 cancellation / h^2
+        break
+    else:
+        pytest.fail("no point away from the activation boundaries")
+    x = np.zeros(5, np.float32)  # every pre-activation is exactly 0
+    with pytest.raises(ValueError, match="near activation boundary"):
+        pmlp.second_order_input_residual(w, x, np.random.default_rng(1))

@@ -488,3 +488,24 @@ def test_compute_cotangents_module_api(sphere64):
     assert_close(np_(p[4]), o[4], TOL, "dl_dsdf")
     assert abs(p[5] - o[5]) <= TOL * max(abs(o[5]), 1e-12)
     assert_close(np_(p[6]), o[6], TOL, "dl_dn")
+
+
+def test_adam_update_module_api():
+    """`trainer.adam_update` (`trainer.py:152-172`) on a device tensor vs the oracle, three
+    steps on a leading slice with moment views; then the divergence error."""
+    ost = _c1_state()
+    pst = product_state_from_oracle(ost)
+    rng = np.random.default_rng(5)
+    oad, pad = ost.adam["tables"], pst.adam["tables"]
+    for _ in range(3):
+        g = rng.standard_normal(ost.params.grid.tables[:3].shape).astype(np.float32) * 1e-3
+        otrain.adam_update(oad, ost.params.grid.tables[:3], g, 1e-2, ost.config, "tables",
+                           oad.m[:3], oad.v[:3])
+        ptrain.adam_update(pad, pst.params.grid.tables[:3], g, 1e-2, pst.config, "tables",
+                           pad.m[:3], pad.v[:3])
+    assert pad.t == oad.t == 3
+    assert_close(np_(pst.params.grid.tables), ost.params.grid.tables, 1e-6, "tables")
+    g[0, 0, 0] = np.inf
+    with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for tables"):
+        ptrain.adam_update(pad, pst.params.grid.tables[:3], g, 1e-2, pst.config, "tables",
+                           pad.m[:3], pad.v[:3])
