@@ -198,3 +198,22 @@ def test_second_order_input_residual():
     x = np.zeros(5, np.float32)  # every pre-activation is exactly 0
     with pytest.raises(ValueError, match="near activation boundary"):
         pmlp.second_order_input_residual(w, x, np.random.default_rng(1))
+
+
+def test_theorem1_bench_rows():
+    """`autodiff_oracle.bench_second_order` (`autodiff_oracle.py:208-270`): the analytic
+    second-order backward agrees with generic double autodiff and the CSV has the
+    reference's columns."""
+    from paper_2212_05231_b200 import autodiff_oracle as ad
+
+    rows = ad.bench_second_order(16, 3, [8, 64], runs=3)
+    assert [r["batch"] for r in rows] == [8, 64] and all(r["speedup"] > 0 for r in rows)
+    csv = ad.bench_rows_to_csv(rows).splitlines()
+    assert csv[0] == "width,depth,batch,analytic_us,oracle_us,speedup" and len(csv) == 3
+    # the graph side itself against the golden vectors (generic M)
+    gold = dict(np.load(GOLD / "mlp.npz", allow_pickle=False))
+    w = pmlp.MlpWeights([gold[f"d3_w{i}"] for i in range(3)])
+    x = torch.from_numpy(gold["d3_x"].astype(np.float32)).cuda()
+    m = torch.from_numpy(gold["d3_m"].astype(np.float32)).cuda()
+    for i, g in enumerate(ad.graph_grad_of_grad(w, x, m)):
+        assert_close(_np(g), gold[f"d3_g2_{i}"], TOL, f"graph g2_{i}")
