@@ -70,57 +70,7 @@ def make_dataset(wl, device=None):
     preset, views, w, h, focal = wl["scene"]
     if device is None or w * h <= 64 * 64:
         return scene_io.make_synthetic(preset, views=views, seed=0, width=w, height=h, focal=focal)
-    return _make_dataset_gpu(preset, views, w, h, focal, device)
-
-
-def _make_dataset_gpu(preset, views, w, h, focal, device):
-    import torch
-
-    from paper_2212_05231_b200 import scene_io
-
-    spheres, motion = scene_io.preset_scene(preset)
-    rng = np.random.default_rng(0)
-    elev = np.deg2rad(np.where(np.arange(views) % 2 == 0, 18.0, -12.0))
-    azim = 2 * np.pi * np.arange(views) / views + rng.uniform(0, 2 * np.pi / views)
-    light = torch.tensor(scene_io.LIGHT, dtype=torch.float64, device=device)
-    ys, xs = torch.meshgrid(torch.arange(h, device=device, dtype=torch.float64),
-                            torch.arange(w, device=device, dtype=torch.float64), indexing="ij")
-    frames = []
-    for v in range(views):
-        pose = scene_io.orbit_pose(azim[v], elev[v], 2.6)
-        R = torch.tensor(pose[:3, :3], device=device)
-        eye = torch.tensor(pose[:3, 3], device=device)
-        dc = torch.stack([(xs.reshape(-1) + 0.5 - w / 2.0) / focal,
-                          (ys.reshape(-1) + 0.5 - h / 2.0) / focal,
-                          torch.ones(h * w, device=device, dtype=torch.float64)], 1)
-        d = dc @ R.T
-        d = d / torch.linalg.norm(d, dim=1, keepdim=True)
-        best = torch.full((h * w,), float("inf"), device=device, dtype=torch.float64)
-        which = torch.full((h * w,), -1, device=device, dtype=torch.int64)
-        for si, (c, r, _) in enumerate(spheres):
-            oc = eye - torch.tensor(c, device=device)
-            b = d @ oc
-            disc = b * b - (oc @ oc - r * r)
-            t = torch.where(disc >= 0, -b - torch.sqrt(torch.clamp(disc, min=0.0)),
-                            torch.full_like(b, float("inf")))
-            t = torch.where(t > 1e-6, t, torch.full_like(t, float("inf")))
-            closer = t < best
-            best = torch.where(closer, t, best)
-            which = torch.where(closer, torch.full_like(which, si), which)
-        hit = torch.isfinite(best)
-        col = torch.zeros((h * w, 3), device=device, dtype=torch.float64)
-        for si, (c, r, albedo) in enumerate(spheres):
-            sel = hit & (which == si)
-            p = eye + best[sel, None] * d[sel]
-            nrm = (p - torch.tensor(c, device=device)) / r
-            lam = torch.clamp(nrm @ light, min=0.0)
-            col[sel] = torch.tensor(albedo, device=device) * (0.3 + 0.7 * lam)[:, None]
-        rgb8 = (col.clamp(0, 1) * 255).round().to(torch.uint8).reshape(h, w, 3).cpu().numpy()
-        fr = scene_io.CameraFrame(focal, focal, w / 2.0, h / 2.0, w, h, pose,
-                                  rgb8.astype(np.float64) / 255.0,
-                                  hit.reshape(h, w).to(torch.float64).cpu().numpy(), 0)
-        frames.append(fr)
-    return scene_io.MultiViewDataset(frames)
+    return scene_io.make_synthetic_device(preset, views, w, h, focal, device)
 
 
 class ClockSampler:
@@ -255,8 +205,13 @@ def time_samplers(ds, count, dev):
     return {"rays": count, "host_ms": host, "device_ms": (time.perf_counter() - t0) * 1e3 / 5}
 
 
-def l2_probes(dev, nbytes=64 << 20):
-    """Measured L2 read and random-RED bandwidth (GB/s) over a working-set-sized buffer."""
+def l2_probes(dev, nbytes=64 << 20, table_rows=11 * (1 << 19)):
+    """In-run L2 ceilings (GB/s of useful bytes) for the hash gather / scatter:
+    * l2_read_gbs: 16-B ld.global.cg sweep over a 64 MiB buffer (L2-resident);
+    * gather_gbs: random 8-B row loads over the addressable table size (11 hashed
+      levels x 2^19 rows x 8 B = 44 MiB), 8 in flight per thread: the gather's pattern;
+    * red_coalesced_gbs: float2 REDs with full sectors (lane k -> row base + k): the L2
+      atomic units' ceiling; red_random_gbs: random float2 REDs (the old probe)."""
     import torch
 
     from paper_2212_05231_b200 import _lib
@@ -264,24 +219,28 @@ def l2_probes(dev, nbytes=64 << 20):
     buf = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
     sink = torch.zeros(1, dtype=torch.float32, device=dev)
     st = _lib.stream_ptr()
-    iters = 20
-    for _ in range(2):
-        _lib.call("ns2b_bench_l2_read", _lib.ptr(buf), buf.numel(), 2, _lib.ptr(sink), st)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    _lib.call("ns2b_bench_l2_read", _lib.ptr(buf), buf.numel(), iters, _lib.ptr(sink), st)
-    e1.record()
-    torch.cuda.synchronize()
-    read_gbs = nbytes * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+    def timed(fn, *a):
+        fn(*a)  # warm (L2 residency)
+        e0.record()
+        fn(*a)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3
+
+    iters = 20
+    sec = timed(lambda: _lib.call("ns2b_bench_l2_read", _lib.ptr(buf), buf.numel(), iters, _lib.ptr(sink), st))
+    out = {"l2_read_gbs": nbytes * iters / sec / 1e9, "buffer_mib": nbytes >> 20}
+    nload = 1 << 28
+    sec = timed(lambda: _lib.call("ns2b_bench_gather", _lib.ptr(buf), table_rows, nload, 3, _lib.ptr(sink), st))
+    out["gather_gbs"] = nload * 8 / sec / 1e9
     nops = 1 << 27
-    _lib.call("ns2b_bench_red", _lib.ptr(buf), buf.numel() // 2, 1 << 20, 1, st)
-    e0.record()
-    _lib.call("ns2b_bench_red", _lib.ptr(buf), buf.numel() // 2, nops, 7, st)
-    e1.record()
-    torch.cuda.synchronize()
-    red_s = e0.elapsed_time(e1) * 1e-3
-    return {"l2_read_gbs": read_gbs, "red_f32x2_gops": nops / red_s / 1e9,
-            "red_f32x2_gbs": nops * 8 / red_s / 1e9, "buffer_mib": nbytes >> 20}
+    sec = timed(lambda: _lib.call("ns2b_bench_red_coalesced", _lib.ptr(buf), table_rows, nops, 5, st))
+    out["red_coalesced_gbs"] = nops * 8 / sec / 1e9
+    sec = timed(lambda: _lib.call("ns2b_bench_red", _lib.ptr(buf), table_rows, nops, 7, st))
+    out["red_random_gbs"] = nops * 8 / sec / 1e9
+    return out
 
 
 def run_ours(args, wl):
@@ -317,9 +276,14 @@ def run_ours(args, wl):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(host):
+    def step(i, mode):
+        if mode == "sampler":  # public API incl. sampling: picks H2D, shard rays on the device
+            return trainer.train_step(st, ds)
+        return trainer.train_step(st, ds, batch=batch(i, mode == "host"))
+
+    def timed(mode):
         for i in range(args.warmup):
-            trainer.train_step(st, ds, batch=batch(i, host))
+            step(i, mode)
         barrier()
         n0 = _lib.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -327,7 +291,7 @@ def run_ours(args, wl):
         e0.record()
         reps = []
         for i in range(args.warmup, nb):
-            reps.append(trainer.train_step(st, ds, batch=batch(i, host)))
+            reps.append(step(i, mode))
         e1.record()
         barrier()
         wall = time.perf_counter() - t0
@@ -340,23 +304,29 @@ def run_ours(args, wl):
     clocks = ClockSampler(torch.cuda.current_device())
     st.timers = {}
     clocks.start()
-    ms_dev, launches, reps, wall = timed(host=False)
+    ms_dev, launches, reps, wall = timed("dev")
     clk = clocks.stop()
     timers = st.timers
     st.timers = None
     per_kernel = {k: statistics.mean(a.elapsed_time(b) for a, b in v[-args.steps:])
                   for k, v in timers.items()}
-    # end-to-end leg through the public API with host batches
+    # end-to-end legs through the public API: (1) train_step(state, dataset) with the
+    # dataset in HBM -- the reference's sampling draws on the host, this step's picks
+    # (8 B/ray) copied H2D, rays built on the device; (2) pinned host ray batches (72 B/ray
+    # of origins, directions, targets) copied H2D every step
+    ds.to_device(0, dev)
+    st.rng = np.random.default_rng(11)
+    ms_e2e, _, _, wall_e2e = timed("sampler")
+    ms_e2e_rays, _, _, _ = timed("host")
     if os.environ.get("NS2B_BENCH_DEBUG"):
         st.timers = {}
         clk2 = ClockSampler(torch.cuda.current_device())
         clk2.path = clk2.path.with_suffix(".e2e.csv")
         clk2.start()
-    ms_e2e, _, _, wall_e2e = timed(host=True)
     if os.environ.get("NS2B_BENCH_DEBUG"):
         print(json.dumps({"clocks_dev": clk, "clocks_e2e": clk2.stop()}), file=sys.stderr)
         st.timers = {}
-        ms_dev2, _, reps2, _ = timed(host=False)
+        ms_dev2, _, reps2, _ = timed("dev")
         print(json.dumps({"P_dev": [r.sample_count for r in reps], "loss_dev": [r.total for r in reps],
                           "P_again": [r.sample_count for r in reps2],
                           "loss_again": [r.total for r in reps2]}), file=sys.stderr)
@@ -373,49 +343,54 @@ def run_ours(args, wl):
     P_mean = statistics.mean(r.sample_count for r in reps)
     value = m_global * args.steps / (ms_dev * 1e-3)
     e2e = m_global * args.steps / (ms_e2e * 1e-3)
+    e2e_rays = m_global * args.steps / (ms_e2e_rays * 1e-3)
     if rank != 0:
         return
     sampler = time_samplers(ds, m_global, dev)
+    occ_copy = renderer.OccupancyGrid(st.occ.resolution, (tuple(st.occ.lo), tuple(st.occ.hi)), st.occ.threshold)
+    renderer.update_occupancy(occ_copy, st.params, wl["levels"])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    renderer.update_occupancy(occ_copy, st.params, wl["levels"])
+    e1.record()
+    torch.cuda.synchronize()
+    occ_ms = e0.elapsed_time(e1)
     peaks = load_peaks()
     l2 = l2_probes(dev)
     Pl = P_mean / world  # per-rank samples per launch
     L = wl["levels"]
-    # Algorithmic work per sample:
-    #   gather:  8 corners x 2 fp32 features x L table reads + 12 B position + 28 B ray id
-    #            and fp64 view dir + 600 B written (pre-staged encoding tile 192 B,
-    #            d feature/dx 384 B, fp32 position + view dir 24 B)
-    #   scatter: 8 corners x L float2 REDs (8 B each) + 32 B of inputs
+    # Algorithmic work per sample, no staging bytes:
+    #   gather:  table reads 8 corners x 2 fp32 features x L levels = 64 L B (1024 at L=16),
+    #            against the in-run L2 read probe (tables are L2-resident)
+    #   scatter: 8 corners x L float2 REDs = 64 L B, against the coalesced-RED probe
     #   MLP fwd: 11,520 MAC (SDF 36x64, 64x16, j_d 64x36; colour 25x64, 64x64, 64x3)
     #   MLP bwd: 23,104 MAC (input cotangents 5,888 colour + 3,328 SDF, weight gradients
-    #            5,888 + 3,328, Theorem-1 pvec + dH1 second term + dH2[0] 4,672) -- the
-    #            forward is not recomputed (its staged tiles are read back); algorithmic
-    #            dims, not the 3x split.  fwd + bwd = 34,624 MAC = SURVEY 8(d)'s ~34.9k.
+    #            5,888 + 3,328, Theorem-1 pvec + dH1 second term + dH2[0] 4,672);
+    #            algorithmic dims, not the 3x fp16 split.  fwd + bwd = 34,624 MAC.
+    #   composite: ~100 B/sample of HBM (fp64 alpha / weight / T, sdf, colour, cotangents)
     work = {
-        "field_gather": ("hbm", Pl * (8 * 2 * 4 * L + 12 + 28 + 600), "GB/s"),
-        "field_scatter": ("hbm", Pl * (8 * 8 * L + 32), "GB/s"),
-        "field_mlp_forward": ("tensor", Pl * 2 * 11520, "TFLOP/s"),
-        "field_mlp_backward": ("tensor", Pl * 2 * 23104, "TFLOP/s"),
-        "composite": ("hbm", Pl * 100, "GB/s"),
+        "field_gather": ("l2", Pl * 64 * L, "GB/s", l2["l2_read_gbs"], "in-run l2_read_gbs"),
+        "field_scatter": ("l2", Pl * 64 * L, "GB/s", l2["red_coalesced_gbs"], "in-run red_coalesced_gbs"),
+        "field_mlp_forward": ("tensor", Pl * 2 * 11520, "TFLOP/s", peaks["bf16_tflops_sustained"],
+                              "MEASURED_PEAKS bf16_tflops_sustained"),
+        "field_mlp_backward": ("tensor", Pl * 2 * 23104, "TFLOP/s", peaks["bf16_tflops_sustained"],
+                               "MEASURED_PEAKS bf16_tflops_sustained"),
+        "composite": ("hbm", Pl * 100, "GB/s", peaks["hbm_gbs"], "MEASURED_PEAKS hbm_gbs"),
     }
     kern = {}
-    for k, (bound, amount, unit) in work.items():
+    for k, (bound, amount, unit, peak, src) in work.items():
         if k not in per_kernel:
             continue
         sec = per_kernel[k] * 1e-3
-        if unit == "GB/s":
-            ach, peak = amount / sec / 1e9, peaks["hbm_gbs"]
-        else:
-            ach, peak = amount / sec / 1e12, peaks["bf16_tflops_sustained"]
-        kern[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                   "ms": per_kernel[k], "per_sample": amount / Pl}
-    kern["field_gather"]["l2_frac"] = kern["field_gather"]["achieved"] / l2["l2_read_gbs"]
-    red_ops = Pl * 8 * L
-    kern["field_scatter"]["red_gops"] = red_ops / (per_kernel["field_scatter"] * 1e-3) / 1e9
-    kern["field_scatter"]["red_frac_of_probe"] = kern["field_scatter"]["red_gops"] / l2["red_f32x2_gops"]
+        ach = amount / sec / (1e9 if unit == "GB/s" else 1e12)
+        kern[k] = {"bound": bound, "achieved": ach, "peak": peak, "peak_source": src, "unit": unit,
+                   "frac": ach / peak, "ms": per_kernel[k], "per_sample": amount / Pl}
+    kern["field_gather"]["frac_of_random_gather_probe"] = kern["field_gather"]["achieved"] / l2["gather_gbs"]
     # DRAM traffic per launch from the committed ncu capture (bench.py cannot run ncu
     # itself): bytes moved and the DRAM bandwidth that implies at this run's kernel time
     traffic = {}
-    tp = ROOT / "profiles" / "r01_dram_traffic.json"
+    tps = sorted((ROOT / "profiles").glob("r*_dram_traffic.json"))
+    tp = tps[-1] if tps else ROOT / "profiles" / "none"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("kernels", {})
     for k, v in kern.items():
@@ -426,14 +401,14 @@ def run_ours(args, wl):
     d = kern[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": d["unit"], "frac": d["frac"],
-                "peak_source": "MEASURED_PEAKS.json (" + peaks["source"] + "): "
-                               + ("hbm_gbs" if d["unit"] == "GB/s" else "bf16_tflops_sustained"),
+                "peak_source": d["peak_source"] + " (" + peaks["source"] + ")",
                 "traffic": d.get("dram_traffic_bytes"),
-                "traffic_source": "profiles/r01_dram_traffic.json (ncu dram__bytes_read.sum + "
+                "traffic_source": f"profiles/{tp.name} (ncu dram__bytes_read.sum + "
                                   "dram__bytes_write.sum, one launch)" if "dram_traffic_bytes" in d else None,
                 "algorithmic_per_sample": d["per_sample"],
                 "step_share": d["ms"] / (ms_dev / args.steps), "kernels": kern,
-                "per_kernel_ms": per_kernel, "l2_probe": l2, "sampler": sampler}
+                "per_kernel_ms": per_kernel, "l2_probe": l2, "sampler": sampler,
+                "occupancy_refresh_ms": occ_ms}
     # CPU baseline on a bounded sample (the oracle, all host cores)
     wl["_dataset"] = ds
     cpu = None
@@ -452,9 +427,21 @@ def run_ours(args, wl):
         "config": {"workload": wl["workload"], "global_batch": m_global, "rays_per_gpu": wl["rays"],
                    "levels": L, "table_size": wl["table"], "parallelism": f"dp{world}",
                    "samples_per_step": P_mean, "lambda": L, "occupancy": "frozen after step-0 refresh",
-                   "l2": "working set > L2 (per-sample buffers ~GBs per step), no flush needed"},
-        "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": m_global // world * 72,
-                "d2h_bytes_per_step": 4 + 64, "ms_per_step": ms_e2e / args.steps},
+                   "l2": "working set > L2 (per-sample buffers ~GBs per step), no flush needed",
+                   "timed_region": "value: march, field gather/forward, composite+loss, field "
+                                   "backward+scatter, all-reduce, Adam per step with the ray batch "
+                                   "already in HBM (sampled before the timed region); e2e adds the "
+                                   "sampling.  The occupancy refresh (every 16 steps in the "
+                                   "reference; its cost is roofline.occupancy_refresh_ms) is outside "
+                                   "both: occupancy is frozen after the step-0 refresh so every step "
+                                   "is the same workload"},
+        "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": 8 * (m_global // world),
+                "d2h_bytes_per_step": 4 + 64, "ms_per_step": ms_e2e / args.steps,
+                "path": "trainer.train_step(state, dataset) with dataset.to_device(): host rng draws "
+                        "(the reference's), this rank's picks H2D (int64), rays + targets built on "
+                        "the device; P (int32) and the 8-double step report D2H",
+                "pinned_host_rays": {"value": e2e_rays, "ms_per_step": ms_e2e_rays / args.steps,
+                                     "h2d_bytes_per_step": 72 * (m_global // world)}},
         "gpu_launches": launches,
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -281,6 +281,14 @@ NS2B_API int ns2b_bench_l2_read(const float *buf, int64_t nfloats, int32_t iters
                                 void *stream);
 /* nops random float2 REDs over nrows 8-B rows of buf (the scatter's access pattern). */
 NS2B_API int ns2b_bench_red(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void *stream);
+/* nloads random 8-B row loads (ld.global.nc) over nrows rows of buf, 8 in flight per
+ * thread: the hash gather's access pattern (useful bytes = 8 per load). */
+NS2B_API int ns2b_bench_gather(const float *buf, int64_t nrows, int64_t nloads, uint32_t seed,
+                               float *sink, void *stream);
+/* nops float2 REDs, lane k of each warp on row base + k (full sectors): the L2 atomic
+ * units' ceiling for the scatter. */
+NS2B_API int ns2b_bench_red_coalesced(float *buf, int64_t nrows, int64_t nops, uint32_t seed,
+                                      void *stream);
 
 /* tcgen05 issue-rate probe (profiling aid, one CTA): `iters` kind::f16 MMAs of one of the
  * MLP kernels' shapes (0: M128 N64 K/MN, 1: M64 N16 MN/MN, 2: M64 N64 MN/MN, 3: M128

@@ -87,6 +87,8 @@ _SIGS = {
                                             P]),
     "ns2b_bench_l2_read": (ctypes.c_int, [P, I64, I32, P, P]),
     "ns2b_bench_red": (ctypes.c_int, [P, I64, I64, ctypes.c_uint32, P]),
+    "ns2b_bench_gather": (ctypes.c_int, [P, I64, I64, ctypes.c_uint32, P, P]),
+    "ns2b_bench_red_coalesced": (ctypes.c_int, [P, I64, I64, ctypes.c_uint32, P]),
     "ns2b_bench_umma": (ctypes.c_int, [I32, I32, I32, P, P]),
     "ns2b_rays_from_picks": (ctypes.c_int, [P, I64, I64, P, P, P, I32, I32, P, P, P, P, P, P]),
     "ns2b_selftest_umma": (ctypes.c_int, [P, P, P, I32, P]),

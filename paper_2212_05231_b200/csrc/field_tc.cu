@@ -42,6 +42,9 @@ namespace tc {
 
 constexpr int TILE = 128;
 constexpr int kHead = 14;  // staged maxima land in [2^13, 2^14)
+#ifndef NS2B_PRED_SLACK
+#define NS2B_PRED_SLACK 10  // accepted predicted exponents: staged max in [2^(13-slack), 2^15)
+#endif
 
 // shared memory map (bytes); every tile is hi part then lo part
 constexpr uint32_t WH1 = 0;                          // 64 x 48
@@ -351,7 +354,7 @@ struct PredScale {
     __device__ __forceinline__ bool check(int k, int &e) {
         const float m = __uint_as_float(mx[par][k]);
         const int ex = exp_for(m);
-        const bool ok = !(m > 0.f) || (e <= ex + 1 && e >= ex - 10);
+        const bool ok = !(m > 0.f) || (e <= ex + 1 && e >= ex - NS2B_PRED_SLACK);
         if (!ok) {
             e = ex - 1;
             if (threadIdx.x == 0) pred[k] = e;
@@ -1720,6 +1723,9 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
             cell_frac(un1, lv.n, cy, fy);
             cell_frac(un2, lv.n, cz, fz);
             float *gt = g_tab + l * f.T * 2;
+            // the 16-B x-pair RED needs a 16-B aligned level base: with an odd table size
+            // every other level starts 8-B aligned, so those levels take two float2 REDs
+            const bool pair16 = (reinterpret_cast<uintptr_t>(gt) & 15u) == 0;
             // runs of equal cells along the warp's samples (consecutive samples of a ray):
             // on the coarse levels all 8 corners of a run are pre-summed by one segmented
             // scan and only the run's last lane issues the REDs
@@ -1769,7 +1775,7 @@ field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *_
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // x-pairs (c, c + 4): one 16-B RED when adjacent
-                if ((row[c] ^ row[c + 4]) == 1u) {
+                if (pair16 && (row[c] ^ row[c + 4]) == 1u) {
                     const bool sw = row[c] & 1u;
                     red_add_f32x4(gt + 2 * (row[c] & ~1u), sw ? a[c + 4] : a[c], sw ? b[c + 4] : b[c],
                                   sw ? a[c] : a[c + 4], sw ? b[c] : b[c + 4]);

@@ -37,6 +37,33 @@ __global__ void red_kernel(float *__restrict__ buf, uint32_t nrows, int64_t nops
     }
 }
 
+// Random 8-B gathers: the hash-grid gather's access pattern (one float2 row per lane,
+// rows uniformly random over a table-sized buffer, 8 independent loads in flight per
+// thread like one level's 8 corners).  Useful bytes = 8 per load.
+__global__ void gather_kernel(const float2 *__restrict__ buf, uint32_t nrows, int64_t nloads, uint32_t seed,
+                              float *__restrict__ sink) {
+    float acc = 0.f;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i < nloads; i += stride) {
+        float2 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = __ldg(buf + hash32(static_cast<uint32_t>(i + c) ^ seed) % nrows);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc += v[c].x + v[c].y;
+    }
+    if (acc == 123456.f) sink[0] = acc;
+}
+
+// Coalesced float2 REDs (lane k of a warp adds to row base + k): the L2 atomic units'
+// throughput with full sectors, the ceiling for the table scatter's REDs.
+__global__ void red_coalesced_kernel(float *__restrict__ buf, uint32_t nrows, int64_t nops, uint32_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nops;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t warp_base = (hash32(static_cast<uint32_t>(i >> 5) ^ seed) % (nrows / 32)) * 32;
+        red_add_f32x2(buf + 2 * static_cast<int64_t>(warp_base + (i & 31)), 1e-9f, 1e-9f);
+    }
+}
+
 }  // namespace ns2b
 
 using namespace ns2b;
@@ -55,6 +82,19 @@ int ns2b_bench_red(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void 
     red_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(buf, static_cast<uint32_t>(nrows), nops,
                                                            seed);
     return check_launch("bench_red");
+}
+
+int ns2b_bench_gather(const float *buf, int64_t nrows, int64_t nloads, uint32_t seed, float *sink, void *stream) {
+    NS2B_REQUIRE(nrows >= 1 && nrows < (1ll << 32), "bench_gather: row count");
+    gather_kernel<<<kNumSMs * 16, 128, 0, as_stream(stream)>>>(reinterpret_cast<const float2 *>(buf),
+                                                               static_cast<uint32_t>(nrows), nloads, seed, sink);
+    return check_launch("bench_gather");
+}
+
+int ns2b_bench_red_coalesced(float *buf, int64_t nrows, int64_t nops, uint32_t seed, void *stream) {
+    NS2B_REQUIRE(nrows >= 32 && nrows < (1ll << 32), "bench_red_coalesced: row count");
+    red_coalesced_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(buf, static_cast<uint32_t>(nrows), nops, seed);
+    return check_launch("bench_red_coalesced");
 }
 
 }  // extern "C"

@@ -294,9 +294,10 @@ def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform, field_lr_sca
         if joint:
             ws.flag.zero_()
             ws.sums[1].fill_(dslog / params.sharpness)
-            trainer._apply_gradients(st, na, params.sharpness, field_lr_scale)
-            if int(ws.flag.item()) != 0:
-                raise FloatingPointError("divergence: non-finite gradient")
+            stepped = trainer._apply_gradients(st, na, params.sharpness, field_lr_scale)
+            bits = int(ws.flag.item())
+            if bits != 0:
+                trainer._raise_divergence(st, bits, stepped)
             params.refresh_host_mirror()
     st.step += 1
     return rep

@@ -251,14 +251,16 @@ class _Timer:
         return False
 
 
-def _upload_batch(ws, batch, lo, hi, stream):
-    """Copy rays [lo, hi) of the batch into the workspace (pinned, async)."""
+def _upload_batch(ws, batch, sl, stream):
+    """Copy the rays `sl` (this rank's shard) of the batch into the workspace."""
     for dst, src in ((ws.o, batch.origins), (ws.d, batch.directions), (ws.tgt, batch.target_colors)):
         if isinstance(src, torch.Tensor):
-            s = src[lo:hi]
+            s = src[sl]
+            if s.device.type == "cpu" and not s.is_contiguous():
+                s = s.contiguous().pin_memory()
             dst.copy_(s, non_blocking=True)
         else:
-            h = torch.from_numpy(np.ascontiguousarray(src[lo:hi], np.float64))
+            h = torch.from_numpy(np.ascontiguousarray(src[sl], np.float64))
             dst.copy_(h.pin_memory(), non_blocking=True)
 
 
@@ -274,14 +276,21 @@ def train_step(state, dataset, time_index=0, batch=None):
     level = level_schedule(state.step, cfg)
     if state.step % cfg.occupancy_update_every == 0:
         renderer.update_occupancy(occ, params, level)
-    if batch is None:
-        batch = scene_io.sample_ray_batch(dataset, time_index, cfg.batch_size, cfg.fg_fraction,
-                                          state.rng)
-    m_total = batch.count
-    lo, hi = dp.shard(m_total)
-    m = hi - lo
-    ws.rays(m)
-    _upload_batch(ws, batch, lo, hi, st)
+    sampler = getattr(dataset, "_device_samplers", {}).get(time_index) if batch is None else None
+    if sampler is not None:
+        # f2 (`dataset.to_device()`): the reference's rng draws on the host, only this
+        # rank's picks go up and only its rays are built, straight into the workspace
+        m_total = cfg.batch_size
+        ws.rays(dp.shard_size(m_total))
+        sampler.sample_into(m_total, cfg.fg_fraction, state.rng, ws.o, ws.d, ws.tgt, dp.rank, dp.world)
+    else:
+        if batch is None:
+            batch = scene_io.sample_ray_batch(dataset, time_index, cfg.batch_size, cfg.fg_fraction,
+                                              state.rng)
+        m_total = batch.count
+        ws.rays(dp.shard_size(m_total))
+        _upload_batch(ws, batch, dp.shard(m_total), st)
+    m = ws.m
 
     timers = getattr(state, "timers", None)
     # K1: march (count, scan) -> P -> fill
@@ -320,6 +329,7 @@ def train_step(state, dataset, time_index=0, batch=None):
     lay = params.layout
     end = lay.active_end(na)
     ws.flag.zero_()
+    stepped = []
     if P_glob > 0:
         ws.grads[:end].zero_()
         ws.count64.fill_(P_glob)
@@ -338,7 +348,7 @@ def train_step(state, dataset, time_index=0, batch=None):
                 dp.allreduce_(ws.grads[:end])
                 dp.allreduce_(ws.sums[:4])
         with _Timer(timers, "adam", st):
-            _apply_gradients(state, na, s)
+            stepped = _apply_gradients(state, na, s)
     elif dp.active:
         dp.allreduce_(ws.sums[:4])
     # one D2H: [huber sum, dslog, sq err, eik sum, flag, slog]
@@ -349,9 +359,7 @@ def train_step(state, dataset, time_index=0, batch=None):
     st.synchronize()
     rep = ws.report_host.tolist()
     if rep[4] != 0:
-        bits = int(rep[4])
-        name = next(n for n in _CHECK_ORDER if bits & (1 << _CHECK_ORDER.index(n)))
-        raise FloatingPointError(f"divergence: non-finite gradient for {name}")
+        _raise_divergence(state, int(rep[4]), stepped)
     params.refresh_host_mirror(rep[5])
     c_loss = rep[0] / m_total
     e_loss = rep[3] / P_glob if P_glob > 0 else 0.0
@@ -361,6 +369,17 @@ def train_step(state, dataset, time_index=0, batch=None):
     state.last_dslog = rep[1] * s
     state.step += 1
     return report
+
+
+def _raise_divergence(state, bits, stepped):
+    """The device flag is set: no parameter or moment was written (the Adam kernels
+    check it first), so the step counters advanced by `_apply_gradients` are rolled
+    back before raising -- bias correction and checkpoints keep the reference's `t`
+    (`trainer.py:158-159` raises before its group's `t` moves)."""
+    for n in stepped:
+        state.adam[n].t -= 1
+    name = next(n for n in _CHECK_ORDER if bits & (1 << _CHECK_ORDER.index(n)))
+    raise FloatingPointError(f"divergence: non-finite gradient for {name}")
 
 
 def _apply_gradients(state, n_active, sharpness, lr_scale=1.0, schedule=True):
@@ -399,6 +418,7 @@ def _apply_gradients(state, n_active, sharpness, lr_scale=1.0, schedule=True):
               _lib.ptr(state.v_flat), _lib.i64_array(offs), _lib.i64_array(lens),
               _lib.f64_array(lrs), _lib.i64_array(ts), len(names), cfg.adam_beta1,
               cfg.adam_beta2, cfg.adam_eps, _lib.ptr(ws.flag), sp)
+    return names + ["sharpness_log"]
 
 
 def adam_update(state, param, grad, lr, config, name="param", m=None, v=None):
@@ -470,11 +490,10 @@ def apply_gradients(state, grads, dl_dslog, lr_scale=1.0, max_active_level=None)
             dst.copy_(as_device(src, torch.float32).reshape(dst.shape))
     ws.sums[1:2].fill_(float(dl_dslog))
     ws.flag.zero_()
-    _apply_gradients(state, na, 1.0, lr_scale, schedule=False)
+    stepped = _apply_gradients(state, na, 1.0, lr_scale, schedule=False)
     bits = int(ws.flag.item())
     if bits:
-        name = next(n for n in _CHECK_ORDER if bits & (1 << _CHECK_ORDER.index(n)))
-        raise FloatingPointError(f"divergence: non-finite gradient for {name}")
+        _raise_divergence(state, bits, stepped)
     params.refresh_host_mirror(float(params.sharpness_log.item()))
 
 

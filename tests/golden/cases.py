@@ -57,6 +57,21 @@ STEP_CASES = {
 }
 
 
+# TrainState.create cases (`trainer.py:192-212`): seeded init of the parameters in the
+# reference's draw order, for the config-1 and config-2 field shapes.
+INIT_CASES = {
+    "c1": dict(batch_size=4096, num_levels=8, table_size=2**14, seed=0),
+    "c2": dict(batch_size=1 << 18, num_levels=16, table_size=2**19, seed=0),
+    "np2": dict(batch_size=512, num_levels=6, table_size=393217, max_resolution=512, seed=3),
+}
+
+
+def sha256(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
 def sparse_sample(a, k=4000, seed=7):
     """(flat indices, values) of up to k nonzeros of a, deterministic."""
     flat = a.reshape(-1)

@@ -305,9 +305,36 @@ def dynamic_case():
     np.savez_compressed(OUT / "dynamic_c1.npz", **res)
 
 
+def init_case():
+    """TrainState.create at the INIT_CASES configs: resolutions, MLP layers, s_log and
+    the rng state afterwards in full; tables as sha256 + level norms + a sparse sample
+    (64 MiB at config 2)."""
+    res = {}
+    for name, kw in cases.INIT_CASES.items():
+        cfg = trainer.TrainConfig(**kw)
+        st = trainer.TrainState.create(cfg)
+        p, k = st.params, name + "_"
+        res[k + "resolutions"] = np.asarray(p.grid.resolutions, np.int64)
+        for i, h in enumerate(p.sdf_net.layers):
+            res[k + f"sdf{i}"] = h
+        for i, h in enumerate(p.color_net.layers):
+            res[k + f"col{i}"] = h
+        res[k + "slog"] = np.asarray(p.sharpness_log, np.float64)
+        res[k + "tables_sha256"] = np.array(cases.sha256(p.grid.tables))
+        res[k + "tables_norms"] = cases.level_norms(p.grid.tables)
+        res[k + "tables_idx"], res[k + "tables_val"] = cases.sparse_sample(p.grid.tables)
+        res[k + "aabb"] = np.array([p.grid.aabb_min, p.grid.aabb_min + p.grid.aabb_extent])
+        res[k + "occ"] = np.array([st.occ.resolution, st.occ.threshold, st.occ.step_size])
+        res[k + "rng_next"] = st.rng.integers(0, 2**62, size=8)
+    np.savez_compressed(OUT / "init.npz", **res)
+
+
 def main():
     if sys.argv[1:] == ["dynamic"]:
         dynamic_case()
+        return
+    if sys.argv[1:] == ["init"]:
+        init_case()
         return
     checkpoint_case()
     kat()
@@ -317,6 +344,7 @@ def main():
     for g in ("c1", "c2"):
         field_case(g)
     occupancy_case()
+    init_case()
     for s in cases.STEP_CASES:
         step_case(s)
     for f in sorted(OUT.glob("*.npz")):

@@ -1,0 +1,251 @@
+"""Config-2 parity: the step `bench.py` times (BASELINE configs[1]) against the oracle.
+
+Scene: the DTU-shaped two-spheres dataset (49 orbit views, 1600x1200, the scene aabb),
+field: 16 levels, T = 2^19 (5 dense + 11 hashed levels), 64-wide SDF + colour MLPs,
+Eikonal weight 0.1 -- exactly the bench workload -- on a 4096-ray sub-batch drawn by the
+oracle's `sample_ray_batch` (`scene_io.py:129-172`), so the oracle finishes in seconds.
+
+Two bars (`trainer.py:281-310`):
+* `test_c2_steps_flat`: every step starts from identical parameters and moments (the
+  oracle's are copied into the product), and two kinds of rays are removed from the
+  batch first: rays whose alpha-clamp set differs between the two sides (the NeuS alpha
+  is clipped at 0 with zero gradient but an O(s) gradient just above,
+  `renderer.py:52-56`; see tests/test_oracle_conditioning.py), and rays holding a sample
+  whose ReLU pre-activation is within 1e-6 (relative) of zero in the oracle's forward
+  (a mask that fp32 rounding can flip; see `relu_tie_rays`).  Rays are independent, so
+  the remaining rays see the same arithmetic; losses, P and every gradient tensor are
+  then held to a flat 1e-3 (relL2 and max-abs / max|ref|), post-Adam MLP parameters to
+  1e-3.  The achieved errors are ~1e-5 (profiles/r02_c2_step_parity.jsonl).
+* `test_c2_steps_chained`: three (lambda = 16) or two (lambda = 2) consecutive steps on
+  the FULL sub-batch (nothing dropped), the parameters and Adam moments re-synchronised
+  after each step, gradients held to max(1e-3, 2x the oracle's own sensitivity to a 1e-6
+  weight perturbation) -- the c1 protocol of test_gpu_parity.py.
+
+Achieved errors are printed per tensor (pytest -s) and appended as JSON lines to
+$NS2B_PARITY_LOG when set (profiles/r02_c2_step_parity.jsonl).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers skip at collection
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import cases  # noqa: E402
+from helpers import np_, product_state_from_oracle, sync_product_from_oracle  # noqa: E402
+from oracle import render as orender  # noqa: E402
+from oracle import scene as oscene  # noqa: E402
+from oracle import train as otrain  # noqa: E402
+from paper_2212_05231_b200 import scene_io as pscene  # noqa: E402
+from paper_2212_05231_b200 import trainer as ptrain  # noqa: E402
+from parity import max_err, rel_err  # noqa: E402
+from test_gpu_parity import assert_adam_tables, oracle_sensitivity, sens_bar  # noqa: E402
+
+TOL = 1e-3
+RAYS = 4096
+ALPHA_MAX = 1.0 - 1e-7  # renderer.py:28-32
+
+
+def record(test, step, errs, **extra):
+    line = {"test": test, "step": step, **extra,
+            "errors": {k: {"relL2": float(r), "max": float(m)} for k, (r, m) in errs.items()}}
+    print(json.dumps(line))
+    path = os.environ.get("NS2B_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(line) + "\n")
+
+
+@pytest.fixture(scope="module")
+def dtu():
+    """The bench's DTU-shaped dataset (`bench.py` c2 workload)."""
+    return pscene.make_synthetic_device("two-spheres", 49, 1600, 1200, 1.4 * 1200, torch.device("cuda"))
+
+
+@pytest.fixture(scope="module")
+def sphere64():
+    return oscene.make_synthetic("sphere", views=8, seed=0, image_size=64)
+
+
+# (grid, level_init, steps): config 2 at lambda = 16 and along the schedule (lambda = 2),
+# and the odd table size (np2: 393217 rows, so every other level of the gradient buffer
+# starts 8-B aligned -- the scatter's 16-B x-pair REDs must fall back there)
+FLAT_CASES = [("c2", 16, 3), ("c2", 2, 2), ("np2", 6, 2)]
+
+
+def c2_oracle_state(ds, level_init, grid="c2"):
+    spec = cases.GRIDS[grid]
+    cfg = otrain.TrainConfig(batch_size=RAYS, num_levels=spec["num_levels"], table_size=spec["table_size"],
+                             min_resolution=spec["min_resolution"], max_resolution=spec["max_resolution"],
+                             seed=0, level_init=level_init)
+    ost = otrain.TrainState.create(cfg, aabb=ds.scene_aabb)
+    orender.update_occupancy(ost.occ, ost.params, otrain.level_schedule(0, cfg))
+    ost.step = 1  # later steps: no occupancy refresh, both sides march the same bits
+    return cfg, ost
+
+
+def flip_rays(p_alphas, rec):
+    """Rays with an interval whose clamp state (alpha == 0, or == ALPHA_MAX) differs."""
+    a_gpu = p_alphas[rec.interval_first]
+    bad = ((a_gpu == 0) != (rec.alphas == 0)) | ((a_gpu >= ALPHA_MAX) != (rec.alphas >= ALPHA_MAX))
+    return np.unique(rec.ray_ids[rec.interval_first[bad]])
+
+
+def relu_tie_rays(params, rec, tau=1e-6):
+    """Rays with a sample whose ReLU pre-activation (either net, any hidden unit) lies
+    within tau (relative to sum |h| |a|) of zero in the oracle's forward.  The tensor-core
+    forward matches the oracle's z to ~1e-7 relative, so such a mask can flip, and a
+    flipped mask changes that sample's backward discontinuously (its j_d, normal and
+    cotangents): at c2 ~10 of 373k samples, which alone move single fine-level table
+    entries by up to 3e-3 of the level's max (tools/diag_c2.py); with their cotangents
+    zeroed the worst table entry is within 5e-6."""
+    c = rec.cache
+    margin = np.full(c.x.shape[0], np.inf)
+    for net, t in ((params.sdf_net, c.sdf_trace), (params.color_net, c.color_trace)):
+        a = t.x
+        for h, act in zip(net.layers[:-1], t.activations):
+            z = a.astype(np.float64) @ h.T.astype(np.float64)
+            sc = np.abs(a).astype(np.float64) @ np.abs(h.T).astype(np.float64)
+            margin = np.minimum(margin, (np.abs(z) / np.maximum(sc, 1e-30)).min(1))
+            a = act
+    return np.unique(rec.ray_ids[margin < tau])
+
+
+def grad_errors(pst, og, level):
+    sdf_g, col_g, tab_g = pst.params.layout.views(pst.ws.grads)
+    errs = {}
+    for i in range(2):
+        a, b = np_(sdf_g[i]), og.sdf_layers[i]
+        errs[f"grad_sdf{i}"] = (rel_err(a, b), max_err(a, b))
+    for i in range(3):
+        a, b = np_(col_g[i]), og.color_layers[i]
+        errs[f"grad_color{i}"] = (rel_err(a, b), max_err(a, b))
+    gt = np_(tab_g)
+    for lv in range(level):
+        errs[f"grad_tables{lv}"] = (rel_err(gt[lv], og.tables[lv]), max_err(gt[lv], og.tables[lv]))
+    return errs
+
+
+def subset(b, keep):
+    return oscene.RayBatch(b.origins[keep], b.directions[keep], b.target_colors[keep],
+                           b.foreground_flags[keep])
+
+
+@pytest.mark.parametrize("grid,level_init,steps", FLAT_CASES)
+def test_c2_steps_flat(request, grid, level_init, steps):
+    dtu = request.getfixturevalue("dtu" if grid == "c2" else "sphere64")
+    cfg, ost = c2_oracle_state(dtu, level_init, grid)
+    pst = product_state_from_oracle(ost)
+    rng = np.random.default_rng(21)
+    for step in range(steps):
+        sync_product_from_oracle(pst, ost)
+        b = oscene.sample_ray_batch(dtu, 0, RAYS, cfg.fg_fraction, rng)
+        level = otrain.level_schedule(ost.step, cfg)
+        # the alpha-clamp sets of the two sides on the full batch (forward only)
+        from paper_2212_05231_b200 import renderer as prender
+
+        _, orec = orender.render_rays(b, ost.params, ost.occ, level)
+        _, prec = prender.render_rays(b, pst.params, pst.occ, level)
+        assert prec.sample_count == orec.sample_count
+        flips = flip_rays(np_(prec.alphas_per_sample), orec)
+        assert flips.size <= max(4, 0.005 * RAYS), f"{flips.size} rays with alpha-clamp flips"
+        ties = relu_tie_rays(ost.params, orec)
+        assert ties.size <= 0.05 * RAYS, f"{ties.size} rays with near-tie ReLU pre-activations"
+        drop = np.union1d(flips, ties)
+        bk = subset(b, np.setdiff1d(np.arange(RAYS), drop))
+        old = ost.params.grid.tables.astype(np.float64)
+        lr = cfg.lr_tables * otrain.lr_factor(ost.step, cfg.total_steps, cfg.lr_final_fraction)
+        tr = {}
+        ro = otrain.train_step(ost, dtu, batch=bk, trace=tr)
+        rp = ptrain.train_step(pst, dtu, batch=bk)
+        assert rp.sample_count == ro.sample_count and rp.level == ro.level == level
+        rec = tr["records"]
+        assert flip_rays(np_(pst.ws.alphas[:rp.sample_count]), rec).size == 0
+        errs = grad_errors(pst, tr["grads"], level)
+        for k in ("color", "eikonal", "total", "psnr"):
+            a, r = getattr(rp, k), getattr(ro, k)
+            errs[f"loss_{k}"] = (abs(a - r) / max(abs(r), 1e-30), abs(a - r) / max(abs(r), 1e-30))
+        errs["dl_dslog"] = (abs(pst.last_dslog - tr["dl_dslog"]) / abs(tr["dl_dslog"]),) * 2
+        pp = pst.params
+        for i in range(2):
+            a, b_ = np_(pp.sdf_net.layers[i]), ost.params.sdf_net.layers[i]
+            errs[f"param_sdf{i}"] = (rel_err(a, b_), max_err(a, b_))
+        for i in range(3):
+            a, b_ = np_(pp.color_net.layers[i]), ost.params.color_net.layers[i]
+            errs[f"param_color{i}"] = (rel_err(a, b_), max_err(a, b_))
+        record(f"{grid}_flat", step, errs, level=level, rays=int(bk.count), dropped_rays=int(drop.size),
+               alpha_flip_rays=int(flips.size), relu_tie_rays=int(ties.size), samples=int(ro.sample_count))
+        bad = {k: v for k, v in errs.items() if v[0] > TOL or v[1] > TOL}
+        assert not bad, f"step {step}: above 1e-3: {bad}"
+        assert_adam_tables(np_(pp.grid.tables), ost.params.grid.tables, old, lr)
+        assert abs(pp.sharpness - ost.params.sharpness) <= 1e-6 * ost.params.sharpness
+
+
+@pytest.mark.parametrize("level_init,steps", [(16, 3), (2, 2)])
+def test_c2_steps_chained(dtu, level_init, steps):
+    cfg, ost = c2_oracle_state(dtu, level_init)
+    pst = product_state_from_oracle(ost)
+    rng = np.random.default_rng(22)
+    for step in range(steps):
+        b = oscene.sample_ray_batch(dtu, 0, RAYS, cfg.fg_fraction, rng)
+        sens = oracle_sensitivity(ost, dtu, b, seeds=(1, 2))
+        old = ost.params.grid.tables.astype(np.float64)
+        old_mlp = [h.astype(np.float64) for h in list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers)]
+        lr = cfg.lr_tables * otrain.lr_factor(ost.step, cfg.total_steps, cfg.lr_final_fraction)
+        tr = {}
+        ro = otrain.train_step(ost, dtu, batch=b, trace=tr)
+        rp = ptrain.train_step(pst, dtu, batch=b)
+        assert rp.sample_count == ro.sample_count and rp.level == ro.level
+        rec = tr["records"]
+        a_gpu = np_(pst.ws.alphas[:rp.sample_count])[rec.interval_first]
+        flips = int(((a_gpu == 0) != (rec.alphas == 0)).sum())
+        assert flips <= max(2, 1e-4 * rec.alphas.size), f"{flips} alpha-clamp flips"
+        errs = grad_errors(pst, tr["grads"], ro.level)
+        record("c2_chained", step, errs, level=ro.level, samples=int(ro.sample_count),
+               alpha_clamp_flips=flips,
+               bars={k: sens_bar(sens, k.replace("grad_", "")) for k in errs})
+        for k in ("color", "eikonal", "total", "psnr"):
+            a, r = getattr(rp, k), getattr(ro, k)
+            assert abs(a - r) <= TOL * max(abs(r), 1e-9), f"{k}: {a} vs {r}"
+        assert abs(pst.last_dslog - tr["dl_dslog"]) <= TOL * abs(tr["dl_dslog"])
+        for k, (r_, m_) in errs.items():
+            rb, mb = sens_bar(sens, k.replace("grad_", ""))
+            assert r_ <= rb and m_ <= mb, f"{k} step {step}: relL2 {r_:.2e} (bar {rb:.1e}), max {m_:.2e} ({mb:.1e})"
+        pp = pst.params
+        # Adam's first steps move every entry by ~lr whatever |g| is, so an MLP entry whose
+        # gradient sits at the noise floor (or moves through a clamp flip) may step the
+        # other way: relL2 within 1e-3, per-entry steps by the assert_adam_tables bar
+        lr_m = cfg.lr_mlp * otrain.lr_factor(ost.step - 1, cfg.total_steps, cfg.lr_final_fraction)
+        for name, got, ref, prev in zip(
+                ["sdf0", "sdf1", "color0", "color1", "color2"],
+                list(pp.sdf_net.layers) + list(pp.color_net.layers),
+                list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers), old_mlp):
+            assert rel_err(np_(got), ref) <= TOL, f"{name}: relL2 {rel_err(np_(got), ref):.2e}"
+            assert_adam_tables(np_(got), ref, prev, lr_m, name)
+        assert_adam_tables(np_(pp.grid.tables), ost.params.grid.tables, old, lr)
+        # Adam turned the noise-floor gradient entries into opposite +-lr steps: start the
+        # next step from the oracle's parameters and moments again
+        sync_product_from_oracle(pst, ost)
+
+
+@pytest.mark.parametrize("name", list(cases.INIT_CASES))
+def test_product_init_matches_reference(name):
+    """The product's seeded `TrainState.create` (`trainer.py:192-212`, `field.py:81-165`,
+    `hash_encoding.py:31-45`) equals the reference's bit for bit (golden init.npz,
+    written by the reference), including the rng stream it leaves for the sampler."""
+    from test_oracle_golden import check_init, load
+
+    st = ptrain.TrainState.create(ptrain.TrainConfig(**cases.INIT_CASES[name]))
+    p = st.params
+    check_init(load("init.npz"), name, p.grid.resolutions, [np_(h) for h in p.sdf_net.layers],
+               [np_(h) for h in p.color_net.layers], np_(p.sharpness_log), np_(p.grid.tables),
+               [p.grid.aabb_min, p.grid.aabb_min + p.grid.aabb_extent],
+               [st.occ.resolution, st.occ.threshold, st.occ.step_size], st.rng)

@@ -120,7 +120,7 @@ def test_march_bit_exact(sphere64):
     assert_exact(np_(got.positions32), ref.positions.astype(np.float32), "fp32 positions")
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("name", ["c1", "c2", "np2"])
 @pytest.mark.parametrize("lam", ["all", 3])
 def test_field_forward_backward(name, lam):
     from test_oracle_golden import oracle_field_params

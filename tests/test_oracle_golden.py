@@ -215,3 +215,42 @@ def test_train_step(name):
         for i, h in enumerate(p.color_net.layers):
             assert_close(h, gold[k + f"new_col{i}"], 1e-6, f"new_col{i}")
         assert_close(p.sharpness_log, gold[k + "new_slog"], 1e-12, "slog")
+
+
+def check_init(gold, name, resolutions, sdf, col, slog, tables, aabb, occ, rng):
+    """TrainState.create parity against the reference's golden init (bit-exact)."""
+    k = name + "_"
+    assert_exact(np.asarray(resolutions, np.int64), gold[k + "resolutions"], "resolutions")
+    for i, h in enumerate(sdf):
+        assert_exact(np.asarray(h), gold[k + f"sdf{i}"], f"sdf{i}")
+    for i, h in enumerate(col):
+        assert_exact(np.asarray(h), gold[k + f"col{i}"], f"col{i}")
+    assert_exact(np.asarray(slog, np.float64).reshape(-1), gold[k + "slog"].reshape(-1), "s_log")
+    tables = np.ascontiguousarray(tables, np.float32)
+    assert cases.sha256(tables) == str(gold[k + "tables_sha256"]), "tables differ (sha256)"
+    assert_exact(tables.reshape(-1)[gold[k + "tables_idx"]], gold[k + "tables_val"], "tables sample")
+    assert_exact(np.asarray(aabb, np.float64), gold[k + "aabb"], "aabb")
+    assert_exact(np.asarray(occ, np.float64), gold[k + "occ"], "occupancy grid")
+    assert_exact(rng.integers(0, 2**62, size=8), gold[k + "rng_next"], "rng stream after init")
+
+
+@pytest.mark.parametrize("name", list(cases.INIT_CASES))
+def test_oracle_init(name):
+    """`trainer.py:192-212` / `field.py:81-165` / `hash_encoding.py:31-45`: the oracle's
+    seeded TrainState.create equals the reference's, bit for bit."""
+    gold = load("init.npz")
+    st = otrain.TrainState.create(otrain.TrainConfig(**cases.INIT_CASES[name]))
+    p = st.params
+    check_init(gold, name, p.grid.resolutions, p.sdf_net.layers, p.color_net.layers, p.sharpness_log,
+               p.grid.tables, [p.grid.aabb_min, p.grid.aabb_min + p.grid.aabb_extent],
+               [st.occ.resolution, st.occ.threshold, st.occ.step_size], st.rng)
+
+
+@pytest.mark.parametrize("name", list(cases.INIT_CASES))
+def test_product_level_resolutions(name):
+    """The product's `hash_encoding.level_resolutions` (host, no device needed)."""
+    from paper_2212_05231_b200 import hash_encoding as pe
+
+    kw = cases.INIT_CASES[name]
+    res = pe.level_resolutions(kw["num_levels"], 16, kw.get("max_resolution", 2048))
+    assert_exact(np.asarray(res, np.int64), load("init.npz")[name + "_resolutions"], "resolutions")

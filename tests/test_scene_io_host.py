@@ -65,3 +65,41 @@ def test_load_dataset(tmp_path):
     (tmp_path / "transforms.json").write_text(json.dumps(bad))
     with pytest.raises(ValueError, match="invalid pose"):
         ps.load_dataset(tmp_path)
+
+
+def _golden_batches():
+    """The reference's first two `sample_ray_batch` draws after `TrainState.create`
+    (tests/golden/step_c1_full.npz, written by make_golden.py from the reference)."""
+    from pathlib import Path
+
+    import cases
+
+    g = dict(np.load(Path(__file__).resolve().parent / "golden" / "step_c1_full.npz"))
+    spec = cases.STEP_CASES["c1_full"]
+    return g, spec
+
+
+def test_host_sampler_matches_reference_golden():
+    """`scene_io.sample_ray_batch` (`scene_io.py:129-172`) on the product's in-memory
+    `make_synthetic` dataset, drawing from the rng the seeded init leaves (the oracle's
+    `TrainState.create`, pinned to the reference's rng stream in test_oracle_golden):
+    the reference's golden batches, origins and targets bit-exact, directions within
+    1 ulp (the 3x3 rotation's BLAS summation order), and so is the oracle's sampler."""
+    from oracle import train as otrain
+
+    g, spec = _golden_batches()
+    sc = spec["scene"]
+    ds = ps.make_synthetic(sc["preset"], views=sc["views"], seed=sc["seed"], image_size=sc["image_size"])
+    ods = oscene.make_synthetic(sc["preset"], views=sc["views"], seed=sc["seed"], image_size=sc["image_size"])
+    cfg = otrain.TrainConfig(**spec["cfg"])
+    rng = otrain.TrainState.create(cfg).rng
+    orng = otrain.TrainState.create(cfg).rng
+    for s in range(2):
+        b = ps.sample_ray_batch(ds, 0, cfg.batch_size, cfg.fg_fraction, rng)
+        ob = oscene.sample_ray_batch(ods, 0, cfg.batch_size, cfg.fg_fraction, orng)
+        for got in (b, ob):
+            assert np.array_equal(got.origins, g[f"s{s}_origins"])
+            assert np.array_equal(got.target_colors, g[f"s{s}_targets"])
+            ulp = np.abs(got.directions - g[f"s{s}_dirs"]) / np.spacing(np.abs(g[f"s{s}_dirs"]))
+            assert ulp.max() <= 1, f"step {s}: directions {ulp.max()} ulp"
+    assert rng.bit_generator.state == orng.bit_generator.state

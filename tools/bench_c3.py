@@ -59,7 +59,46 @@ def torch_sdf(x, tables, resolutions, lo, ext, h1, h2):
     return (a1 @ h2.T)[:, 0]
 
 
-def autograd_step(x, tables, resolutions, lo, ext, h1, h2, chunk=1 << 18):
+_OFFS = {}
+
+
+def torch_sdf_vec(x, tables, resolutions, lo, ext, h1, h2):
+    """The same SDF as `torch_sdf`, vectorised: all levels and all 8 corners of a point
+    in one index tensor (L, P, 8) and ONE gather from the flattened tables, weights as
+    one (L, P, 8) product -- the fair plain-PyTorch formulation of the encoding."""
+    dt = tables.dtype
+    L, T = tables.shape[0], tables.shape[1]
+    dev = x.device
+    key = (dev, L)
+    if key not in _OFFS:
+        o = torch.tensor([[(c >> 2) & 1, (c >> 1) & 1, c & 1] for c in range(8)], device=dev)
+        res = torch.tensor(resolutions, device=dev, dtype=torch.int64)
+        dense = (res + 1) ** 3 <= T
+        _OFFS[key] = (o, res, dense)
+    o, res, dense = _OFFS[key]
+    xn = ((x.float() - lo.float()) / ext.float()).clamp(0.0, 1.0)
+    t = xn.double()[None] * res[:, None, None].double()              # (L, P, 3)
+    c = (torch.ceil(t.detach()) - 1).clamp(min=0)
+    c = torch.minimum(c, (res - 1)[:, None, None].double())
+    fr = (t - c).to(dt)                                               # (L, P, 3)
+    cc = c.to(torch.int64)[:, :, None, :] + o[None, None]             # (L, P, 8, 3)
+    n1 = (res + 1)[:, None, None]
+    row_d = cc[..., 0] + cc[..., 1] * n1 + cc[..., 2] * n1 * n1
+    row_h = (cc[..., 0] ^ (cc[..., 1] * P1) ^ (cc[..., 2] * P2)) % T
+    row = torch.where(dense[:, None, None], row_d, row_h)
+    row = row + (torch.arange(L, device=dev) * T)[:, None, None]
+    ob = o.bool()[None, None]                                         # (1, 1, 8, 3)
+    w = torch.where(ob, fr[:, :, None, :], 1.0 - fr[:, :, None, :]).prod(dim=3)  # (L, P, 8)
+    v = tables.reshape(L * T, -1)[row]                                # (L, P, 8, F)
+    feats = (w[..., None] * v).sum(dim=2)                             # (L, P, F)
+    feats = feats.permute(1, 0, 2).reshape(x.shape[0], -1)
+    xe = x.to(dt)
+    e = torch.cat([xe, feats, torch.ones_like(xe[:, :1])], dim=1)
+    a1 = torch.relu(e @ h1.T)
+    return (a1 @ h2.T)[:, 0]
+
+
+def autograd_step(x, tables, resolutions, lo, ext, h1, h2, chunk=1 << 18, sdf=None):
     """Eikonal loss mean((|grad_x d| - 1)^2) and its parameter gradients by double
     backward, in chunks of points (the mean is split exactly) to bound autograd memory."""
     n_all = x.shape[0]
@@ -67,7 +106,7 @@ def autograd_step(x, tables, resolutions, lo, ext, h1, h2, chunk=1 << 18):
     total = 0.0
     for s in range(0, n_all, chunk):
         xc = x[s:s + chunk].detach().to(tables.dtype).requires_grad_(True)
-        d = torch_sdf(xc, tables, resolutions, lo, ext, h1, h2)
+        d = (sdf or torch_sdf)(xc, tables, resolutions, lo, ext, h1, h2)
         (n,) = torch.autograd.grad(d.sum(), xc, create_graph=True)
         loss = ((n.norm(dim=1) - 1.0) ** 2).sum() / n_all
         g = torch.autograd.grad(loss, [tables, h1, h2])
@@ -120,7 +159,7 @@ def _autograd_at(p, x, dtype):
     ext = torch.tensor(p.grid.aabb_extent, device="cuda", dtype=dtype)
     args = [t.detach().clone().to(dtype).requires_grad_(True)
             for t in (p.grid.tables, p.sdf_net.layers[0], p.sdf_net.layers[1])]
-    return autograd_step(x, args[0], res, lo, ext, args[1], args[2])
+    return autograd_step(x, args[0], res, lo, ext, args[1], args[2], sdf=torch_sdf_vec)
 
 
 def compare(points=14, order="uniform"):
@@ -142,7 +181,14 @@ def main():
     ap.add_argument("--points", type=int, default=22)
     ap.add_argument("--order", default="uniform", choices=["uniform", "rays"])
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--compile", action="store_true", help="also time a torch.compile'd baseline")
+    ap.add_argument("--check64", action="store_true",
+                    help="accuracy of ours and torch fp32 against torch fp64 double backward at --points")
     a = ap.parse_args()
+    if a.check64:
+        print(json.dumps({"config": f"c3 accuracy vs torch fp64 double backward, 2^{a.points} points ({a.order})",
+                          **compare(a.points, a.order)}))
+        return
     p, x = setup(a.points, a.order)
     res = p.grid.resolutions.tolist()
     lo = torch.tensor(p.grid.aabb_min, device="cuda", dtype=torch.float32)
@@ -164,13 +210,21 @@ def main():
         return e0.elapsed_time(e1) / a.iters, out
 
     t_ours, (lo_, gr) = timed(lambda: ours_step(p, x))
-    t_ag, (la, (gt, g1, g2)) = timed(lambda: autograd_step(x, tab, res, lo, ext, h1, h2))
-    print(json.dumps({
-        "config": f"c3: SDF fwd + normal + Eikonal bwd, 2^{a.points} points ({a.order}), 16 levels 2^19",
-        "points": x.shape[0], "ours_ms": t_ours, "autograd_ms": t_ag, "speedup": t_ag / t_ours,
-        "loss": [float(lo_), float(la)],
-        "grad_rel_l2": {"tables": rel(gr.tables, gt), "h1": rel(gr.sdf_layers[0], g1),
-                        "h2": rel(gr.sdf_layers[1], g2)}}))
+    out = {"config": f"c3: SDF fwd + normal + Eikonal bwd, 2^{a.points} points ({a.order}), 16 levels 2^19",
+           "points": x.shape[0], "ours_ms": t_ours, "loss_ours": float(lo_), "baselines": {}}
+    variants = {"loop": torch_sdf, "vectorised": torch_sdf_vec}
+    if a.compile:
+        variants["vectorised+torch.compile"] = torch.compile(torch_sdf_vec, dynamic=False)
+    for name, fn in variants.items():
+        try:
+            t_ag, (la, (gt, g1, g2)) = timed(lambda: autograd_step(x, tab, res, lo, ext, h1, h2, sdf=fn))
+            out["baselines"][name] = {
+                "autograd_ms": t_ag, "speedup": t_ag / t_ours, "loss": float(la),
+                "grad_rel_l2": {"tables": rel(gr.tables, gt), "h1": rel(gr.sdf_layers[0], g1),
+                                "h2": rel(gr.sdf_layers[1], g2)}}
+        except Exception as exc:  # e.g. torch.compile without double-backward support
+            out["baselines"][name] = {"unavailable": f"{type(exc).__name__}: {str(exc).splitlines()[0][:200]}"}
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
