@@ -94,6 +94,16 @@ constexpr uint32_t TB_SB = 432;    // 64
 constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
 constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
+// Weight-gradient GEMMs (dW = X^T Y summed over the tile's 128 samples, and over a CTA's
+// ~1.2k tiles in TMEM) take the forward-side activation operand in fp16 (its hi part
+// only: fp16 storage of A1, CIN, A1c, A2c and E for the weight gradients, fp32
+// accumulation) and the cotangent operand split hi + lo:
+//   activation is A:  A_hi B_hi + A_hi B_lo   (gemm2a)
+//   activation is B:  A_hi B_hi + A_lo B_hi   (gemm2w)
+// two MMAs per K step instead of three, and the forward stores (the backward DMAs) only
+// the hi halves of its tiles.  The per-sample chain GEMMs keep the full 3-term split.
+#define WG_ACT_A umma::gemm2a
+#define WG_ACT_B umma::gemm2w
 
 #ifdef NS2B_PHASE_PROF
 #define PMARK(i)                                  \
@@ -267,15 +277,16 @@ struct LevelSm {
 // Per-tile workspace (see ns2b_field_workspace_bytes):
 //   gather  -> pre-staged E tiles (fp16 hi | lo, UMMA tile layout) + exponent, d feature/dx
 //              value-major [tile][96][128] fp32, position | view dir [tile][6][128] fp32;
-//   MLP fwd -> its staged operand tiles A1 | CIN | A1c | A2c (fp16 hi | lo) + exponents,
+//   MLP fwd -> its staged operand tiles A1 | CIN | A1c | A2c (fp16 hi parts) + exponents,
 //              ReLU masks [tile][4][128] (uint2: m1 | mc1 << 16, mc2 of a column quarter),
 //              normal | colour [tile][6][128] fp32, j_d feature rows (into the sb block);
 //   MLP bwd -> scatter inputs [tile][68][128] fp32 = dL/dfeature (32) | j_d rows (32) | q (3).
 // The backward therefore never recomputes the forward: it DMAs the forward's tiles.
 //   MLP bwd (input cotangents requested) -> [tile][9][128] fp32 = dcin_x (3) | dcin_v (3) | de_x (3).
 constexpr int JROWS = 96, SBROWS = 68, XVROWS = 6, NCROWS = 6, XINROWS = 9;
-constexpr uint32_t FW_A1 = 0, FW_CIN = 2 * T64B, FW_A1C = FW_CIN + 2 * TCB, FW_A2C = FW_A1C + 2 * T64B,
-                   FWB = FW_A2C + 2 * T64B;
+// stored tiles: fp16 hi parts only (the weight-gradient GEMMs read nothing else)
+constexpr uint32_t FW_A1 = 0, FW_CIN = T64B, FW_A1C = FW_CIN + TCB, FW_A2C = FW_A1C + T64B,
+                   FWB = FW_A2C + T64B;
 struct Workspace {
     uint8_t *e_tiles;
     int *e_exp;
@@ -564,7 +575,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             umma::gemm3w<4>(tb + TM_SB, S.K(TX, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
             umma::gemm2a<4>(tb + TM_SA, S.K(TC, T64B, 64), S.MN(WH1S, WH1B, 48), ID_KM(48), false);
             umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), 2 * T64B);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(TX), T64B);
         }
         wait_mma(mbar, phase);
         PMARK(4);
@@ -663,7 +674,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
         if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
             umma::gemm3w<2>(tb + TM_SA, S.K(TC, TCB, 32), S.K(WC1, WC1B, 32), ID_KK(64), false);
             umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), 2 * TCB);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(TC), TCB);
         }
         const bool jnext = ntile * TILE < P;
         if (jnext) j_load(ntile);  // next tile's d feature/dx: its latency hides under the Zc1 GEMM
@@ -710,7 +721,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             if (lane == 0) umma::bulk_wait_read_n<2>();
             __syncwarp();
             umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), 2 * T64B);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(TZ), T64B);
         }
         wait_mma(mbar, phase);
         PMARK(10);
@@ -765,7 +776,7 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             }
         }
         if (t == kMmaWarp * 32) {  // the thread that issues (and drains) the tile stores
-            umma::bulk_s2g(fwt + FW_A2C, S.p(TY), 2 * T64B);
+            umma::bulk_s2g(fwt + FW_A2C, S.p(TY), T64B);
             ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
         ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
@@ -998,10 +1009,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         const int64_t t0 = blockIdx.x;
         if (t0 * TILE < P) {
             if (t == kDmaThread) {
-                dma(TW, fwt(t0) + FW_A2C, 2 * T64B, mb_w);
-                dma(TZ, fwt(t0) + FW_A1C, 2 * T64B, mb_z);
-                dma(TC, fwt(t0) + FW_CIN, 2 * TCB, mb_c);
-                dma(TE, ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mb_e);
+                dma(TW, fwt(t0) + FW_A2C, T64B, mb_w);
+                dma(TZ, fwt(t0) + FW_A1C, T64B, mb_z);
+                dma(TC, fwt(t0) + FW_CIN, TCB, mb_c);
+                dma(TE, ws.e_tiles + t0 * 2 * TEB, TEB, mb_e);  // E hi part (weight gradient)
             }
             j_load(t0);
             j_store();
@@ -1054,7 +1065,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         if (t == kDmaThread && has_next) {  // next tile's inputs -> L2 while this one runs
             umma::prefetch_l2(fwt(ntile), FWB);
             umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
-            umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, 2 * TEB);
+            umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, TEB);
             umma::prefetch_l2(ws.fw_nc + ntile * NCROWS * TILE, NCROWS * TILE * 4);
             umma::prefetch_l2(ws.fw_mask + ntile * 4 * TILE, 4 * TILE * 8);
             const int64_t nlast = min(static_cast<int64_t>(P), (ntile + 1) * TILE);  // dl_dc / dl_dsdf rows
@@ -1114,7 +1125,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 umma::gemm3w<1>(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_w, ph_w));
-                umma::gemm3w<8>(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
+                WG_ACT_A<8>(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
             }
             ph_w ^= 1u;
         }
@@ -1156,7 +1167,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 umma::gemm3w<4>(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_z, ph_z));
-                umma::gemm3w<8>(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), ID_WG(64), acc);
+                WG_ACT_B<8>(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), ID_WG(64), acc);
             }
             ph_z ^= 1u;
         }
@@ -1198,9 +1209,9 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), ID_KM(32), false);
                 umma::commit_elect(mbar);
                 // TW is free: dC3 (B0) completed before B1's chain GEMM did
-                if (lane == 0) dma(TW, fwt(tile) + FW_A1, 2 * T64B, mb_w);
+                if (lane == 0) dma(TW, fwt(tile) + FW_A1, T64B, mb_w);
                 PWAIT(umma::mbar_wait(mb_c, ph_c));
-                umma::gemm3w<8>(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), ID_WG(32), acc);
+                WG_ACT_B<8>(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), ID_WG(32), acc);
             }
             ph_c ^= 1u;
         }
@@ -1263,7 +1274,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 umma::gemm3w<1>(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_w, ph_w));
-                umma::gemm3w<8>(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
+                WG_ACT_A<8>(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
             }
             ph_w ^= 1u;
         }
@@ -1316,7 +1327,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         PMARK(12);
         // ------------------------------------------------ B4: u -> DE, dH1, G
         // TC is free (dC1 of B2 completed before B3's chain GEMM): next tile's CIN
-        if (t == kDmaThread && has_next) dma(TC, fwt(ntile) + FW_CIN, 2 * TCB, mb_c);
+        if (t == kDmaThread && has_next) dma(TC, fwt(ntile) + FW_CIN, TCB, mb_c);
         int eU;
         {
             float u[2][8], mu = 0.f;
@@ -1359,7 +1370,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_e, ph_e));
-                umma::gemm3w<8>(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), ID_WG(48), acca);
+                WG_ACT_B<8>(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), ID_WG(48), acca);
                 umma::gemm2a<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
                 umma::commit_elect(mbarw);
             }
@@ -1370,7 +1381,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         PMARK(15);
         // ------------------------------------------------ B5: scatter inputs; next tile's DMAs
         // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
-        if (t == kDmaThread && has_next) dma(TW, fwt(ntile) + FW_A2C, 2 * T64B, mb_w);
+        if (t == kDmaThread && has_next) dma(TW, fwt(ntile) + FW_A2C, T64B, mb_w);
         {
             // dL/dfeature pairs (DE) and q for the scatter kernel
             const float sde = pow2i(-(eU + eH1));
@@ -1397,8 +1408,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             wait_mma(mbarw, phasew);  // B4's weight-gradient GEMMs: TX, TY, TZ, TE free
             PMARK(16);
             if (t == kDmaThread && has_next) {
-                dma(TE, ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mb_e);
-                dma(TZ, fwt(ntile) + FW_A1C, 2 * T64B, mb_z);
+                dma(TE, ws.e_tiles + ntile * 2 * TEB, TEB, mb_e);
+                dma(TZ, fwt(ntile) + FW_A1C, T64B, mb_z);
             }
             if (has_next) {
                 j_store();

@@ -19,7 +19,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU containers skip at c
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import cases  # noqa: E402
-from helpers import np_, product_params_from_oracle, product_state_from_oracle  # noqa: E402
+from helpers import np_, product_params_from_oracle, product_state_from_oracle, sync_product_from_oracle  # noqa: E402
 from oracle import field as ofield  # noqa: E402
 from oracle import hashgrid as ohg  # noqa: E402
 from oracle import kernels as ok  # noqa: E402
@@ -31,7 +31,7 @@ from paper_2212_05231_b200 import _lib  # noqa: E402
 from paper_2212_05231_b200 import field as pfield  # noqa: E402
 from paper_2212_05231_b200 import renderer as prender  # noqa: E402
 from paper_2212_05231_b200 import trainer as ptrain  # noqa: E402
-from parity import assert_close, assert_exact  # noqa: E402
+from parity import assert_close, assert_exact, rel_err  # noqa: E402
 
 TOL = 1e-3
 
@@ -289,9 +289,10 @@ def sens_bar(sens, key):
 
 @pytest.mark.parametrize("level_init", [2, 8])
 def test_train_steps_match_oracle(sphere64, level_init):
-    """Three full steps from the same init and the same ray batches: sample counts
-    exact; losses, all gradients and MLP parameters within 1e-3; tables after Adam by
-    assert_adam_tables."""
+    """Three full steps on the same ray batches, each from the oracle's parameters and
+    moments: sample counts exact; losses and all gradients within max(1e-3, 2x the
+    oracle's self-sensitivity); MLP parameters within 1e-3 relL2 and, like the tables,
+    per entry by assert_adam_tables."""
     cfg = otrain.TrainConfig(batch_size=2048, num_levels=8, table_size=2**14, seed=0,
                              level_init=level_init)
     ost = otrain.TrainState.create(cfg)
@@ -303,6 +304,7 @@ def test_train_steps_match_oracle(sphere64, level_init):
         b = oscene.sample_ray_batch(sphere64, 0, cfg.batch_size, cfg.fg_fraction, rng)
         sens = oracle_sensitivity(ost, sphere64, b)
         old = ost.params.grid.tables.astype(np.float64)
+        old_mlp = [h.astype(np.float64) for h in list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers)]
         tr = {}
         lr = cfg.lr_tables * otrain.lr_factor(ost.step, cfg.total_steps, cfg.lr_final_fraction)
         ro = otrain.train_step(ost, sphere64, batch=b, trace=tr)
@@ -330,15 +332,20 @@ def test_train_steps_match_oracle(sphere64, level_init):
             r_, m_ = sens_bar(sens, f"tables{lv}")
             assert_close(gt[lv], og.tables[lv], r_, f"grad tables level {lv} (step {step})", m_)
         pp = pst.params
-        for i in range(2):
-            assert_close(np_(pp.sdf_net.layers[i]), ost.params.sdf_net.layers[i], TOL, f"sdf{i}")
-        for i in range(3):
-            assert_close(np_(pp.color_net.layers[i]), ost.params.color_net.layers[i], TOL,
-                         f"color{i}")
+        # Adam's first steps move every entry by ~lr whatever |g| is: MLP parameters
+        # within 1e-3 relL2, per-entry steps by the assert_adam_tables bar
+        lr_m = cfg.lr_mlp * otrain.lr_factor(ost.step - 1, cfg.total_steps, cfg.lr_final_fraction)
+        for name, got, ref, prev in zip(["sdf0", "sdf1", "color0", "color1", "color2"],
+                                        list(pp.sdf_net.layers) + list(pp.color_net.layers),
+                                        list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers),
+                                        old_mlp):
+            assert rel_err(np_(got), ref) <= TOL, name
+            assert_adam_tables(np_(got), ref, prev, lr_m, name)
         assert_adam_tables(np_(pp.grid.tables), ost.params.grid.tables, old, lr)
         assert abs(pp.sharpness - ost.params.sharpness) <= 1e-6 * ost.params.sharpness
-        # keep the two runs on identical parameters so later steps stay comparable
-        pp.grid.tables.copy_(torch.from_numpy(ost.params.grid.tables))
+        # the next step starts from the oracle's parameters and moments again (Adam turns
+        # noise-floor gradient entries into opposite +-lr steps, which compound)
+        sync_product_from_oracle(pst, ost)
 
 
 def test_oracle_loop_on_gpu_kernels(sphere64, monkeypatch):
