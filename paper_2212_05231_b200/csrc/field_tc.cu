@@ -388,6 +388,8 @@ __device__ __forceinline__ void stage_blk(const Smem &s, uint32_t off, uint32_t 
     *reinterpret_cast<uint4 *>(s.p(off + part) + o) = l;
 }
 
+// hi part only (a tile that is stored for the backward's weight-gradient GEMMs and read
+// by no GEMM of its own kernel)
 // Common per-CTA setup of both MLP kernels: weight tiles, H2 row 0, barriers, TMEM.
 struct MlpShared {
     uint32_t tmem_base;
@@ -930,23 +932,27 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                  const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
                  Workspace ws, int want_xin) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // [0] chain MMAs, [1] weight-gradient MMAs, [2..5] DMA into TW, TZ, TC, TE
-    __shared__ uint64_t bars[6];
+    // [0] chain MMAs, [1] weight-gradient MMAs, [2..6] DMA into TW (A2c), TZ (A1c), TC (CIN),
+    // TE (E), TA1 (A1)
+    __shared__ uint64_t bars[7];
     __shared__ MlpShared sh;
     uint64_t *mbar = bars, *mbarw = bars + 1, *mb_w = bars + 2, *mb_z = bars + 3, *mb_c = bars + 4,
-             *mb_e = bars + 5;
+             *mb_e = bars + 5, *mb_a = bars + 6;
+    // the stored tiles arrive as fp16 hi parts only, so TW's second half holds A1: its
+    // DMA no longer waits for dC3 to release TW
+    constexpr uint32_t TA1 = TW + T64B;
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int qd = warp & 3, qt = warp >> 2;
     const int r = 32 * qd + lane;
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
-    mlp_setup<false>(S, f, sh, bars, 6);
+    mlp_setup<false>(S, f, sh, bars, 7);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0;
+    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0, ph_a = 0;
     PredScale PS{sh.slot_mx, sh.slot_pred, 1};
     const int P = *count;
     const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
@@ -1010,6 +1016,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         if (t0 * TILE < P) {
             if (t == kDmaThread) {
                 dma(TW, fwt(t0) + FW_A2C, T64B, mb_w);
+                dma(TA1, fwt(t0) + FW_A1, T64B, mb_a);
                 dma(TZ, fwt(t0) + FW_A1C, T64B, mb_z);
                 dma(TC, fwt(t0) + FW_CIN, TCB, mb_c);
                 dma(TE, ws.e_tiles + t0 * 2 * TEB, TEB, mb_e);  // E hi part (weight gradient)
@@ -1208,8 +1215,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), ID_KM(32), false);
                 umma::commit_elect(mbar);
-                // TW is free: dC3 (B0) completed before B1's chain GEMM did
-                if (lane == 0) dma(TW, fwt(tile) + FW_A1, T64B, mb_w);
+                // TW is free (dC3 of B0 completed before B1's chain GEMM did): next tile's A2c
+                if (lane == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, T64B, mb_w);
                 PWAIT(umma::mbar_wait(mb_c, ph_c));
                 WG_ACT_B<8>(tb + TB_DC1, S.MN(TX, T64B, 64), S.MN(TC, TCB, 32), ID_WG(32), acc);
             }
@@ -1273,10 +1280,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
                 umma::gemm3w<1>(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), ID_KM(64), false);
                 umma::commit_elect(mbar);
-                PWAIT(umma::mbar_wait(mb_w, ph_w));
-                WG_ACT_A<8>(tb + TB_DH2, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
+                PWAIT(umma::mbar_wait(mb_a, ph_a));
+                WG_ACT_A<8>(tb + TB_DH2, S.MN(TA1, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
             }
-            ph_w ^= 1u;
+            ph_a ^= 1u;
         }
         // While U = DLY H2 runs: mvec = [J q (features), q, 0] (field.py:326-327) -> MV (TZ)
         // and the ReLU mask M1 -> TY (exact in fp16: hi part only), both for B4's
@@ -1380,8 +1387,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         wait_mma(mbar, phase);
         PMARK(15);
         // ------------------------------------------------ B5: scatter inputs; next tile's DMAs
-        // TW is free (dH2 of B3 completed before B4's chain GEMM): next tile's A2c
-        if (t == kDmaThread && has_next) dma(TW, fwt(ntile) + FW_A2C, T64B, mb_w);
+        // TA1 is free (dH2 of B3 completed before B4's chain GEMM): next tile's A1
+        if (t == kDmaThread && has_next) dma(TA1, fwt(ntile) + FW_A1, T64B, mb_a);
         {
             // dL/dfeature pairs (DE) and q for the scatter kernel
             const float sde = pow2i(-(eU + eH1));
