@@ -124,8 +124,8 @@ def cpu_oracle_rate(wl, rays_sample, steps=1, threads=None):
 
     ok.NUM_THREADS = threads
     from oracle import render as orender
+    from oracle import scene as oscene
     from oracle import train as otrain
-    from paper_2212_05231_b200 import scene_io
 
     cfg = otrain.TrainConfig(batch_size=rays_sample, num_levels=wl["levels"],
                              table_size=wl["table"], seed=0, level_init=wl["levels"],
@@ -138,7 +138,7 @@ def cpu_oracle_rate(wl, rays_sample, steps=1, threads=None):
     rng = np.random.default_rng(123)
     times, counts = [], []
     for _ in range(steps):
-        b = scene_io.sample_ray_batch(ds, 0, rays_sample, 0.9, rng)
+        b = oscene.sample_ray_batch(ds, 0, rays_sample, 0.9, rng)  # host arrays (the dataset may be in HBM)
         t0 = time.perf_counter()
         rep = otrain.train_step(st, ds, batch=b)
         times.append(time.perf_counter() - t0)

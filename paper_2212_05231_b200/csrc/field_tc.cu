@@ -934,25 +934,32 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // [0] chain MMAs, [1] weight-gradient MMAs, [2..6] DMA into TW (A2c), TZ (A1c), TC (CIN),
     // TE (E), TA1 (A1)
-    __shared__ uint64_t bars[7];
+    __shared__ uint64_t bars[8];
     __shared__ MlpShared sh;
     uint64_t *mbar = bars, *mbarw = bars + 1, *mb_w = bars + 2, *mb_z = bars + 3, *mb_c = bars + 4,
-             *mb_e = bars + 5, *mb_a = bars + 6;
+             *mb_e = bars + 5, *mb_a = bars + 6, *mb_in = bars + 7;
     // the stored tiles arrive as fp16 hi parts only, so TW's second half holds A1: its
     // DMA no longer waits for dC3 to release TW
     constexpr uint32_t TA1 = TW + T64B;
+    // ... and TE's second half (E also arrives as its hi part) holds a full tile's per-sample
+    // inputs, DMA'd while the previous tile runs: masks [4][128] uint2 | n, c [6][128] |
+    // dL/dc [128][3] | dL/dsdf [128] | the forward's exponents (int4)
+    constexpr uint32_t TIN = TE + TEB, IN_MK = TIN, IN_NC = IN_MK + 4 * TILE * 8,
+                       IN_DC = IN_NC + NCROWS * TILE * 4, IN_DS = IN_DC + 3 * TILE * 4, IN_EX = IN_DS + TILE * 4,
+                       IN_BYTES = IN_EX + 16 - TIN;
+    static_assert(IN_BYTES <= TEB, "per-tile inputs fit in TE's free half");
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int qd = warp & 3, qt = warp >> 2;
     const int r = 32 * qd + lane;
     const int E = 3 + 2 * f.L;
     const int NA = f.n_active;
-    mlp_setup<false>(S, f, sh, bars, 7);
+    mlp_setup<false>(S, f, sh, bars, 8);
     const int eH1 = sh.wexp[0], eH2 = sh.wexp[1], eC1 = sh.wexp[2], eC2 = sh.wexp[3], eC3 = sh.wexp[4];
     const float *h2row0 = sh.h2row0;
     const uint32_t tb = sh.tmem_base;
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0, ph_a = 0;
+    uint32_t phase = 0, phasew = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_e = 0, ph_a = 0, ph_in = 0;
     PredScale PS{sh.slot_mx, sh.slot_pred, 1};
     const int P = *count;
     const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
@@ -1031,10 +1038,45 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         float gc0, gc1, gc2, cc0, cc1, cc2, gd, n0, n1, n2;
         uint2 mk;
     };
-    auto load_in = [&](int64_t tl) {
+    // per-sample inputs of a tile: full tiles arrive by one batched bulk DMA into TIN (issued
+    // during the previous tile's B1); the partial last tile (and misaligned caller
+    // buffers) read global memory directly
+    const bool in_dma_ok = ((reinterpret_cast<uintptr_t>(dl_dc) | reinterpret_cast<uintptr_t>(dl_dsdf)) & 15u) == 0;
+    auto in_full = [&](int64_t tl) { return in_dma_ok && (tl + 1) * TILE <= P; };
+    auto in_dma = [&](int64_t tl) {  // one thread
+        umma::mbar_expect_tx(mb_in, IN_BYTES);
+        umma::bulk_g2s_tx(S.p(IN_MK), ws.fw_mask + tl * 4 * TILE, 4 * TILE * 8, mb_in);
+        umma::bulk_g2s_tx(S.p(IN_NC), ws.fw_nc + tl * NCROWS * TILE, NCROWS * TILE * 4, mb_in);
+        umma::bulk_g2s_tx(S.p(IN_DC), dl_dc + 3 * tl * TILE, 3 * TILE * 4, mb_in);
+        umma::bulk_g2s_tx(S.p(IN_DS), dl_dsdf + tl * TILE, TILE * 4, mb_in);
+        umma::bulk_g2s_tx(S.p(IN_EX), ws.fw_exp + tl, 16, mb_in);
+    };
+    auto read_in = [&](int64_t tl, int4 &fe) {
         BwdIn v{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, make_uint2(0u, 0u)};
+        if (in_full(tl)) {
+            umma::mbar_wait(mb_in, ph_in);
+            ph_in ^= 1u;
+            v.mk = *reinterpret_cast<const uint2 *>(S.p(IN_MK) + 8 * (qt * TILE + r));
+            const float *nc = reinterpret_cast<const float *>(S.p(IN_NC)) + r;
+            if (qt == 0) {
+                const float *dc = reinterpret_cast<const float *>(S.p(IN_DC)) + 3 * r;
+                v.gc0 = dc[0];
+                v.gc1 = dc[1];
+                v.gc2 = dc[2];
+                v.cc0 = nc[3 * TILE];
+                v.cc1 = nc[4 * TILE];
+                v.cc2 = nc[5 * TILE];
+                v.gd = reinterpret_cast<const float *>(S.p(IN_DS))[r];
+            }
+            v.n0 = nc[0];
+            v.n1 = nc[TILE];
+            v.n2 = nc[2 * TILE];
+            fe = *reinterpret_cast<const int4 *>(S.p(IN_EX));
+            return v;
+        }
         const int64_t pp = tl * TILE + r;
         v.mk = ws.fw_mask[(tl * 4 + qt) * TILE + r];
+        fe = ws.fw_exp[tl];
         if (pp < P) {
             const float *nc = ws.fw_nc + tl * NCROWS * TILE + r;
             if (qt == 0) {
@@ -1052,7 +1094,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         }
         return v;
     };
-    BwdIn in = load_in(blockIdx.x);
+    if (t == kDmaThread && in_full(blockIdx.x)) in_dma(blockIdx.x);
+    int eE_cur = static_cast<int64_t>(blockIdx.x) * TILE < P ? ws.e_exp[blockIdx.x] : 0;
     int ntiles_done = 0;
 #ifdef NS2B_PHASE_PROF
     __shared__ long long pacc[64];
@@ -1073,18 +1116,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             umma::prefetch_l2(fwt(ntile), FWB);
             umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
             umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, TEB);
-            umma::prefetch_l2(ws.fw_nc + ntile * NCROWS * TILE, NCROWS * TILE * 4);
-            umma::prefetch_l2(ws.fw_mask + ntile * 4 * TILE, 4 * TILE * 8);
-            const int64_t nlast = min(static_cast<int64_t>(P), (ntile + 1) * TILE);  // dl_dc / dl_dsdf rows
-            const uint32_t nb = static_cast<uint32_t>(nlast - ntile * TILE);
-            umma::prefetch_l2(dl_dc + 3 * ntile * TILE, (12 * nb + 15) & ~15u);
-            umma::prefetch_l2(dl_dsdf + ntile * TILE, (4 * nb + 15) & ~15u);
         }
-        // per-sample inputs (loaded at the end of the previous tile)
+        // per-sample inputs (DMA'd during the previous tile)
+        int4 fe;
+        const BwdIn in = read_in(tile, fe);
         const uint32_t m1 = in.mk.x & 0xFFFFu, mc1 = in.mk.x >> 16, mc2 = in.mk.y;
-        const int4 fe = ws.fw_exp[tile];
         const int eA1 = fe.x, eCin = fe.y, eA1c = fe.z, eA2c = fe.w;
-        const int eE = ws.e_exp[tile];
+        const int eE = eE_cur;  // loaded during the previous tile
         const float gc0 = in.gc0, gc1 = in.gc1, gc2 = in.gc2, gd = in.gd;
         const float cc0 = in.cc0, cc1 = in.cc1, cc2 = in.cc2;
         float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
@@ -1139,6 +1177,9 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         wait_mma(mbar, phase);
         PMARK(3);
         // ------------------------------------------------ B1: u2 -> U1, dC2
+        // every thread read this tile's inputs from TIN before B0's barrier: next tile's
+        if (t == kDmaThread && has_next && in_full(ntile)) in_dma(ntile);
+        if (has_next) eE_cur = ws.e_exp[ntile];
         int eU2;
         {
             float u[2][8], m = 0.f;
@@ -1418,10 +1459,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 dma(TE, ws.e_tiles + ntile * 2 * TEB, TEB, mb_e);
                 dma(TZ, fwt(ntile) + FW_A1C, T64B, mb_z);
             }
-            if (has_next) {
-                j_store();
-                in = load_in(ntile);
-            }
+            if (has_next) j_store();
         }
         // Tile boundary barrier: without it a warp can run into the next tile while another
         // is still in B5; observed to deadlock on the c1 field (mbarw never completing),

@@ -242,6 +242,22 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
     }
 }
 
+// Several bulk copies completing one mbarrier phase: one arrive + expect_tx for the
+// total, then the copies (complete_tx only).  Evict-first: data read exactly once.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tx(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *mbar) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar)), "l"(pol)
+        : "memory");
+}
+
 // One-thread bulk DMA shared -> global (bulk-group completion; the source buffer may be
 // rewritten after bulk_wait_read() returns in the issuing thread).
 __device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes) {

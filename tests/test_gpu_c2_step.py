@@ -16,10 +16,9 @@ Two bars (`trainer.py:281-310`):
   the remaining rays see the same arithmetic; losses, P and every gradient tensor are
   then held to a flat 1e-3 (relL2 and max-abs / max|ref|), post-Adam MLP parameters to
   1e-3.  The achieved errors are ~1e-5 (profiles/r02_c2_step_parity.jsonl).
-* `test_c2_steps_chained`: three (lambda = 16) or two (lambda = 2) consecutive steps on
-  the FULL sub-batch (nothing dropped), the parameters and Adam moments re-synchronised
-  after each step, gradients held to max(1e-3, 5x the oracle's own sensitivity to a 1e-6
-  weight perturbation, max over 3 seeds; see `chained_bar`).
+* `test_c2_steps_chained`: three (lambda = 16) or two (lambda = 2) consecutive steps with
+  only the alpha-clamp-flip rays removed (ReLU ties kept), parameters and Adam moments
+  re-synchronised after each step: relL2 within a flat 1e-3, max-abs within 1e-2.
 
 Achieved errors are printed per tensor (pytest -s) and appended as JSON lines to
 $NS2B_PARITY_LOG when set (profiles/r02_c2_step_parity.jsonl).
@@ -47,7 +46,7 @@ from oracle import train as otrain  # noqa: E402
 from paper_2212_05231_b200 import scene_io as pscene  # noqa: E402
 from paper_2212_05231_b200 import trainer as ptrain  # noqa: E402
 from parity import max_err, rel_err  # noqa: E402
-from test_gpu_parity import assert_adam_tables, oracle_sensitivity  # noqa: E402
+from test_gpu_parity import assert_adam_tables  # noqa: E402
 
 TOL = 1e-3
 RAYS = 4096
@@ -189,52 +188,47 @@ def test_c2_steps_flat(request, grid, level_init, steps):
         assert abs(pp.sharpness - ost.params.sharpness) <= 1e-6 * ost.params.sharpness
 
 
-def chained_bar(sens, key):
-    """max(1e-3, 5x the oracle's distance from itself under a 1e-6 relative perturbation
-    of its MLP weights, max over 3 perturbation seeds).  On the full batch that distance
-    is made of a handful of discontinuity events (one or two alpha-clamp flips, ~100 ReLU
-    ties among ~370k samples) whose effect depends on which samples they hit, so a given
-    draw differs from the oracle's perturbed runs by up to ~4x their distance (measured:
-    level-4 table gradient, step 2).  This bar only bounds that noise; the flat test above
-    holds the same configuration to a fixed 1e-3 (achieved ~3e-5) with those rays removed."""
-    r, m = sens[key.replace("grad_", "")]
-    return max(TOL, 5 * r), max(TOL, 5 * m)
+MAX_TIE = 1e-2  # max-abs bar with ReLU ties kept (they move single entries by <= 3e-3)
 
 
 @pytest.mark.parametrize("level_init,steps", [(16, 3), (2, 2)])
 def test_c2_steps_chained(dtu, level_init, steps):
+    """Consecutive steps on the sub-batch with only the alpha-clamp-flip rays removed (the
+    O(s) discontinuity; typically 0-3 rays), ReLU ties kept: relL2 within a flat 1e-3 on
+    every gradient tensor, max-abs within 1e-2 (a tie flips one sample's mask and moves
+    the few fine-level entries it touches by up to 3e-3 of the level's max,
+    tools/diag_c2.py); post-Adam parameters by the Adam-aware bar; parameters and moments
+    re-synchronised after each step."""
     cfg, ost = c2_oracle_state(dtu, level_init)
     pst = product_state_from_oracle(ost)
     rng = np.random.default_rng(22)
+    from paper_2212_05231_b200 import renderer as prender
+
     for step in range(steps):
         b = oscene.sample_ray_batch(dtu, 0, RAYS, cfg.fg_fraction, rng)
-        sens = oracle_sensitivity(ost, dtu, b, seeds=(1, 2, 3))
+        level = otrain.level_schedule(ost.step, cfg)
+        _, orec = orender.render_rays(b, ost.params, ost.occ, level)
+        _, prec = prender.render_rays(b, pst.params, pst.occ, level)
+        flips = flip_rays(np_(prec.alphas_per_sample), orec)
+        assert flips.size <= max(4, 0.005 * RAYS), f"{flips.size} rays with alpha-clamp flips"
+        bk = subset(b, np.setdiff1d(np.arange(RAYS), flips))
         old = ost.params.grid.tables.astype(np.float64)
         old_mlp = [h.astype(np.float64) for h in list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers)]
         lr = cfg.lr_tables * otrain.lr_factor(ost.step, cfg.total_steps, cfg.lr_final_fraction)
         tr = {}
-        ro = otrain.train_step(ost, dtu, batch=b, trace=tr)
-        rp = ptrain.train_step(pst, dtu, batch=b)
+        ro = otrain.train_step(ost, dtu, batch=bk, trace=tr)
+        rp = ptrain.train_step(pst, dtu, batch=bk)
         assert rp.sample_count == ro.sample_count and rp.level == ro.level
-        rec = tr["records"]
-        a_gpu = np_(pst.ws.alphas[:rp.sample_count])[rec.interval_first]
-        flips = int(((a_gpu == 0) != (rec.alphas == 0)).sum())
-        assert flips <= max(2, 1e-4 * rec.alphas.size), f"{flips} alpha-clamp flips"
         errs = grad_errors(pst, tr["grads"], ro.level)
         record("c2_chained", step, errs, level=ro.level, samples=int(ro.sample_count),
-               alpha_clamp_flips=flips,
-               bars={k: chained_bar(sens, k) for k in errs})
+               alpha_flip_rays=int(flips.size), relu_tie_rays=int(relu_tie_rays(ost.params, orec).size))
         for k in ("color", "eikonal", "total", "psnr"):
             a, r = getattr(rp, k), getattr(ro, k)
             assert abs(a - r) <= TOL * max(abs(r), 1e-9), f"{k}: {a} vs {r}"
         assert abs(pst.last_dslog - tr["dl_dslog"]) <= TOL * abs(tr["dl_dslog"])
         for k, (r_, m_) in errs.items():
-            rb, mb = chained_bar(sens, k)
-            assert r_ <= rb and m_ <= mb, f"{k} step {step}: relL2 {r_:.2e} (bar {rb:.1e}), max {m_:.2e} ({mb:.1e})"
+            assert r_ <= TOL and m_ <= MAX_TIE, f"{k} step {step}: relL2 {r_:.2e}, max {m_:.2e}"
         pp = pst.params
-        # Adam's first steps move every entry by ~lr whatever |g| is, so an MLP entry whose
-        # gradient sits at the noise floor (or moves through a clamp flip) may step the
-        # other way: relL2 within 1e-3, per-entry steps by the assert_adam_tables bar
         lr_m = cfg.lr_mlp * otrain.lr_factor(ost.step - 1, cfg.total_steps, cfg.lr_final_fraction)
         for name, got, ref, prev in zip(
                 ["sdf0", "sdf1", "color0", "color1", "color2"],
@@ -243,8 +237,6 @@ def test_c2_steps_chained(dtu, level_init, steps):
             assert rel_err(np_(got), ref) <= TOL, f"{name}: relL2 {rel_err(np_(got), ref):.2e}"
             assert_adam_tables(np_(got), ref, prev, lr_m, name)
         assert_adam_tables(np_(pp.grid.tables), ost.params.grid.tables, old, lr)
-        # Adam turned the noise-floor gradient entries into opposite +-lr steps: start the
-        # next step from the oracle's parameters and moments again
         sync_product_from_oracle(pst, ost)
 
 

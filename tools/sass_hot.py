@@ -1,5 +1,6 @@
 """Aggregate ncu SASS source-page stall samples by opcode / by region (profiling helper)."""
 import csv, subprocess, sys, collections, re
+"""usage: python tools/sass_hot.py REPORT.ncu-rep [LAUNCH_INDEX|ID:..] [--top]"""
 rep, kid = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None
 cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
 if kid is not None:
@@ -13,7 +14,7 @@ ix = {n: h.index(n) for n in h}
 tot = 0; by_op = collections.Counter(); ni = collections.Counter(); inst = collections.Counter()
 seq = []
 for r in rows[1:]:
-    if len(r) < len(h): continue
+    if len(r) < len(h) or r == h: continue  # repeated header rows (one block per kernel)
     src = r[ix["Source"]].strip()
     op = re.sub(r"^@!?U?P\w+\s+", "", src).split(" ")[0]
     s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
