@@ -192,6 +192,13 @@ class DynamicConfig:
     lr_transform: float = 1e-3
     lr_transform_joint: float = 1e-4
     frame_lr_scale: float = 0.3   # field learning-rate scale while fine-tuning frames > 0
+    # The transform is fit to the photometric (colour) loss only.  The Eikonal term is a
+    # regulariser of the field, but as a function of the transform it rewards moving the
+    # samples to wherever |grad f| is closest to 1: on the translating sphere its 0.1-weighted
+    # variation over T_x in [-0.05, -0.035] (2.6e-4) exceeds the colour loss's (1.7e-4), and
+    # it pulls the estimate from the colour optimum at -0.050 to -0.035..-0.040
+    # (tools/dyn_scan.py, profiles/r02_dynamic_scan.jsonl).  True restores the full loss.
+    transform_eikonal: bool = False
 
     @classmethod
     def from_train_config(cls, cfg, **kw):
@@ -257,10 +264,12 @@ def _cotangents(state, batch, rendered, rec):
     return color, eik, mse, dl_dc, dl_dsdf, dslog, dl_dn.float()
 
 
-def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform, field_lr_scale=1.0):
+def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform, field_lr_scale=1.0,
+                 transform_eikonal=False):
     """One step of frame `frame` > 0: transform-only (joint=False: field frozen, only
     the input-gradient kernel runs) or joint (field backward + Adam as well, the field's
-    learning rates scaled by `field_lr_scale`)."""
+    learning rates scaled by `field_lr_scale`).  The transform's gradient comes from the
+    colour loss alone unless `transform_eikonal` (DynamicConfig.transform_eikonal)."""
     st = seq.train
     cfg, params = st.config, st.params
     level = trainer.level_schedule(st.step, cfg)
@@ -285,11 +294,15 @@ def dynamic_step(seq, dataset, frame, gt, opt, joint, lr_transform, field_lr_sca
             ws.grads[:lay.active_end(na)].zero_()
             sdf_g, col_g, tab_g = lay.views(ws.grads)
             grads = fieldmod.FieldGrads(tab_g, sdf_g, col_g, ws.grads)
-            fieldmod.field_backward(params, rec.cache, dl_dc, dl_dsdf, dl_dn, need_input_grads=True,
-                                    grads=grads)
-            dl_dx, dl_dv = grads.dl_dx, grads.dl_dv
+            fieldmod.field_backward(params, rec.cache, dl_dc, dl_dsdf, dl_dn,
+                                    need_input_grads=transform_eikonal, grads=grads)
+            if transform_eikonal:
+                dl_dx, dl_dv = grads.dl_dx, grads.dl_dv
+            else:  # the field's gradients include the Eikonal term, the transform's do not
+                dl_dx, dl_dv = field_input_grads(params, rec.cache, dl_dc, dl_dsdf, None)
         else:
-            dl_dx, dl_dv = field_input_grads(params, rec.cache, dl_dc, dl_dsdf, dl_dn)
+            dl_dx, dl_dv = field_input_grads(params, rec.cache, dl_dc, dl_dsdf,
+                                             dl_dn if transform_eikonal else None)
         opt.step(gt, ft.param_gradient(rec.frame_positions, v, dl_dx, dl_dv), lr_transform)
         if joint:
             ws.flag.zero_()
@@ -324,7 +337,8 @@ def train_frame(seq, dataset, frame, config=None, on_step=None):
         for k in range(dc.frame_steps):
             joint = k >= dc.transform_steps
             r = dynamic_step(seq, dataset, frame, gt, opt, joint,
-                             dc.lr_transform_joint if joint else dc.lr_transform, dc.frame_lr_scale)
+                             dc.lr_transform_joint if joint else dc.lr_transform, dc.frame_lr_scale,
+                             dc.transform_eikonal)
             reports.append(r)
             if on_step:
                 on_step(r)

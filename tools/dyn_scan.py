@@ -44,28 +44,18 @@ def main():
         out["scan"].append({"tx": round(float(tx), 4), "color": color, "eikonal": eik,
                             "total": color + cfg.eikonal_weight * eik})
     print(json.dumps(out))
-    # (b) transform-only trajectories
-    import copy
-
+    # (b) transform-only trajectories, with and without the Eikonal term in its gradient
     for use_eik in (True, False):
-        seq2 = copy.deepcopy(seq) if False else seq
         gt = dyn.GlobalTransform.identity()
         opt = dyn.TransformAdam()
         traj = []
-        orig = dyn._cotangents
-        if not use_eik:
-            def no_eik(state, b, r, rec, _o=orig):
-                c = _o(state, b, r, rec)
-                return c[:6] + (torch.zeros_like(c[6]),)
-            dyn._cotangents = no_eik
         st_step = st.step
         for k in range(400):
-            dyn.dynamic_step(seq2, ds, 1, gt, opt, False, 1e-3)
+            dyn.dynamic_step(seq, ds, 1, gt, opt, False, 1e-3, transform_eikonal=use_eik)
             if k % 50 == 49:
                 traj.append([round(float(v), 5) for v in gt.t])
-        dyn._cotangents = orig
         st.step = st_step
-        print(json.dumps({"eikonal_in_transform_grad": use_eik, "T_trajectory": traj}))
+        print(json.dumps({"eikonal_in_transform_grad": use_eik, "T_trajectory_every_50": traj}))
 
 
 if __name__ == "__main__":
