@@ -210,7 +210,8 @@ __device__ __forceinline__ float absmax(const float *v) {
 // (forward) a sixth tile holds H1' = diag(H2[0]) H1, so the j_d GEMM S1 H1 becomes
 // M1 H1' with the exact 0/1 ReLU mask M1 as its A operand.
 template <bool kH1S>
-__device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wmax, int *wexp) {
+__device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wmax, int *wexp,
+                                  uint32_t h1s_off = WH1S) {
     const int E = 3 + 2 * f.L;
     constexpr int NM = kH1S ? 6 : 5, NR = kH1S ? 288 : 224;
     auto fetch = [&](int r, int c) -> float {  // row r of the stacked [H1|H2|C1|C2|C3|H1'] tiles
@@ -247,7 +248,7 @@ __device__ void load_weight_tiles(const Smem &s, const FieldDev &f, uint32_t *wm
         else if (k == 2) stage<32>(s, WC1, WC1B, r - 80, row, e);
         else if (k == 3) stage<64>(s, WC2, WC2B, r - 144, row, e);
         else if (k == 4) stage<64>(s, WC3, WC3B, r - 208, row, e);
-        else stage<48>(s, WH1S, WH1B, r - 224, row, e);
+        else stage<48>(s, h1s_off, WH1B, r - 224, row, e);
     }
 }
 
@@ -822,6 +823,433 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tb, 512);
+}
+
+// ---------------------------------------------------------------------------
+// MLP forward, two tiles in flight (field_fwd2_kernel): the 512 threads form two
+// independent 256-thread groups, each running the forward above on its own tiles (the
+// CTA's even / odd tiles) with its own shared buffers, TMEM columns, mbarriers, named
+// barrier and MMA-issuing warp, so one group's epilogue overlaps the other's MMAs,
+// DMAs and barrier waits.  Per group:
+//   threads: warp w (0..7) reads TMEM lane quadrant w % 4 and owns column blocks
+//            4 (w / 4) .. 4 (w / 4) + 3 of every 64-wide row (32 columns);
+//   TMEM:    two 64-column chain slots (Z1 -> A, Y -> B, JD -> A, Zc1 -> A, Zc2 -> B);
+//   smem:    EB (24 KB): E (P0) -> M1 (P1) -> CIN (P2) -> A2c hi (P4, store only);
+//            AB (32 KB): A1 (P1) -> A1c (P3);  plus row-scalar exchange scratch.
+// d feature/dx (J) is read straight from global memory in P2 (prefetched to L2 a tile
+// ahead): it only enters the normal, so it needs neither registers a tile ahead nor TMEM.
+// Results equal field_fwd_kernel's up to the order of the per-row partial sums.
+constexpr uint32_t F2_H1S = TE;                       // H1' right after the weights
+constexpr uint32_t F2_G0 = F2_H1S + 2 * WH1B;         // group 0 buffers
+constexpr uint32_t F2_EB = 0, F2_AB = 2 * TEB, F2_XCH = F2_AB + 2 * T64B,  // offsets in a group block
+                   F2_LG = F2_XCH + 8 * TILE * 4, F2_MK = F2_LG + 6 * TILE * 4, F2_GB = F2_MK + 24 * TILE;
+constexpr uint32_t SMEM_FWD2 = F2_G0 + 2 * F2_GB;
+static_assert(SMEM_FWD2 <= 227 * 1024, "fwd2 shared memory");
+
+__device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(g + 1) : "memory"); }
+__device__ __forceinline__ void group_publish(int g) {
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    group_sync(g);
+    umma::fence_after_sync();
+}
+
+// PredScale for a 256-thread group (the leader thread owns the prediction slot)
+struct PredScaleG {
+    uint32_t (*mx)[NSLOT];
+    int *pred;
+    int par;
+    bool leader;
+    __device__ __forceinline__ int guess(int k) const { return pred[k]; }
+    __device__ __forceinline__ void contrib(int k, float m) {
+        const uint32_t w = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+        if ((threadIdx.x & 31) == 0 && w) atomicMax(&mx[par][k], w);
+    }
+    __device__ __forceinline__ bool check(int k, int &e) {
+        const float m = __uint_as_float(mx[par][k]);
+        const int ex = exp_for(m);
+        const bool ok = !(m > 0.f) || (e <= ex + 1 && e >= ex - NS2B_PRED_SLACK);
+        if (!ok) {
+            e = ex - 1;
+            if (leader) pred[k] = e;
+        }
+        return ok;
+    }
+};
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restrict__ sdf_out,
+                  float *__restrict__ col_out, float *__restrict__ nrm_out, float *__restrict__ geo_out,
+                  double *__restrict__ eik_sum, Workspace ws) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bars[4];  // [2g] chain MMAs, [2g+1] E-tile DMA
+    __shared__ uint32_t wmax[6];
+    __shared__ int wexp[6];
+    __shared__ float h2row0[H];
+    __shared__ float c3w[3][H];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ uint32_t gmx[2][2][NSLOT];
+    __shared__ int gpred[2][NSLOT];
+    const Smem S{smem_raw};
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int g = warp >> 3, gw = warp & 7, tg = t & 255;
+    const int qd = gw & 3, qh = gw >> 2;
+    const int r = 32 * qd + lane;
+    const int NA = f.n_active;
+    const int E = 3 + 2 * f.L;
+    // ---- setup (all 512 threads)
+    if (t < H) h2row0[t] = f.sdf_w[H * (E + 1) + t];
+    if (t < 3 * H) c3w[t / H][t % H] = f.color_w[H * CIN + H * H + t];
+    load_weight_tiles<true>(S, f, wmax, wexp, F2_H1S);
+    if (t < 2 * NSLOT) {
+        gmx[t / NSLOT][0][t % NSLOT] = 0u;
+        gmx[t / NSLOT][1][t % NSLOT] = 0u;
+        gpred[t / NSLOT][t % NSLOT] = 0;
+    }
+    if (t == 0) {
+        for (int i = 0; i < 4; ++i) umma::mbar_init(bars + i, 1);
+        umma::fence_barrier_init();
+    }
+    if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 256);
+    publish();
+    const int eH1 = wexp[0], eH2 = wexp[1], eC1 = wexp[2], eC2 = wexp[3], eH1s = wexp[5];
+    uint64_t *mbar = bars + 2 * g, *mbare = bars + 2 * g + 1;
+    const uint32_t gbase = F2_G0 + g * F2_GB;
+    const uint32_t EB = gbase + F2_EB, AB = gbase + F2_AB;
+    float *xch = reinterpret_cast<float *>(S.p(gbase + F2_XCH));  // [2][128] d | [2][3][128] normal
+    float *lgx = reinterpret_cast<float *>(S.p(gbase + F2_LG));   // [2][3][128] logit partials
+    uint8_t *mkx = S.p(gbase + F2_MK);                            // [3][8][128] mask bytes
+    const uint32_t tb = tmem_base_sh + g * 128;
+    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    const uint32_t SA = 0, SB = 64;
+    const bool io = (gw == 7 && lane == 0);  // stores, DMAs, prefetches of the group
+    PredScaleG PS{gmx[g], gpred[g], 1, tg == 0};
+    uint32_t phase = 0, phasee = 0;
+    const int P = *count;
+    const int64_t stride = 2 * static_cast<int64_t>(gridDim.x);
+    const int64_t t0 = blockIdx.x + static_cast<int64_t>(g) * gridDim.x;
+    float eik = 0.f;
+    if (io && t0 * TILE < P) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
+    int eE_cur = t0 * TILE < P ? ws.e_exp[t0] : 0;
+    for (int64_t tile = t0; tile * TILE < P; tile += stride) {
+        const int64_t p = tile * TILE + r;
+        const bool valid = p < P;
+        const int64_t ntile = tile + stride;
+        const bool has_next = ntile * TILE < P;
+        PS.par ^= 1;
+        if (io && has_next) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
+        const float *xvt = ws.xv + tile * XVROWS * TILE + r;
+        const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
+        const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
+        const int eE = eE_cur;
+        uint8_t *fwt = ws.fw_tiles + tile * static_cast<int64_t>(FWB);
+        float *SBt = ws.sb + tile * SBROWS * TILE;
+        float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
+        // ------------------------------------------------ P0: Z1 = E H1^T -> A
+        if (gw == 7) {
+            umma::mbar_wait(mbare, phasee);
+            umma::gemm3w<3>(tb + SA, S.K(EB, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
+            if (lane == 0) umma::bulk_wait_read_n<0>();  // the previous tile's A1c store has left AB
+            __syncwarp();
+            umma::commit_elect(mbar);
+        }
+        phasee ^= 1u;
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ P1: a1 -> AB, M1 -> EB; d
+        uint32_t m1 = 0u;  // my 32 hidden-unit bits (blocks 4qh..4qh+3)
+        int eA1;
+        float d_sdf;
+        {
+            float z[4][8], ma = 0.f, dpart = 0.f;
+            const float sc = pow2i(-(eE + eH1));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int b = 4 * qh + i;
+                umma::tmem_ld8(my + SA + 8 * b, z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    m1 |= on ? (1u << (8 * i + k)) : 0u;
+                    const float a = on ? z[i][k] * sc : 0.f;
+                    z[i][k] = a;
+                    ma = fmaxf(ma, a);
+                    dpart = fmaf(h2row0[8 * b + k], a, dpart);
+                }
+            }
+            xch[qh * TILE + r] = dpart;
+            eA1 = PS.guess(kA1);
+            PS.contrib(kA1, ma);
+            auto stg = [&](int e) {
+                const float sa = pow2i(e);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) stage_blk<64>(S, AB, T64B, r, 4 * qh + i, z[i], sa);
+            };
+            stg(eA1);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // M1 (exact in fp16: hi part only) into EB (E is dead)
+                const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
+                auto h2 = [&](int k) {
+                    return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
+                };
+                *reinterpret_cast<uint4 *>(S.p(EB) + umma::tile_off(r, 8 * (4 * qh + i), 64)) =
+                    make_uint4(h2(0), h2(2), h2(4), h2(6));
+            }
+            group_publish(g);
+            if (tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;
+            if (!PS.check(kA1, eA1)) {
+                stg(eA1);
+                group_publish(g);
+            }
+            d_sdf = xch[r] + xch[TILE + r];
+        }
+        if (gw == 7) {
+            umma::gemm3w<4>(tb + SB, S.K(AB, T64B, 64), S.K(WH2, WH2B, 64), ID_KK(16), false);
+            umma::gemm2a<4>(tb + SA, S.K(EB, T64B, 64), S.MN(F2_H1S, WH1B, 48), ID_KM(48), false);
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(AB), T64B);
+        }
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ P2: normal, cin -> EB; Zc1 -> A
+        int eCin;
+        {
+            float y[16];
+            umma::tmem_ld8(my + SB, *reinterpret_cast<float(*)[8]>(y));
+            umma::tmem_ld8(my + SB + 8, *reinterpret_cast<float(*)[8]>(y + 8));
+            const float scy = pow2i(-(eA1 + eH2));
+#pragma unroll
+            for (int o = 0; o < 16; ++o) y[o] *= scy;
+            y[0] = d_sdf;
+            const float scd = pow2i(-eH1s);
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+            if (qh == 0) {
+                float jx[4];
+                umma::tmem_ld4(my + SA + 32, jx);
+                p0 = jx[0] * scd;
+                p1 = jx[1] * scd;
+                p2 = jx[2] * scd;
+            }
+            const float *jt = ws.jac + tile * JROWS * TILE + r;
+#pragma unroll 2
+            for (int l = 8 * qh; l < min(NA, 8 * qh + 8); ++l) {
+                float d0, d1;
+                umma::tmem_ld2(my + SA + 2 * l, d0, d1);
+                d0 *= scd;
+                d1 *= scd;
+                const float *jr = jt + 6 * l * TILE;
+                const float j0 = __ldcs(jr), j1 = __ldcs(jr + TILE), j2 = __ldcs(jr + 2 * TILE);
+                const float j3 = __ldcs(jr + 3 * TILE), j4 = __ldcs(jr + 4 * TILE), j5 = __ldcs(jr + 5 * TILE);
+                __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
+                __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
+                p0 = fmaf(d0, j0, fmaf(d1, j3, p0));
+                p1 = fmaf(d0, j1, fmaf(d1, j4, p1));
+                p2 = fmaf(d0, j2, fmaf(d1, j5, p2));
+            }
+            float *xn = xch + 2 * TILE;  // [2][3][128]
+            xn[(3 * qh + 0) * TILE + r] = p0;
+            xn[(3 * qh + 1) * TILE + r] = p1;
+            xn[(3 * qh + 2) * TILE + r] = p2;
+            group_sync(g);
+            const float n0 = xn[r] + xn[3 * TILE + r];
+            const float n1 = xn[TILE + r] + xn[4 * TILE + r];
+            const float n2 = xn[2 * TILE + r] + xn[5 * TILE + r];
+            const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+            if (valid && qh == 0) eik += (nn - 1.f) * (nn - 1.f);
+            // cin = [x, n, v, y] (field.py:237-239): half 0 stages blocks 0, 1; half 1 blocks 2, 3
+            float blk[2][8];
+            if (qh == 0) {
+                blk[0][0] = x0; blk[0][1] = x1; blk[0][2] = x2; blk[0][3] = n0;
+                blk[0][4] = n1; blk[0][5] = n2; blk[0][6] = v0; blk[0][7] = v1;
+                blk[1][0] = v2;
+#pragma unroll
+                for (int k = 1; k < 8; ++k) blk[1][k] = y[k - 1];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) blk[0][k] = y[7 + k];
+                blk[1][0] = y[15];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) blk[1][k] = 0.f;
+            }
+            float mc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mc = fmaxf(mc, fmaxf(fabsf(blk[0][k]), fabsf(blk[1][k])));
+            eCin = PS.guess(kCin);
+            PS.contrib(kCin, mc);
+            auto stg = [&](int e) {
+                const float sc = pow2i(e);
+                stage_blk<32>(S, EB, TCB, r, 2 * qh, blk[0], sc);
+                stage_blk<32>(S, EB, TCB, r, 2 * qh + 1, blk[1], sc);
+            };
+            stg(eCin);  // EB: the JD GEMM (M1) completed
+            if (valid && qh == 0) {
+                sdf_out[p] = d_sdf;
+                nct[0] = n0;
+                nct[TILE] = n1;
+                nct[2 * TILE] = n2;
+                if (nrm_out) {
+                    nrm_out[3 * p] = n0;
+                    nrm_out[3 * p + 1] = n1;
+                    nrm_out[3 * p + 2] = n2;
+                }
+                if (geo_out)
+#pragma unroll
+                    for (int o = 1; o < 16; ++o) geo_out[15 * p + o - 1] = y[o];
+            }
+            group_publish(g);
+            if (!PS.check(kCin, eCin)) {
+                stg(eCin);
+                group_publish(g);
+            }
+        }
+        if (gw == 7) {
+            umma::gemm3w<2>(tb + SA, S.K(EB, TCB, 32), S.K(WC1, WC1B, 32), ID_KK(64), false);
+            if (lane == 0) umma::bulk_wait_read_n<0>();  // A1's store has left AB before P3 restages it
+            __syncwarp();
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(EB), TCB);
+        }
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ P3: a1c -> AB; Zc2 -> B
+        uint32_t mc1 = 0u, mc2 = 0u;
+        int eA1c, eA2c;
+        {
+            float z[4][8], m = 0.f;
+            const float sc = pow2i(-(eCin + eC1));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                umma::tmem_ld8(my + SA + 8 * (4 * qh + i), z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    mc1 |= on ? (1u << (8 * i + k)) : 0u;
+                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    m = fmaxf(m, z[i][k]);
+                }
+            }
+            eA1c = PS.guess(kA1c);
+            PS.contrib(kA1c, m);
+            auto stg = [&](int e) {
+                const float s = pow2i(e);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) stage_blk<64>(S, AB, T64B, r, 4 * qh + i, z[i], s);
+            };
+#pragma unroll 1
+            for (int pass = 0;; ++pass) {
+                stg(eA1c);
+                group_publish(g);
+                if (pass) break;
+                if (PS.check(kA1c, eA1c)) break;
+            }
+        }
+        if (gw == 7) {
+            umma::gemm3w<4>(tb + SB, S.K(AB, T64B, 64), S.K(WC2, WC2B, 64), ID_KK(64), false);
+            if (lane == 0) umma::bulk_wait_read_n<0>();  // CIN's store has left EB before P4 restages it
+            __syncwarp();
+            umma::commit_elect(mbar);
+            if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(AB), T64B);
+        }
+        wait_mma(mbar, phase);
+        // ------------------------------------------------ P4: a2c (hi, store only) -> EB; logits
+        {
+            float z[4][8], m = 0.f;
+            const float sc = pow2i(-(eA1c + eC2));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                umma::tmem_ld8(my + SB + 8 * (4 * qh + i), z[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool on = z[i][k] > 0.f;
+                    mc2 |= on ? (1u << (8 * i + k)) : 0u;
+                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    m = fmaxf(m, z[i][k]);
+                }
+            }
+            eA2c = PS.guess(kA2c);
+            PS.contrib(kA2c, m);
+            float lp0 = 0.f, lp1 = 0.f, lp2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int b = 4 * qh + i;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    lp0 = fmaf(c3w[0][8 * b + k], z[i][k], lp0);
+                    lp1 = fmaf(c3w[1][8 * b + k], z[i][k], lp1);
+                    lp2 = fmaf(c3w[2][8 * b + k], z[i][k], lp2);
+                }
+            }
+            lgx[(3 * qh + 0) * TILE + r] = lp0;
+            lgx[(3 * qh + 1) * TILE + r] = lp1;
+            lgx[(3 * qh + 2) * TILE + r] = lp2;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // mask bytes [m1 | mc1 | mc2][block][row]
+                const int b = 4 * qh + i;
+                mkx[(0 * 8 + b) * TILE + r] = static_cast<uint8_t>(m1 >> (8 * i));
+                mkx[(1 * 8 + b) * TILE + r] = static_cast<uint8_t>(mc1 >> (8 * i));
+                mkx[(2 * 8 + b) * TILE + r] = static_cast<uint8_t>(mc2 >> (8 * i));
+            }
+            auto stg = [&](int e) {  // hi part only: the backward's weight-gradient GEMMs read nothing else
+                const float s = pow2i(e);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 h = make_uint4(pack_half2(z[i][0] * s, z[i][1] * s), pack_half2(z[i][2] * s, z[i][3] * s),
+                                               pack_half2(z[i][4] * s, z[i][5] * s), pack_half2(z[i][6] * s, z[i][7] * s));
+                    *reinterpret_cast<uint4 *>(S.p(EB) + umma::tile_off(r, 8 * (4 * qh + i), 64)) = h;
+                }
+            };
+#pragma unroll 1
+            for (int pass = 0;; ++pass) {
+                stg(eA2c);
+                group_publish(g);
+                if (pass) break;
+                if (PS.check(kA2c, eA2c)) break;
+            }
+        }
+        if (io) {
+            umma::bulk_s2g(fwt + FW_A2C, S.p(EB), T64B);
+            ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
+            if (has_next) {  // next tile's E into EB once the A2c store has read it
+                umma::bulk_wait_read_n<0>();
+                umma::bulk_g2s(S.p(EB), ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mbare);
+            }
+        }
+        if (has_next) eE_cur = ws.e_exp[ntile];
+        // ------------------------------------------------ P5: colours, masks
+        if (qh == 0) {
+            const float l0 = lgx[r] + lgx[3 * TILE + r];
+            const float l1 = lgx[TILE + r] + lgx[4 * TILE + r];
+            const float l2 = lgx[2 * TILE + r] + lgx[5 * TILE + r];
+            const float cc0 = sigmoid_f(l0), cc1 = sigmoid_f(l1), cc2 = sigmoid_f(l2);
+            nct[3 * TILE] = cc0;
+            nct[4 * TILE] = cc1;
+            nct[5 * TILE] = cc2;
+            if (valid) {
+                col_out[3 * p] = cc0;
+                col_out[3 * p + 1] = cc1;
+                col_out[3 * p + 2] = cc2;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {  // the backward's layout: quarter q holds blocks q and q + 4
+            const int q = 2 * qh + j;
+            auto word = [&](int kind) {
+                return static_cast<uint32_t>(mkx[(kind * 8 + q) * TILE + r]) |
+                       (static_cast<uint32_t>(mkx[(kind * 8 + q + 4) * TILE + r]) << 8);
+            };
+            ws.fw_mask[(tile * 4 + q) * TILE + r] = make_uint2(word(0) | (word(1) << 16), word(2));
+        }
+    }
+    if (eik_sum) {
+        double v = warp_sum(static_cast<double>(eik));
+        if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
+    }
+    if (io) umma::bulk_wait_all();
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tmem_base_sh, 256);
 }
 
 // ---------------------------------------------------------------------------
@@ -1852,9 +2280,33 @@ static int ensure_tc_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(field_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_BWD));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(field_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SMEM_FWD2));
     if (e != cudaSuccess) return set_error(NS2B_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
     g_tc_attr = 1;
     return NS2B_OK;
+}
+
+// NS2B_FWD=1 selects the one-tile forward (field_fwd_kernel); the default is the
+// two-tiles-in-flight field_fwd2_kernel
+static bool use_fwd1() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NS2B_FWD");
+        v = (e && atoi(e) == 1) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, float *sdf, float *colors,
+                       float *normals, float *geo, double *eik_sum, const Workspace &ws, cudaStream_t st) {
+    if (use_fwd1())
+        field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD, st>>>(f, count, sdf, colors, normals,
+                                                                                     geo, eik_sum, ws);
+    else
+        field_fwd2_kernel<<<grid_for((ntiles + 1) / 2, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
+            f, count, sdf, colors, normals, geo, eik_sum, ws);
 }
 
 }  // namespace tc
@@ -1886,8 +2338,7 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
                                                                                          count, ws);
         return check_launch("field_gather");
     case 1:
-        tc::field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
-            f, count, sdf, colors, normals, geo, eik_sum, ws);
+        tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st);
         return check_launch("field_mlp_forward");
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
@@ -1916,8 +2367,7 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     tc::field_gather_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
                                                                                          count, ws);
     if ((rc = check_launch("field_gather"))) return rc;
-    tc::field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD, st>>>(
-            f, count, sdf, colors, normals, geo, eik_sum, ws);
+    tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st);
     return check_launch("field_forward_tc");
 }
 
