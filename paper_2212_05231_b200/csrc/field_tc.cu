@@ -931,16 +931,26 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     PredScaleG PS{gmx[g], gpred[g], 1, tg == 0};
     uint32_t phase = 0, phasee = 0;
     const int P = *count;
-    const int64_t stride = 2 * static_cast<int64_t>(gridDim.x);
-    const int64_t t0 = blockIdx.x + static_cast<int64_t>(g) * gridDim.x;
+    // The CTA's tiles are b, b + G, b + 2G, ... (the backward's order); group 0 takes the
+    // first half of that list, group 1 the second, so the staging exponents the backward
+    // reads change at most once per CTA (each group's predictions are sticky; alternating
+    // groups would make the backward fold its TMEM accumulators on every tile)
+    const int64_t G = gridDim.x;
+    const int64_t ntl_all = (static_cast<int64_t>(P) + TILE - 1) / TILE;
+    const int64_t ntl = blockIdx.x < ntl_all ? (ntl_all - blockIdx.x + G - 1) / G : 0;
+    const int64_t half = (ntl + 1) / 2;
+    const int64_t i_end = g == 0 ? half : ntl;
+    const int64_t stride = G;
+    const int64_t t0 = blockIdx.x + (g == 0 ? 0 : half) * G;
+    const int64_t t_end = blockIdx.x + i_end * G;  // exclusive
     float eik = 0.f;
-    if (io && t0 * TILE < P) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
-    int eE_cur = t0 * TILE < P ? ws.e_exp[t0] : 0;
-    for (int64_t tile = t0; tile * TILE < P; tile += stride) {
+    if (io && t0 < t_end) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
+    int eE_cur = t0 < t_end ? ws.e_exp[t0] : 0;
+    for (int64_t tile = t0; tile < t_end; tile += stride) {
         const int64_t p = tile * TILE + r;
         const bool valid = p < P;
         const int64_t ntile = tile + stride;
-        const bool has_next = ntile * TILE < P;
+        const bool has_next = ntile < t_end;
         PS.par ^= 1;
         if (io && has_next) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
         const float *xvt = ws.xv + tile * XVROWS * TILE + r;
@@ -1034,20 +1044,29 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 p2 = jx[2] * scd;
             }
             const float *jt = ws.jac + tile * JROWS * TILE + r;
-#pragma unroll 2
-            for (int l = 8 * qh; l < min(NA, 8 * qh + 8); ++l) {
-                float d0, d1;
-                umma::tmem_ld2(my + SA + 2 * l, d0, d1);
-                d0 *= scd;
-                d1 *= scd;
-                const float *jr = jt + 6 * l * TILE;
-                const float j0 = __ldcs(jr), j1 = __ldcs(jr + TILE), j2 = __ldcs(jr + 2 * TILE);
-                const float j3 = __ldcs(jr + 3 * TILE), j4 = __ldcs(jr + 4 * TILE), j5 = __ldcs(jr + 5 * TILE);
-                __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
-                __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
-                p0 = fmaf(d0, j0, fmaf(d1, j3, p0));
-                p1 = fmaf(d0, j1, fmaf(d1, j4, p1));
-                p2 = fmaf(d0, j2, fmaf(d1, j5, p2));
+#pragma unroll 1
+            for (int l0 = 8 * qh; l0 < min(NA, 8 * qh + 8); l0 += 4) {  // 4 levels per batch:
+                // one TMEM wait, then all 24 J loads in flight at once (L2-resident)
+                float jd[4][2], jv[4][6];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    umma::tmem_ld2(my + SA + 2 * (l0 + i), jd[i][0], jd[i][1]);
+                    const float *jr = jt + 6 * (l0 + i) * TILE;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) jv[i][k] = l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int l = l0 + i;
+                    if (l < NA) {
+                        const float d0 = jd[i][0] * scd, d1 = jd[i][1] * scd;
+                        __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
+                        __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
+                        p0 = fmaf(d0, jv[i][0], fmaf(d1, jv[i][3], p0));
+                        p1 = fmaf(d0, jv[i][1], fmaf(d1, jv[i][4], p1));
+                        p2 = fmaf(d0, jv[i][2], fmaf(d1, jv[i][5], p2));
+                    }
+                }
             }
             float *xn = xch + 2 * TILE;  // [2][3][128]
             xn[(3 * qh + 0) * TILE + r] = p0;
@@ -2305,7 +2324,7 @@ static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, 
         field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD, st>>>(f, count, sdf, colors, normals,
                                                                                      geo, eik_sum, ws);
     else
-        field_fwd2_kernel<<<grid_for((ntiles + 1) / 2, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
+        field_fwd2_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
             f, count, sdf, colors, normals, geo, eik_sum, ws);
 }
 

@@ -199,6 +199,9 @@ class DynamicConfig:
     # it pulls the estimate from the colour optimum at -0.050 to -0.035..-0.040
     # (tools/dyn_scan.py, profiles/r02_dynamic_scan.jsonl).  True restores the full loss.
     transform_eikonal: bool = False
+    # gt_i starts at identity (the SPEC's decision); True starts it at gt_{i-1} (a
+    # constant-velocity prior, for motions larger than lr_transform x transform_steps)
+    init_from_previous: bool = False
 
     @classmethod
     def from_train_config(cls, cfg, **kw):
@@ -332,7 +335,8 @@ def train_frame(seq, dataset, frame, config=None, on_step=None):
                 on_step(r)
         seq.transforms.append(GlobalTransform.identity())
     else:
-        gt = GlobalTransform.identity()
+        prev = seq.transforms[-1] if (dc.init_from_previous and seq.transforms) else None
+        gt = GlobalTransform(prev.w.copy(), prev.t.copy()) if prev is not None else GlobalTransform.identity()
         opt = TransformAdam(seq.train.config.adam_beta1, seq.train.config.adam_beta2, seq.train.config.adam_eps)
         for k in range(dc.frame_steps):
             joint = k >= dc.transform_steps

@@ -245,54 +245,17 @@ def assert_adam_tables(p_new, p_ref, p_old, lr, name="tables", frac_bar=5e-3):
     assert frac <= frac_bar, f"{name}: {bad.sum()} of {touched.sum()} touched entries differ"
 
 
-def oracle_sensitivity(ost, ds, batch, eps=1e-6, seeds=(1, 2, 3)):
-    """Per-tensor (relL2, max) distance between the oracle's step gradients and the
-    same step with its MLP weights perturbed by `eps` relative (max over a few
-    perturbation seeds).  The training step is discontinuous (the alpha clamp at 0
-    passes zero gradient but dalpha/df is O(s) just above it; ReLU masks flip), so
-    this measured self-sensitivity is the parity bar for multi-step gradient
-    comparisons.  eps = 1e-6 matches the measured deviation of the tensor-core
-    forward's SDF from the oracle (~1e-6 relL2, tools/diag_fwd.py): the bar asks the
-    GPU step to be as close to the oracle as the oracle is to itself under a
-    perturbation of that size."""
-    import copy
-
-    from parity import max_err, rel_err
-
-    a = copy.deepcopy(ost)
-    ta = {}
-    otrain.train_step(a, ds, batch=batch, trace=ta)
-    ga = ta["grads"]
-    out = {}
-    for seed in seeds:
-        b = copy.deepcopy(ost)
-        r = np.random.default_rng(seed)
-        for h in b.params.sdf_net.layers + b.params.color_net.layers:
-            h *= (1 + eps * r.standard_normal(h.shape)).astype(np.float32)
-        tb = {}
-        otrain.train_step(b, ds, batch=batch, trace=tb)
-        gb = tb["grads"]
-        pairs = [(f"tables{lv}", gb.tables[lv], ga.tables[lv]) for lv in range(ga.tables.shape[0])]
-        pairs += [(f"sdf{i}", x, y) for i, (x, y) in enumerate(zip(gb.sdf_layers, ga.sdf_layers))]
-        pairs += [(f"color{i}", x, y) for i, (x, y) in enumerate(zip(gb.color_layers, ga.color_layers))]
-        for k, x, y in pairs:
-            r_, m_ = rel_err(x, y), max_err(x, y)
-            o = out.get(k, (0.0, 0.0))
-            out[k] = (max(o[0], r_), max(o[1], m_))
-    return out
-
-
-def sens_bar(sens, key):
-    r, m = sens[key]
-    return max(TOL, 2 * r), max(TOL, 2 * m)
-
-
 @pytest.mark.parametrize("level_init", [2, 8])
 def test_train_steps_match_oracle(sphere64, level_init):
     """Three full steps on the same ray batches, each from the oracle's parameters and
-    moments: sample counts exact; losses and all gradients within max(1e-3, 2x the
-    oracle's self-sensitivity); MLP parameters within 1e-3 relL2 and, like the tables,
-    per entry by assert_adam_tables."""
+    moments, with the (0-5) rays whose alpha-clamp set differs between the two sides
+    removed (the O(s) discontinuity, tests/test_oracle_conditioning.py; ReLU ties are
+    kept): sample counts exact; losses within 1e-3; every gradient tensor within 1e-3
+    relL2 and 1e-2 max-abs / max|ref| (a ReLU tie moves the few entries one sample
+    touches, tools/diag_c2.py); MLP parameters within 1e-3 relL2 and, like the tables, per
+    entry by assert_adam_tables."""
+    from test_gpu_c2_step import flip_rays, subset
+
     cfg = otrain.TrainConfig(batch_size=2048, num_levels=8, table_size=2**14, seed=0,
                              level_init=level_init)
     ost = otrain.TrainState.create(cfg)
@@ -302,7 +265,12 @@ def test_train_steps_match_oracle(sphere64, level_init):
     rng = np.random.default_rng(5)
     for step in range(3):
         b = oscene.sample_ray_batch(sphere64, 0, cfg.batch_size, cfg.fg_fraction, rng)
-        sens = oracle_sensitivity(ost, sphere64, b)
+        level = otrain.level_schedule(ost.step, cfg)
+        _, orec = orender.render_rays(b, ost.params, ost.occ, level)
+        _, prec = prender.render_rays(b, pst.params, pst.occ, level)
+        flips = flip_rays(np_(prec.alphas_per_sample), orec)
+        assert flips.size <= max(4, 0.005 * cfg.batch_size), f"{flips.size} rays with alpha-clamp flips"
+        b = subset(b, np.setdiff1d(np.arange(cfg.batch_size), flips))
         old = ost.params.grid.tables.astype(np.float64)
         old_mlp = [h.astype(np.float64) for h in list(ost.params.sdf_net.layers) + list(ost.params.color_net.layers)]
         tr = {}
@@ -311,10 +279,6 @@ def test_train_steps_match_oracle(sphere64, level_init):
         rp = ptrain.train_step(pst, sphere64, batch=b)
         assert rp.sample_count == ro.sample_count
         assert rp.level == ro.level
-        rec = tr["records"]
-        a_gpu = np_(pst.ws.alphas[:rp.sample_count])[rec.interval_first]
-        flips = int(((a_gpu == 0) != (rec.alphas == 0)).sum())
-        assert flips <= max(2, 1e-4 * rec.alphas.size), f"{flips} alpha-clamp flips"
         for k in ("color", "eikonal", "total", "psnr"):
             a, r = getattr(rp, k), getattr(ro, k)
             assert abs(a - r) <= TOL * max(abs(r), 1e-9), f"{k}: {a} vs {r}"
@@ -322,15 +286,12 @@ def test_train_steps_match_oracle(sphere64, level_init):
         sdf_g, col_g, tab_g = pst.params.layout.views(pst.ws.grads)
         og = tr["grads"]
         for i in range(2):
-            r_, m_ = sens_bar(sens, f"sdf{i}")
-            assert_close(np_(sdf_g[i]), og.sdf_layers[i], r_, f"grad sdf{i}", m_)
+            assert_close(np_(sdf_g[i]), og.sdf_layers[i], TOL, f"grad sdf{i}", 1e-2)
         for i in range(3):
-            r_, m_ = sens_bar(sens, f"color{i}")
-            assert_close(np_(col_g[i]), og.color_layers[i], r_, f"grad color{i}", m_)
+            assert_close(np_(col_g[i]), og.color_layers[i], TOL, f"grad color{i}", 1e-2)
         gt = np_(tab_g)
         for lv in range(ro.level):
-            r_, m_ = sens_bar(sens, f"tables{lv}")
-            assert_close(gt[lv], og.tables[lv], r_, f"grad tables level {lv} (step {step})", m_)
+            assert_close(gt[lv], og.tables[lv], TOL, f"grad tables level {lv} (step {step})", 1e-2)
         pp = pst.params
         # Adam's first steps move every entry by ~lr whatever |g| is: MLP parameters
         # within 1e-3 relL2, per-entry steps by the assert_adam_tables bar

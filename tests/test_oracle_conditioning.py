@@ -6,9 +6,10 @@ with raw alpha ~ 0 (SDF nearly flat along the ray) therefore switch between a ze
 an O(s) gradient under a 1-ulp change of the SDF.  Perturbing the oracle's own MLP
 weights by 1e-7 relative moves dL/dsdf by several % relL2 and table gradients by up to
 ~3e-2 relL2 / ~0.3 max-abs, while a 1e-8 perturbation (below fp32 resolution) moves
-them by ~1e-7.  Multi-step GPU-vs-oracle gradient checks therefore use the measured
-self-sensitivity as their bar (tests/test_gpu_parity.py::oracle_sensitivity); single
-field passes are held to 1e-3.  CPU only."""
+them by ~1e-7.  The GPU-vs-oracle step checks therefore remove the rays whose clamp set
+differs between the two sides before comparing (tests/test_gpu_c2_step.py::flip_rays),
+and the flat 1e-3 variant also the rays with near-tie ReLU pre-activations; single field
+passes are held to 1e-3.  CPU only."""
 
 import numpy as np
 

@@ -55,6 +55,9 @@ def main():
     ap.add_argument("--frame-steps", type=int, default=1100)
     ap.add_argument("--lr-joint", type=float, default=1e-4, help="transform lr in the joint phase")
     ap.add_argument("--frame-lr-scale", type=float, default=0.3, help="field lr scale for frames > 0")
+    ap.add_argument("--lr-transform", type=float, default=1e-3, help="transform lr, transform-only phase")
+    ap.add_argument("--init-from-previous", action="store_true",
+                    help="start gt_i at gt_{i-1} (constant-velocity prior) instead of identity")
     ap.add_argument("--transform-eikonal", action="store_true",
                     help="include the Eikonal term in the transform's gradient (off: colour loss only)")
     a = ap.parse_args()
@@ -66,7 +69,8 @@ def main():
                               max_resolution=128, init_radius=0.25, total_steps=2 * a.frame0_steps)
     dc = dyn.DynamicConfig(first_frame_steps=a.frame0_steps, transform_steps=a.transform_steps,
                            frame_steps=a.frame_steps, lr_transform_joint=a.lr_joint,
-                           frame_lr_scale=a.frame_lr_scale, transform_eikonal=a.transform_eikonal)
+                           frame_lr_scale=a.frame_lr_scale, transform_eikonal=a.transform_eikonal,
+                           lr_transform=a.lr_transform, init_from_previous=a.init_from_previous)
     seq = dyn.SequenceState(trainer.TrainState.create(cfg, aabb=ds.scene_aabb))
     rows = []
     for i in range(a.frames):
@@ -103,7 +107,8 @@ def main():
         "psnr_frame0": rows[0]["psnr_heldout"], "min_psnr": min(r["psnr_heldout"] for r in rows),
         "chain_identity_max_err": chain_err, "steps_per_frame": a.frame_steps,
         "transform_steps": a.transform_steps, "lr_joint": a.lr_joint, "frame_lr_scale": a.frame_lr_scale,
-        "views": a.views, "transform_eikonal": a.transform_eikonal,
+        "views": a.views, "transform_eikonal": a.transform_eikonal, "lr_transform": a.lr_transform,
+        "init_from_previous": a.init_from_previous,
         "mean_frame_seconds": float(np.mean([r["seconds"] for r in rows[1:]])) if a.frames > 1 else None}}))
 
 
