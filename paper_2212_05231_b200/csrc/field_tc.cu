@@ -834,8 +834,9 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 //   threads: warp w (0..7) reads TMEM lane quadrant w % 4 and owns column blocks
 //            4 (w / 4) .. 4 (w / 4) + 3 of every 64-wide row (32 columns);
 //   TMEM:    two 64-column chain slots (Z1 -> A, Y -> B, JD -> A, Zc1 -> A, Zc2 -> B);
-//   smem:    EB (24 KB): E (P0) -> M1 (P1) -> CIN (P2) -> A2c hi (P4, store only);
-//            AB (32 KB): A1 (P1) -> A1c (P3);  plus row-scalar exchange scratch.
+//   smem:    EB (24 KB): E (P0) -> M1 (P1) -> CIN (P2) -> the next tile's E (DMA'd in P3);
+//            AB (32 KB): A1 (P1) -> A1c (P3) -> A2c hi (P4, store only);  plus row-scalar
+//            exchange scratch.
 // d feature/dx (J) is read straight from global memory in P2 (prefetched to L2 a tile
 // ahead): it only enters the normal, so it needs neither registers a tile ahead nor TMEM.
 // Results equal field_fwd_kernel's up to the order of the per-row partial sums.
@@ -944,6 +945,12 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     const int64_t t0 = blockIdx.x + (g == 0 ? 0 : half) * G;
     const int64_t t_end = blockIdx.x + i_end * G;  // exclusive
     float eik = 0.f;
+#ifdef NS2B_PHASE_PROF
+    __shared__ long long pacc[64];
+    long long plast = clock64();
+    if (t < 64) pacc[t] = 0;
+    __syncthreads();
+#endif
     if (io && t0 < t_end) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
     int eE_cur = t0 < t_end ? ws.e_exp[t0] : 0;
     for (int64_t tile = t0; tile < t_end; tile += stride) {
@@ -970,6 +977,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         }
         phasee ^= 1u;
         wait_mma(mbar, phase);
+        PMARK(1);
         // ------------------------------------------------ P1: a1 -> AB, M1 -> EB; d
         uint32_t m1 = 0u;  // my 32 hidden-unit bits (blocks 4qh..4qh+3)
         int eA1;
@@ -1010,6 +1018,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                     make_uint4(h2(0), h2(2), h2(4), h2(6));
             }
             group_publish(g);
+            PMARK(2);
             if (tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;
             if (!PS.check(kA1, eA1)) {
                 stg(eA1);
@@ -1023,7 +1032,16 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_A1, S.p(AB), T64B);
         }
+        // the first 4 levels of this thread's d feature/dx: their L2 latency hides under the
+        // Y / JD GEMMs
+        const float *jt = ws.jac + tile * JROWS * TILE + r;
+        float jv0[4][6];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) jv0[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
         wait_mma(mbar, phase);
+        PMARK(4);
         // ------------------------------------------------ P2: normal, cin -> EB; Zc1 -> A
         int eCin;
         {
@@ -1043,17 +1061,19 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 p1 = jx[1] * scd;
                 p2 = jx[2] * scd;
             }
-            const float *jt = ws.jac + tile * JROWS * TILE + r;
 #pragma unroll 1
             for (int l0 = 8 * qh; l0 < min(NA, 8 * qh + 8); l0 += 4) {  // 4 levels per batch:
-                // one TMEM wait, then all 24 J loads in flight at once (L2-resident)
+                // the first batch was loaded during P1's GEMMs; the second's 24 loads go out
+                // together (L2-resident)
                 float jd[4][2], jv[4][6];
+                const bool first = l0 == 8 * qh;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     umma::tmem_ld2(my + SA + 2 * (l0 + i), jd[i][0], jd[i][1]);
                     const float *jr = jt + 6 * (l0 + i) * TILE;
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) jv[i][k] = l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f;
+                    for (int k = 0; k < 6; ++k)
+                        jv[i][k] = first ? jv0[i][k] : (l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f);
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -1072,7 +1092,9 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             xn[(3 * qh + 0) * TILE + r] = p0;
             xn[(3 * qh + 1) * TILE + r] = p1;
             xn[(3 * qh + 2) * TILE + r] = p2;
+            PMARK(5);
             group_sync(g);
+            PMARK(6);
             const float n0 = xn[r] + xn[3 * TILE + r];
             const float n1 = xn[TILE + r] + xn[4 * TILE + r];
             const float n2 = xn[2 * TILE + r] + xn[5 * TILE + r];
@@ -1131,7 +1153,9 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             umma::commit_elect(mbar);
             if (lane == 0) umma::bulk_s2g(fwt + FW_CIN, S.p(EB), TCB);
         }
+        PMARK(7);
         wait_mma(mbar, phase);
+        PMARK(8);
         // ------------------------------------------------ P3: a1c -> AB; Zc2 -> B
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
@@ -1166,12 +1190,19 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         }
         if (gw == 7) {
             umma::gemm3w<4>(tb + SB, S.K(AB, T64B, 64), S.K(WC2, WC2B, 64), ID_KK(64), false);
-            if (lane == 0) umma::bulk_wait_read_n<0>();  // CIN's store has left EB before P4 restages it
+            if (lane == 0) {
+                // A1c's store reads AB alongside the Zc2 GEMM; once it and CIN's store (EB) have
+                // read their tiles, P4 may stage A2c into AB and EB can take the next E
+                umma::bulk_s2g(fwt + FW_A1C, S.p(AB), T64B);
+                umma::bulk_wait_read_n<0>();
+                if (has_next) umma::bulk_g2s(S.p(EB), ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mbare);
+            }
             __syncwarp();
             umma::commit_elect(mbar);
-            if (lane == 0) umma::bulk_s2g(fwt + FW_A1C, S.p(AB), T64B);
         }
+        PMARK(9);
         wait_mma(mbar, phase);
+        PMARK(10);
         // ------------------------------------------------ P4: a2c (hi, store only) -> EB; logits
         {
             float z[4][8], m = 0.f;
@@ -1216,7 +1247,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 for (int i = 0; i < 4; ++i) {
                     const uint4 h = make_uint4(pack_half2(z[i][0] * s, z[i][1] * s), pack_half2(z[i][2] * s, z[i][3] * s),
                                                pack_half2(z[i][4] * s, z[i][5] * s), pack_half2(z[i][6] * s, z[i][7] * s));
-                    *reinterpret_cast<uint4 *>(S.p(EB) + umma::tile_off(r, 8 * (4 * qh + i), 64)) = h;
+                    *reinterpret_cast<uint4 *>(S.p(AB) + umma::tile_off(r, 8 * (4 * qh + i), 64)) = h;
                 }
             };
 #pragma unroll 1
@@ -1228,14 +1259,11 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             }
         }
         if (io) {
-            umma::bulk_s2g(fwt + FW_A2C, S.p(EB), T64B);
+            umma::bulk_s2g(fwt + FW_A2C, S.p(AB), T64B);  // (P0 waits for it before P1 restages AB)
             ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
-            if (has_next) {  // next tile's E into EB once the A2c store has read it
-                umma::bulk_wait_read_n<0>();
-                umma::bulk_g2s(S.p(EB), ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mbare);
-            }
         }
         if (has_next) eE_cur = ws.e_exp[ntile];
+        PMARK(11);
         // ------------------------------------------------ P5: colours, masks
         if (qh == 0) {
             const float l0 = lgx[r] + lgx[3 * TILE + r];
@@ -1260,7 +1288,17 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             };
             ws.fw_mask[(tile * 4 + q) * TILE + r] = make_uint2(word(0) | (word(1) << 16), word(2));
         }
+        PMARK(12);
     }
+#ifdef NS2B_PHASE_PROF
+    __syncthreads();
+    if (blockIdx.x == 0 && t == 0) {
+        printf("PHASEPROF fwd2");
+        for (int i = 0; i < 64; ++i)
+            if (pacc[i]) printf(" %d:%lld", i, pacc[i]);
+        printf("\n");
+    }
+#endif
     if (eik_sum) {
         double v = warp_sum(static_cast<double>(eik));
         if (lane == 0 && v != 0.0) atomicAdd(eik_sum, v);
