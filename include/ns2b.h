@@ -177,6 +177,18 @@ NS2B_API int ns2b_field_mlp_forward(const ns2b_field_t *field, const float *pos3
                                     const int32_t *count, int64_t capacity, float *sdf,
                                     float *colors, float *normals, float *geo, double *eik_sum,
                                     void *workspace, void *stream);
+/* ns2b_field_mlp_forward with the training step's Eikonal cotangent fused
+ * (trainer.py:229-235: eik_weight 2 (|n| - 1) / max(|n|, 1e-12) n / *eik_count, fp32 in
+ * numpy's order) where the normal is computed; the workspace then carries it in place of
+ * the normal and ns2b_field_mlp_backward uses it instead of recomputing (its own
+ * eik_weight / eik_count are then ignored).  The one-tile forward (NS2B_FWD=1) does not
+ * fuse and the backward computes the term itself; the result is the same. */
+NS2B_API int ns2b_field_mlp_forward_eik(const ns2b_field_t *field, const float *pos32,
+                                        const int32_t *ray_ids, const double *dirs,
+                                        const int32_t *count, int64_t capacity, float *sdf,
+                                        float *colors, float *normals, float *geo, double *eik_sum,
+                                        double eik_weight, const int64_t *eik_count,
+                                        void *workspace, void *stream);
 NS2B_API int ns2b_field_mlp_backward(const ns2b_field_t *field, const float *pos32,
                                      const int32_t *ray_ids, const double *dirs,
                                      const int32_t *count, int64_t capacity, const float *dl_dc,

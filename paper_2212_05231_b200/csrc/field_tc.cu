@@ -299,6 +299,7 @@ struct Workspace {
     uint2 *fw_mask;
     float *fw_nc;
     float *xin;
+    int *flags;  // [0]: 1 when the forward stored the Eikonal cotangent (not n) in fw_nc rows 0-2
 };
 __host__ __device__ inline size_t ws_tile_bytes() {
     return 2 * static_cast<size_t>(TEB) + FWB + sizeof(int4) + sizeof(int) + 4 * TILE * sizeof(uint2) +
@@ -326,6 +327,7 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     w.xin = reinterpret_cast<float *>(b);
     b += ntiles * XINROWS * TILE * sizeof(float);
     w.e_exp = reinterpret_cast<int *>(b);
+    w.flags = w.e_exp + ntiles;  // in the workspace's 256-byte tail
     return w;
 }
 
@@ -432,6 +434,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restrict__ sdf_out,
                  float *__restrict__ col_out, float *__restrict__ nrm_out, float *__restrict__ geo_out,
                  double *__restrict__ eik_sum, Workspace ws) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ws.flags[0] = 0;  // fw_nc rows 0-2 hold the normal
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[2];  // [0] chain MMAs, [1] E-tile DMA
     __shared__ MlpShared sh;
@@ -886,7 +889,12 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restrict__ sdf_out,
                   float *__restrict__ col_out, float *__restrict__ nrm_out, float *__restrict__ geo_out,
-                  double *__restrict__ eik_sum, Workspace ws) {
+                  double *__restrict__ eik_sum, Workspace ws, float eik_w, const int64_t *__restrict__ eik_count) {
+    // with eik_count the Eikonal cotangent (trainer.py:229-235) is fused here, where the
+    // normal is computed, and stored in place of the normal for the backward
+    const bool fuse_eik = eik_count != nullptr;
+    const float Pf = fuse_eik ? static_cast<float>(*eik_count) : 1.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ws.flags[0] = fuse_eik ? 1 : 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[4];  // [2g] chain MMAs, [2g+1] E-tile DMA
     __shared__ uint32_t wmax[6];
@@ -1128,9 +1136,16 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             stg(eCin);  // EB: the JD GEMM (M1) completed
             if (valid && qh == 0) {
                 sdf_out[p] = d_sdf;
-                nct[0] = n0;
-                nct[TILE] = n1;
-                nct[2 * TILE] = n2;
+                if (fuse_eik) {  // trainer.py:229-235 (fp32, numpy's order): dL/dn of the Eikonal term
+                    const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
+                    nct[0] = coef * n0 / Pf;
+                    nct[TILE] = coef * n1 / Pf;
+                    nct[2 * TILE] = coef * n2 / Pf;
+                } else {
+                    nct[0] = n0;
+                    nct[TILE] = n1;
+                    nct[2 * TILE] = n2;
+                }
                 if (nrm_out) {
                     nrm_out[3 * p] = n0;
                     nrm_out[3 * p + 1] = n1;
@@ -1448,6 +1463,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     PredScale PS{sh.slot_mx, sh.slot_pred, 1};
     const int P = *count;
     const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
+    // the forward may already have turned the normal rows into the Eikonal cotangent
+    const bool gn_fused = ws.flags[0] != 0;
     const int jrow = 16 * qd + lane;  // weight row (lanes 0..15) of the M=64 accumulators
     const int b0 = qt, b1 = qt + 4;
     const int nsdf = H * (E + 1) + NOUT * H;
@@ -1605,6 +1622,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         // per-sample inputs (DMA'd during the previous tile)
         int4 fe;
         const BwdIn in = read_in(tile, fe);
+        PMARK(19);
         const uint32_t m1 = in.mk.x & 0xFFFFu, mc1 = in.mk.x >> 16, mc2 = in.mk.y;
         const int eA1 = fe.x, eCin = fe.y, eA1c = fe.z, eA2c = fe.w;
         const int eE = eE_cur;  // loaded during the previous tile
@@ -1618,7 +1636,11 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 gn1 = dl_dn_extra[3 * p + 1];
                 gn2 = dl_dn_extra[3 * p + 2];
             }
-            if (eik_w != 0.f) {  // trainer.py:229-235 (fp32, numpy's order)
+            if (gn_fused) {  // fused by the forward (same arithmetic)
+                gn0 += n0;
+                gn1 += n1;
+                gn2 += n2;
+            } else if (eik_w != 0.f) {  // trainer.py:229-235 (fp32, numpy's order)
                 const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
                 const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
                 gn0 += coef * n0 / Pf;
@@ -1639,6 +1661,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             }
             eD = PS.guess(kDlog);
             PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
+            PMARK(20);
             #pragma unroll 1
             for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
                 if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
@@ -1945,11 +1968,13 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 dma(TZ, fwt(ntile) + FW_A1C, T64B, mb_z);
             }
             if (has_next) j_store();
+            PMARK(17);
         }
         // Tile boundary barrier: without it a warp can run into the next tile while another
         // is still in B5; observed to deadlock on the c1 field (mbarw never completing),
         // so warps leave the tile together.
         publish();
+        PMARK(18);
         if (++ntiles_done == kFoldTiles) {  // bound the TMEM accumulation run (all MMAs done)
             ntiles_done = 0;
 #pragma unroll  // compile-time j: acc_e / acc_live stay in registers
@@ -2357,13 +2382,14 @@ static bool use_fwd1() {
 }
 
 static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, float *sdf, float *colors,
-                       float *normals, float *geo, double *eik_sum, const Workspace &ws, cudaStream_t st) {
-    if (use_fwd1())
+                       float *normals, float *geo, double *eik_sum, const Workspace &ws, cudaStream_t st,
+                       float eik_w = 0.f, const int64_t *eik_count = nullptr) {
+    if (use_fwd1())  // (does not fuse the Eikonal cotangent: its flag tells the backward)
         field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD, st>>>(f, count, sdf, colors, normals,
                                                                                      geo, eik_sum, ws);
     else
         field_fwd2_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
-            f, count, sdf, colors, normals, geo, eik_sum, ws);
+            f, count, sdf, colors, normals, geo, eik_sum, ws, eik_w, eik_count);
 }
 
 }  // namespace tc
@@ -2396,6 +2422,11 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
         return check_launch("field_gather");
     case 1:
         tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st);
+        return check_launch("field_mlp_forward");
+    case 4:
+        NS2B_REQUIRE(eik_count != nullptr, "field_mlp_forward_eik: eik_count required");
+        tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st, static_cast<float>(eik_weight),
+                       eik_count);
         return check_launch("field_mlp_forward");
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");

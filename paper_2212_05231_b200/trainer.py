@@ -315,10 +315,12 @@ def train_step(state, dataset, time_index=0, batch=None):
         _lib.call("ns2b_field_gather", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
                   _lib.ptr(ws.d), _lib.ptr(count), P,
                   _lib.ptr(ws.field_ws), sp)
+    ws.count64.fill_(max(P_glob, 1))  # the Eikonal mean's divisor (global P), fused into the forward
     with _Timer(timers, "field_mlp_forward", st):
-        _lib.call("ns2b_field_mlp_forward", ctypes.byref(f), _lib.ptr(ws.pos32),
+        _lib.call("ns2b_field_mlp_forward_eik", ctypes.byref(f), _lib.ptr(ws.pos32),
                   _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf),
-                  _lib.ptr(ws.colors), None, None, _lib.ptr(ws.sums[3:4]), _lib.ptr(ws.field_ws), sp)
+                  _lib.ptr(ws.colors), None, None, _lib.ptr(ws.sums[3:4]), cfg.eikonal_weight,
+                  _lib.ptr(ws.count64), _lib.ptr(ws.field_ws), sp)
     # K3/K4: composite + Huber + compositing backward
     with _Timer(timers, "composite", st):
         _lib.call("ns2b_composite", _lib.ptr(ws.offsets), m, _lib.ptr(ws.sdf),
@@ -332,7 +334,6 @@ def train_step(state, dataset, time_index=0, batch=None):
     stepped = []
     if P_glob > 0:
         ws.grads[:end].zero_()
-        ws.count64.fill_(P_glob)
         # K5: field backward with the fused Eikonal cotangent
         sdf_g, col_g, tab_g = lay.views(ws.grads)
         with _Timer(timers, "field_mlp_backward", st):

@@ -21,20 +21,25 @@ from paper_2212_05231_b200 import renderer, scene_io, trainer  # noqa: E402
 
 def main():
     frames, views, image, f0 = 2, 12, 64, int(sys.argv[1]) if len(sys.argv) > 1 else 1500
-    ds = scene_io.make_synthetic("translating-sphere", views=views, image_size=image, seed=0, frames=frames)
+    preset = sys.argv[2] if len(sys.argv) > 2 else "translating-sphere"
+    ds = scene_io.make_synthetic(preset, views=views, image_size=image, seed=0, frames=frames)
     for t in range(frames):
         ds.to_device(t)
     cfg = trainer.TrainConfig(batch_size=4096, num_levels=8, table_size=2**14, seed=0, level_init=8,
-                              max_resolution=128, init_radius=0.25, total_steps=2 * f0)
+                              max_resolution=128, init_radius=0.25 if preset == "translating-sphere" else 0.4,
+                              total_steps=2 * f0)
     seq = dyn.SequenceState(trainer.TrainState.create(cfg, aabb=ds.scene_aabb))
     dc = dyn.DynamicConfig(first_frame_steps=f0)
     dyn.train_frame(seq, ds, 0, dc)
     st = seq.train
     level = trainer.level_schedule(st.step, cfg)
     batch = scene_io.sample_ray_batch(ds, 1, 1 << 16, cfg.fg_fraction, np.random.default_rng(5))
-    out = {"frame0_steps": f0, "sharpness": st.params.sharpness, "scan": []}
-    for tx in np.linspace(-0.08, -0.02, 13):
-        gt = dyn.GlobalTransform(np.zeros(3), np.array([tx, 0.0, 0.0]))
+    out = {"preset": preset, "frame0_steps": f0, "sharpness": st.params.sharpness, "scan": []}
+    rot = preset != "translating-sphere"
+    grid = np.deg2rad(np.linspace(-9, 3, 13)) if rot else np.linspace(-0.08, -0.02, 13)
+    for tx in grid:  # rotation: about z (axis-angle (0, 0, a)); translation: along x
+        gt = (dyn.GlobalTransform(np.array([0.0, 0.0, tx]), np.zeros(3)) if rot
+              else dyn.GlobalTransform(np.zeros(3), np.array([tx, 0.0, 0.0])))
         ft = seq.chain.frame_transform(gt)
         occ = renderer.OccupancyGrid(cfg.occupancy_resolution, ds.scene_aabb, cfg.occupancy_threshold)
         renderer.update_occupancy(occ, st.params, level, point_transform=ft.point)
@@ -53,7 +58,7 @@ def main():
         for k in range(400):
             dyn.dynamic_step(seq, ds, 1, gt, opt, False, 1e-3, transform_eikonal=use_eik)
             if k % 50 == 49:
-                traj.append([round(float(v), 5) for v in gt.t])
+                traj.append([round(float(v), 5) for v in (gt.w if rot else gt.t)])
         st.step = st_step
         print(json.dumps({"eikonal_in_transform_grad": use_eik, "T_trajectory_every_50": traj}))
 
