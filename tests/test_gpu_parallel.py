@@ -133,7 +133,7 @@ def test_two_rank_product_step_equals_single_process(device_sampler):
         # few entries may step differently (see test_gpu_parity.assert_adam_tables)
         diff = np.abs(res["flat"][k:] - single["flat"][k:]) > 1e-5
         assert diff.mean() <= 1e-3, f"{diff.sum()} table entries differ"
-        assert abs(res["slog"] - single["slog"]) <= 1e-12
+        assert abs(res["slog"] - single["slog"]) <= 1e-9 * abs(single["slog"])  # reassociated fp64 sums
         if not device_sampler:
             _check_oracle(res)
     assert np.array_equal(got[0]["flat"], got[1]["flat"]), "ranks must hold identical parameters"
