@@ -337,9 +337,12 @@ def test_divergence_raises(sphere64):
     before = np_(pst.params.grid.tables).copy()
     b = oscene.sample_ray_batch(sphere64, 0, 256, 0.9, np.random.default_rng(0))
     pst.step = 1  # skip the occupancy refresh
+    t_before = {k: a.t for k, a in pst.adam.items()}
     with pytest.raises(FloatingPointError, match="divergence: non-finite gradient for"):
         ptrain.train_step(pst, sphere64, batch=b)
     assert np.array_equal(np_(pst.params.grid.tables), before)
+    # no group was stepped, so no Adam step counter moved (bias correction, checkpoints)
+    assert {k: a.t for k, a in pst.adam.items()} == t_before
 
 
 @pytest.mark.parametrize("case", ["empty_occupancy", "rays_miss_box", "single_ray"])
