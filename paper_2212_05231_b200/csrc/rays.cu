@@ -6,7 +6,8 @@
 // Arithmetic follows numpy op for op (fp64, explicit round-to-nearest, no contraction
 // except where numpy's matmul itself fuses):
 //   d_cam = ((px + 0.5 - cx) / fx, (py + 0.5 - cy) / fy, 1)
-//   d     = d_cam @ R^T    (BLAS dgemm order: fma(d2, R2, fma(d1, R1, d0 * R0)))
+//   d     = d_cam @ R^T    (one BLAS dgemm order: fma(d2, R2, fma(d1, R1, d0 * R0));
+//                           another host BLAS may sum differently: within 2 ulp)
 //   d    /= sqrt((d0^2 + d1^2) + d2^2)          (np.linalg.norm, pairwise add)
 //   target = (u8 / 255.0) * mask
 #include "common.cuh"
