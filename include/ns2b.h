@@ -189,6 +189,18 @@ NS2B_API int ns2b_field_mlp_forward_eik(const ns2b_field_t *field, const float *
                                         float *colors, float *normals, float *geo, double *eik_sum,
                                         double eik_weight, const int64_t *eik_count,
                                         void *workspace, void *stream);
+/* ns2b_field_gather + ns2b_field_mlp_forward_eik in one call.  With NS2B_FWD=3 in the
+ * environment it is one kernel (field_fwd2_kernel<true>: the hash-grid gather inside the
+ * two-tile MLP forward; E, d feature/dx, x and v still reach the workspace for the
+ * backward) -- measured slower than the two kernels, so the default (and NS2B_FWD=1|2)
+ * launches the gather kernel and then the one-tile | two-tile forward.  eik_count may be
+ * NULL (no Eikonal fusion).  Results agree to the order of fp32 sums. */
+NS2B_API int ns2b_field_forward_fused_eik(const ns2b_field_t *field, const float *pos32,
+                                          const int32_t *ray_ids, const double *dirs,
+                                          const int32_t *count, int64_t capacity, float *sdf,
+                                          float *colors, float *normals, float *geo, double *eik_sum,
+                                          double eik_weight, const int64_t *eik_count,
+                                          void *workspace, void *stream);
 NS2B_API int ns2b_field_mlp_backward(const ns2b_field_t *field, const float *pos32,
                                      const int32_t *ray_ids, const double *dirs,
                                      const int32_t *count, int64_t capacity, const float *dl_dc,

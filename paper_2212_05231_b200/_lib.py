@@ -70,6 +70,8 @@ _SIGS = {
                                               P, P]),
     "ns2b_field_mlp_forward_eik": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
                                                   F64, P, P, P]),
+    "ns2b_field_forward_fused_eik": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
+                                                    F64, P, P, P]),
     "ns2b_field_mlp_backward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, F64,
                                                P, P, P, P, P]),
     "ns2b_field_scatter": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, I64, P, P, P]),

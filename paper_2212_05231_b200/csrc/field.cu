@@ -178,6 +178,15 @@ int ns2b_field_mlp_forward_eik(const ns2b_field_t *field, const float *pos32, co
                           as_stream(stream));
 }
 
+int ns2b_field_forward_fused_eik(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
+                                 const double *dirs, const int32_t *count, int64_t capacity, float *sdf,
+                                 float *colors, float *normals, float *geo, double *eik_sum, double eik_weight,
+                                 const int64_t *eik_count, void *workspace, void *stream) {
+    return field_stage_tc(5, field, pos32, ray_ids, dirs, count, capacity, sdf, colors, normals, geo, eik_sum,
+                          nullptr, nullptr, nullptr, eik_weight, eik_count, nullptr, nullptr, nullptr, workspace,
+                          as_stream(stream));
+}
+
 int ns2b_field_mlp_backward(const ns2b_field_t *field, const float *pos32, const int32_t *ray_ids,
                             const double *dirs, const int32_t *count, int64_t capacity, const float *dl_dc,
                             const float *dl_dsdf, const float *dl_dn_extra, double eik_weight,

@@ -352,7 +352,7 @@ constexpr int kDmaThread = 14 * 32;
 // phase needs anyway.  A tile whose max left [2^3, 2^15) is restaged with the exact
 // exponent (first tile of a CTA, sudden range changes).  Scaling by 2^e is exact, so
 // the products equal those of an exactly-scaled tile.
-enum Slot { kA1, kCin, kA1c, kA2c, kDlog, kU2, kU1, kDly, kU, kMv, NSLOT };
+enum Slot { kA1, kCin, kA1c, kA2c, kDlog, kU2, kU1, kDly, kU, kMv, kE, NSLOT };
 struct PredScale {
     uint32_t (*mx)[NSLOT];  // [2][NSLOT] block maxima (bits of |v|), tile parity
     int *pred;              // [NSLOT]
@@ -846,7 +846,8 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
 constexpr uint32_t F2_H1S = TE;                       // H1' right after the weights
 constexpr uint32_t F2_G0 = F2_H1S + 2 * WH1B;         // group 0 buffers
 constexpr uint32_t F2_EB = 0, F2_AB = 2 * TEB, F2_XCH = F2_AB + 2 * T64B,  // offsets in a group block
-                   F2_LG = F2_XCH + 8 * TILE * 4, F2_MK = F2_LG + 6 * TILE * 4, F2_GB = F2_MK + 24 * TILE;
+                   F2_LG = F2_XCH + 8 * TILE * 4, F2_MK = F2_LG + 6 * TILE * 4, F2_FS = F2_MK + 24 * TILE,
+                   F2_GB = F2_FS + 32 * TILE * 4;  // F2_FS: the fused gather's raw features [32][128]
 constexpr uint32_t SMEM_FWD2 = F2_G0 + 2 * F2_GB;
 static_assert(SMEM_FWD2 <= 227 * 1024, "fwd2 shared memory");
 
@@ -886,10 +887,18 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
+// kG: the hash-grid gather runs inside the kernel (phase G, before P0): each thread
+// interpolates its 8 levels of its sample, stages the encoding tile E straight into EB,
+// keeps d feature/dx (J) in TMEM for P2's normal and writes J, E's hi part, x and v to
+// the workspace for the backward -- the separate gather kernel and the E / J / x round
+// trip through HBM disappear.
+template <bool kG>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restrict__ sdf_out,
                   float *__restrict__ col_out, float *__restrict__ nrm_out, float *__restrict__ geo_out,
-                  double *__restrict__ eik_sum, Workspace ws, float eik_w, const int64_t *__restrict__ eik_count) {
+                  double *__restrict__ eik_sum, Workspace ws, float eik_w, const int64_t *__restrict__ eik_count,
+                  const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
+                  const double *__restrict__ dirs) {
     // with eik_count the Eikonal cotangent (trainer.py:229-235) is fused here, where the
     // normal is computed, and stored in place of the normal for the backward
     const bool fuse_eik = eik_count != nullptr;
@@ -904,6 +913,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     __shared__ uint32_t tmem_base_sh;
     __shared__ uint32_t gmx[2][2][NSLOT];
     __shared__ int gpred[2][NSLOT];
+    __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int g = warp >> 3, gw = warp & 7, tg = t & 255;
@@ -924,7 +934,13 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         for (int i = 0; i < 4; ++i) umma::mbar_init(bars + i, 1);
         umma::fence_barrier_init();
     }
-    if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 256);
+    if (kG && t < NS2B_MAX_LEVELS) {
+        lvs[t].lv = f.lv[t];
+        lvs[t].sx = f.sx[t];
+        lvs[t].sy = f.sy[t];
+        lvs[t].sz = f.sz[t];
+    }
+    if (warp == 0) umma::tmem_alloc(&tmem_base_sh, kG ? 512 : 256);
     publish();
     const int eH1 = wexp[0], eH2 = wexp[1], eC1 = wexp[2], eC2 = wexp[3], eH1s = wexp[5];
     uint64_t *mbar = bars + 2 * g, *mbare = bars + 2 * g + 1;
@@ -933,9 +949,10 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     float *xch = reinterpret_cast<float *>(S.p(gbase + F2_XCH));  // [2][128] d | [2][3][128] normal
     float *lgx = reinterpret_cast<float *>(S.p(gbase + F2_LG));   // [2][3][128] logit partials
     uint8_t *mkx = S.p(gbase + F2_MK);                            // [3][8][128] mask bytes
-    const uint32_t tb = tmem_base_sh + g * 128;
+    const uint32_t tb = tmem_base_sh + g * (kG ? 256 : 128);
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
-    const uint32_t SA = 0, SB = 64;
+    const uint32_t SA = 0, SB = 64, TJ = 128;  // TJ (kG): 16 levels x 8 columns of J
+    float *fsx = reinterpret_cast<float *>(S.p(gbase + F2_FS));  // kG: raw features [32][128]
     const bool io = (gw == 7 && lane == 0);  // stores, DMAs, prefetches of the group
     PredScaleG PS{gmx[g], gpred[g], 1, tg == 0};
     uint32_t phase = 0, phasee = 0;
@@ -959,25 +976,158 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     if (t < 64) pacc[t] = 0;
     __syncthreads();
 #endif
-    if (io && t0 < t_end) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
-    int eE_cur = t0 < t_end ? ws.e_exp[t0] : 0;
+    if (!kG && io && t0 < t_end) umma::bulk_g2s(S.p(EB), ws.e_tiles + t0 * 2 * TEB, 2 * TEB, mbare);
+    int eE_cur = (!kG && t0 < t_end) ? ws.e_exp[t0] : 0;
     for (int64_t tile = t0; tile < t_end; tile += stride) {
         const int64_t p = tile * TILE + r;
         const bool valid = p < P;
         const int64_t ntile = tile + stride;
         const bool has_next = ntile < t_end;
         PS.par ^= 1;
-        if (io && has_next) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
-        const float *xvt = ws.xv + tile * XVROWS * TILE + r;
-        const float x0 = xvt[0], x1 = xvt[TILE], x2 = xvt[2 * TILE];
-        const float v0 = xvt[3 * TILE], v1 = xvt[4 * TILE], v2 = xvt[5 * TILE];
-        const int eE = eE_cur;
         uint8_t *fwt = ws.fw_tiles + tile * static_cast<int64_t>(FWB);
         float *SBt = ws.sb + tile * SBROWS * TILE;
         float *nct = ws.fw_nc + tile * NCROWS * TILE + r;
+        float x0, x1, x2, v0, v1, v2;
+        int eE;
+        if constexpr (!kG) {
+            if (io && has_next) umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
+            const float *xvt = ws.xv + tile * XVROWS * TILE + r;
+            x0 = xvt[0];
+            x1 = xvt[TILE];
+            x2 = xvt[2 * TILE];
+            v0 = xvt[3 * TILE];
+            v1 = xvt[4 * TILE];
+            v2 = xvt[5 * TILE];
+            eE = eE_cur;
+        } else {
+            // ------------------------------------------ G: gather (_kernels.py:67-119) -> E, J
+            x0 = x1 = x2 = v0 = v1 = v2 = 0.f;
+            if (valid) {
+                x0 = pos[3 * p];
+                x1 = pos[3 * p + 1];
+                x2 = pos[3 * p + 2];
+                if (qh == 0) {
+                    const int rr = ray_ids[p];
+                    v0 = static_cast<float>(dirs[3 * rr]);  // field.py:216 (fp32 view dirs)
+                    v1 = static_cast<float>(dirs[3 * rr + 1]);
+                    v2 = static_cast<float>(dirs[3 * rr + 2]);
+                }
+            }
+            const float un0 = normalize_coord(x0, f.lo[0], f.ext[0]);
+            const float un1 = normalize_coord(x1, f.lo[1], f.ext[1]);
+            const float un2 = normalize_coord(x2, f.lo[2], f.ext[2]);
+            float fmax_ = qh == 0 ? fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), 1.f)) : 0.f;
+            float *Jt = ws.jac + tile * JROWS * TILE + r;
+#pragma unroll 1
+            for (int lb = 0; lb < 8; lb += 2) {  // 2 levels (16 float2 loads) in flight
+                float2 v[2][8];
+                float fr[2][3];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int l = 8 * qh + lb + i;
+                    if (l < NA) {
+                        const LevelInfo lv = lvs[l].lv;
+                        int cx, cy, cz;
+                        cell_frac(un0, lv.n, cx, fr[i][0]);
+                        cell_frac(un1, lv.n, cy, fr[i][1]);
+                        cell_frac(un2, lv.n, cz, fr[i][2]);
+                        const float2 *tab = reinterpret_cast<const float2 *>(f.tables) + l * f.T;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            v[i][c] = __ldg(tab + corner_row(lv, cx + ((c >> 2) & 1), cy + ((c >> 1) & 1), cz + (c & 1)));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int l = 8 * qh + lb + i;
+                    float f0 = 0.f, f1 = 0.f;
+                    if (l < NA) {
+                        const float fx = fr[i][0], fy = fr[i][1], fz = fr[i][2];
+                        const float sx = lvs[l].sx, sy = lvs[l].sy, sz = lvs[l].sz;
+                        float j00 = 0.f, j01 = 0.f, j02 = 0.f, j10 = 0.f, j11 = 0.f, j12 = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const int ox = (c >> 2) & 1, oy = (c >> 1) & 1, oz = c & 1;
+                            const float wx = ox ? fx : 1.f - fx, wy = oy ? fy : 1.f - fy, wz = oz ? fz : 1.f - fz;
+                            const float w = wx * wy * wz;
+                            const float dwx = (ox ? sx : -sx) * (wy * wz);
+                            const float dwy = (oy ? sy : -sy) * (wx * wz);
+                            const float dwz = (oz ? sz : -sz) * (wx * wy);
+                            f0 = fmaf(w, v[i][c].x, f0);
+                            f1 = fmaf(w, v[i][c].y, f1);
+                            j00 = fmaf(dwx, v[i][c].x, j00);
+                            j01 = fmaf(dwy, v[i][c].x, j01);
+                            j02 = fmaf(dwz, v[i][c].x, j02);
+                            j10 = fmaf(dwx, v[i][c].y, j10);
+                            j11 = fmaf(dwy, v[i][c].y, j11);
+                            j12 = fmaf(dwz, v[i][c].y, j12);
+                        }
+                        fmax_ = fmaxf(fmax_, fmaxf(fabsf(f0), fabsf(f1)));
+                        float *jr = Jt + 6 * l * TILE;  // for the backward (evict-first)
+                        __stcs(jr, j00);
+                        __stcs(jr + TILE, j01);
+                        __stcs(jr + 2 * TILE, j02);
+                        __stcs(jr + 3 * TILE, j10);
+                        __stcs(jr + 4 * TILE, j11);
+                        __stcs(jr + 5 * TILE, j12);
+                        const uint32_t c = my + TJ + 8 * l;  // for P2's normal
+                        umma::tmem_st4(c, j00, j01, j02, j10);
+                        umma::tmem_st2(c + 4, j11, j12);
+                    }
+                    fsx[(2 * l) * TILE + r] = f0;  // E feature columns 2l, 2l + 1
+                    fsx[(2 * l + 1) * TILE + r] = f1;
+                }
+            }
+            umma::tmem_st_wait();
+            if (qh == 0 && valid) {  // x, v for the input-gradient pass (dynamic scenes)
+                float *xvt = ws.xv + tile * XVROWS * TILE + r;
+                __stcs(xvt, x0);
+                __stcs(xvt + TILE, x1);
+                __stcs(xvt + 2 * TILE, x2);
+                __stcs(xvt + 3 * TILE, v0);
+                __stcs(xvt + 4 * TILE, v1);
+                __stcs(xvt + 5 * TILE, v2);
+            }
+            // E = [features 0..31 | x y z | 1 | 0 x 12]: half qh stages blocks 2qh, 2qh+1 (its
+            // 8 levels) and block 4 + qh (x, 1 / zeros)
+            int e = PS.guess(kE);
+            PS.contrib(kE, fmax_);
+            auto stg = [&](int ee) {
+                const float sc = pow2i(ee);
+                float blk[8];
+#pragma unroll
+                for (int bb = 0; bb < 2; ++bb) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) blk[k] = fsx[(16 * qh + 8 * bb + k) * TILE + r];
+                    stage_blk<48>(S, EB, TEB, r, 2 * qh + bb, blk, sc);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) blk[k] = 0.f;
+                if (qh == 0) {
+                    blk[0] = x0;
+                    blk[1] = x1;
+                    blk[2] = x2;
+                    blk[3] = 1.f;
+                }
+                stage_blk<48>(S, EB, TEB, r, 4 + qh, blk, sc);
+            };
+            stg(e);  // EB: the previous tile's CIN store and Zc1 GEMM have finished with it
+            group_publish(g);
+            if (tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;  // (the slot reset moves here from P1)
+            if (!PS.check(kE, e)) {
+                stg(e);
+                group_publish(g);
+            }
+            eE = e;
+            PMARK(13);
+            if (io) {  // E's hi part for the backward's dH1 GEMM
+                umma::bulk_s2g(ws.e_tiles + tile * 2 * TEB, S.p(EB), TEB);
+                ws.e_exp[tile] = e;
+            }
+        }
         // ------------------------------------------------ P0: Z1 = E H1^T -> A
         if (gw == 7) {
-            umma::mbar_wait(mbare, phasee);
+            if (!kG) umma::mbar_wait(mbare, phasee);
             umma::gemm3w<3>(tb + SA, S.K(EB, TEB, 48), S.K(WH1, WH1B, 48), ID_KK(64), false);
             if (lane == 0) umma::bulk_wait_read_n<0>();  // the previous tile's A1c store has left AB
             __syncwarp();
@@ -1027,7 +1177,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             }
             group_publish(g);
             PMARK(2);
-            if (tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;
+            if (!kG && tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;
             if (!PS.check(kA1, eA1)) {
                 stg(eA1);
                 group_publish(g);
@@ -1044,10 +1194,13 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         // Y / JD GEMMs
         const float *jt = ws.jac + tile * JROWS * TILE + r;
         float jv0[4][6];
+        if constexpr (!kG) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int k = 0; k < 6; ++k) jv0[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
+                for (int k = 0; k < 6; ++k)
+                    jv0[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
+        }
         wait_mma(mbar, phase);
         PMARK(4);
         // ------------------------------------------------ P2: normal, cin -> EB; Zc1 -> A
@@ -1078,10 +1231,17 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     umma::tmem_ld2(my + SA + 2 * (l0 + i), jd[i][0], jd[i][1]);
-                    const float *jr = jt + 6 * (l0 + i) * TILE;
+                    if constexpr (kG) {  // J from TMEM (the G phase put it there)
+                        float jl[8];
+                        umma::tmem_ld8(my + TJ + 8 * (l0 + i), jl);
 #pragma unroll
-                    for (int k = 0; k < 6; ++k)
-                        jv[i][k] = first ? jv0[i][k] : (l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f);
+                        for (int k = 0; k < 6; ++k) jv[i][k] = jl[k];
+                    } else {
+                        const float *jr = jt + 6 * (l0 + i) * TILE;
+#pragma unroll
+                        for (int k = 0; k < 6; ++k)
+                            jv[i][k] = first ? jv0[i][k] : (l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f);
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -1210,7 +1370,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 // read their tiles, P4 may stage A2c into AB and EB can take the next E
                 umma::bulk_s2g(fwt + FW_A1C, S.p(AB), T64B);
                 umma::bulk_wait_read_n<0>();
-                if (has_next) umma::bulk_g2s(S.p(EB), ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mbare);
+                if (!kG && has_next) umma::bulk_g2s(S.p(EB), ws.e_tiles + ntile * 2 * TEB, 2 * TEB, mbare);
             }
             __syncwarp();
             umma::commit_elect(mbar);
@@ -1277,7 +1437,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             umma::bulk_s2g(fwt + FW_A2C, S.p(AB), T64B);  // (P0 waits for it before P1 restages AB)
             ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
-        if (has_next) eE_cur = ws.e_exp[ntile];
+        if (!kG && has_next) eE_cur = ws.e_exp[ntile];
         PMARK(11);
         // ------------------------------------------------ P5: colours, masks
         if (qh == 0) {
@@ -1321,7 +1481,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     if (io) umma::bulk_wait_all();
     umma::fence_before_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc(tmem_base_sh, 256);
+    if (warp == 0) umma::tmem_dealloc(tmem_base_sh, kG ? 512 : 256);
 }
 
 // ---------------------------------------------------------------------------
@@ -2363,7 +2523,10 @@ static int ensure_tc_attrs() {
         e = cudaFuncSetAttribute(field_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_BWD));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(field_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(field_fwd2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SMEM_FWD2));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(field_fwd2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_FWD2));
     if (e != cudaSuccess) return set_error(NS2B_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
     g_tc_attr = 1;
@@ -2381,6 +2544,8 @@ static bool use_fwd1() {
     return v == 1;
 }
 
+static int fwd_mode();
+
 static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, float *sdf, float *colors,
                        float *normals, float *geo, double *eik_sum, const Workspace &ws, cudaStream_t st,
                        float eik_w = 0.f, const int64_t *eik_count = nullptr) {
@@ -2388,8 +2553,23 @@ static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, 
         field_fwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD, st>>>(f, count, sdf, colors, normals,
                                                                                      geo, eik_sum, ws);
     else
-        field_fwd2_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
-            f, count, sdf, colors, normals, geo, eik_sum, ws, eik_w, eik_count);
+        field_fwd2_kernel<false><<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_FWD2, st>>>(
+            f, count, sdf, colors, normals, geo, eik_sum, ws, eik_w, eik_count, nullptr, nullptr, nullptr);
+}
+
+// NS2B_FWD: 1 = gather kernel + one-tile forward, unset / 2 = gather kernel + two-tile
+// forward (the default), 3 = the two-tile forward with the gather fused
+// (field_fwd2_kernel<true>).  Measured at c2: 3 is slower (gather + forward 25.2 ms vs 6.35 +
+// 7.3 ms): a tile's gather is bound by L1 wavefronts (~10k cycles of L1 per tile), and with
+// two tiles per SM, each gathering before its MLP phases, the L1 idles while both groups
+// run MMAs -- the separate gather kernel keeps four tiles per SM in flight on the L1.
+static int fwd_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NS2B_FWD");
+        v = e ? atoi(e) : 2;
+    }
+    return v;
 }
 
 }  // namespace tc
@@ -2428,6 +2608,20 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
         tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st, static_cast<float>(eik_weight),
                        eik_count);
         return check_launch("field_mlp_forward");
+    case 5:  // gather + MLP forward (+ the Eikonal cotangent when eik_count)
+        NS2B_REQUIRE(pos32 && ray_ids && dirs && count, "field_forward_fused: null input");
+        if (tc::fwd_mode() == 3) {
+            tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2, st>>>(
+                f, count, sdf, colors, normals, geo, eik_sum, ws, static_cast<float>(eik_weight), eik_count, pos32,
+                ray_ids, dirs);
+            return check_launch("field_gather_mlp_forward");
+        }
+        tc::field_gather_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
+                                                                                             count, ws);
+        if ((rc = check_launch("field_gather"))) return rc;
+        tc::launch_fwd(f, ntiles, count, sdf, colors, normals, geo, eik_sum, ws, st, static_cast<float>(eik_weight),
+                       eik_count);
+        return check_launch("field_mlp_forward");
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
         tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
@@ -2452,6 +2646,11 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
+    if (tc::fwd_mode() == 3) {
+        tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2, st>>>(
+            f, count, sdf, colors, normals, geo, eik_sum, ws, 0.f, nullptr, pos32, ray_ids, dirs);
+        return check_launch("field_forward_tc");
+    }
     tc::field_gather_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::GATHER_BLOCK, 0, st>>>(f, pos32, ray_ids, dirs,
                                                                                          count, ws);
     if ((rc = check_launch("field_gather"))) return rc;

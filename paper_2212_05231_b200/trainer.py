@@ -310,12 +310,12 @@ def train_step(state, dataset, time_index=0, batch=None):
     s = params.sharpness
     na = enc.active_level_count(params.grid, level)
     f = params.field_struct(na)
-    # K2: gather (features + d feature/dx -> workspace), tcgen05 MLP forward (+ Eikonal sum)
+    # K2: gather (features + d feature/dx -> workspace), two-tile tcgen05 MLP forward
+    # (+ Eikonal sum and its cotangent, fused)
+    ws.count64.fill_(max(P_glob, 1))  # the Eikonal mean's divisor (global P)
     with _Timer(timers, "field_gather", st):
         _lib.call("ns2b_field_gather", ctypes.byref(f), _lib.ptr(ws.pos32), _lib.ptr(ws.ray_ids),
-                  _lib.ptr(ws.d), _lib.ptr(count), P,
-                  _lib.ptr(ws.field_ws), sp)
-    ws.count64.fill_(max(P_glob, 1))  # the Eikonal mean's divisor (global P), fused into the forward
+                  _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.field_ws), sp)
     with _Timer(timers, "field_mlp_forward", st):
         _lib.call("ns2b_field_mlp_forward_eik", ctypes.byref(f), _lib.ptr(ws.pos32),
                   _lib.ptr(ws.ray_ids), _lib.ptr(ws.d), _lib.ptr(count), P, _lib.ptr(ws.sdf),
