@@ -847,9 +847,9 @@ constexpr uint32_t F2_H1S = TE;                       // H1' right after the wei
 constexpr uint32_t F2_G0 = F2_H1S + 2 * WH1B;         // group 0 buffers
 constexpr uint32_t F2_EB = 0, F2_AB = 2 * TEB, F2_XCH = F2_AB + 2 * T64B,  // offsets in a group block
                    F2_LG = F2_XCH + 8 * TILE * 4, F2_MK = F2_LG + 6 * TILE * 4, F2_FS = F2_MK + 24 * TILE,
-                   F2_GB = F2_FS + 32 * TILE * 4;  // F2_FS: the fused gather's raw features [32][128]
-constexpr uint32_t SMEM_FWD2 = F2_G0 + 2 * F2_GB;
-static_assert(SMEM_FWD2 <= 227 * 1024, "fwd2 shared memory");
+                   F2_GB = F2_FS, F2_GBG = F2_FS + 32 * TILE * 4;  // F2_FS (kG): raw features [32][128]
+constexpr uint32_t SMEM_FWD2 = F2_G0 + 2 * F2_GB, SMEM_FWD2G = F2_G0 + 2 * F2_GBG;
+static_assert(SMEM_FWD2G <= 227 * 1024, "fwd2 shared memory");
 
 __device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(g + 1) : "memory"); }
 __device__ __forceinline__ void group_publish(int g) {
@@ -944,7 +944,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     publish();
     const int eH1 = wexp[0], eH2 = wexp[1], eC1 = wexp[2], eC2 = wexp[3], eH1s = wexp[5];
     uint64_t *mbar = bars + 2 * g, *mbare = bars + 2 * g + 1;
-    const uint32_t gbase = F2_G0 + g * F2_GB;
+    const uint32_t gbase = F2_G0 + g * (kG ? F2_GBG : F2_GB);
     const uint32_t EB = gbase + F2_EB, AB = gbase + F2_AB;
     float *xch = reinterpret_cast<float *>(S.p(gbase + F2_XCH));  // [2][128] d | [2][3][128] normal
     float *lgx = reinterpret_cast<float *>(S.p(gbase + F2_LG));   // [2][3][128] logit partials
@@ -2527,7 +2527,7 @@ static int ensure_tc_attrs() {
                                  static_cast<int>(SMEM_FWD2));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(field_fwd2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(SMEM_FWD2));
+                                 static_cast<int>(SMEM_FWD2G));
     if (e != cudaSuccess) return set_error(NS2B_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
     g_tc_attr = 1;
     return NS2B_OK;
@@ -2611,7 +2611,7 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
     case 5:  // gather + MLP forward (+ the Eikonal cotangent when eik_count)
         NS2B_REQUIRE(pos32 && ray_ids && dirs && count, "field_forward_fused: null input");
         if (tc::fwd_mode() == 3) {
-            tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2, st>>>(
+            tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2G, st>>>(
                 f, count, sdf, colors, normals, geo, eik_sum, ws, static_cast<float>(eik_weight), eik_count, pos32,
                 ray_ids, dirs);
             return check_launch("field_gather_mlp_forward");
@@ -2647,7 +2647,7 @@ int field_forward_tc(const ns2b_field_t *field, const float *pos32, const int32_
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
     if (tc::fwd_mode() == 3) {
-        tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2, st>>>(
+        tc::field_fwd2_kernel<true><<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_FWD2G, st>>>(
             f, count, sdf, colors, normals, geo, eik_sum, ws, 0.f, nullptr, pos32, ray_ids, dirs);
         return check_launch("field_forward_tc");
     }
