@@ -22,7 +22,6 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
-import math
 from dataclasses import dataclass
 
 import numpy as np
