@@ -264,7 +264,11 @@ __device__ __forceinline__ void publish() {
 }
 
 __device__ __forceinline__ void wait_mma(uint64_t *mbar, uint32_t &phase) {
+#ifdef NS2B_SPIN_WAIT
+    umma::mbar_wait_spin(mbar, phase);
+#else
     umma::mbar_wait(mbar, phase);
+#endif
     phase ^= 1u;
     umma::fence_after_sync();
 }
