@@ -20,8 +20,11 @@ from paper_2212_05231_b200 import renderer, scene_io, trainer  # noqa: E402
 
 
 def main():
-    frames, views, image, f0 = 2, 12, 64, int(sys.argv[1]) if len(sys.argv) > 1 else 1500
+    f0 = int(sys.argv[1]) if len(sys.argv) > 1 else 1500
     preset = sys.argv[2] if len(sys.argv) > 2 else "translating-sphere"
+    views = int(sys.argv[3]) if len(sys.argv) > 3 else 12
+    image = int(sys.argv[4]) if len(sys.argv) > 4 else 64
+    frames = 2
     ds = scene_io.make_synthetic(preset, views=views, image_size=image, seed=0, frames=frames)
     for t in range(frames):
         ds.to_device(t)
@@ -33,21 +36,27 @@ def main():
     dyn.train_frame(seq, ds, 0, dc)
     st = seq.train
     level = trainer.level_schedule(st.step, cfg)
-    batch = scene_io.sample_ray_batch(ds, 1, 1 << 16, cfg.fg_fraction, np.random.default_rng(5))
-    out = {"preset": preset, "frame0_steps": f0, "sharpness": st.params.sharpness, "scan": []}
+    out = {"preset": preset, "frame0_steps": f0, "views": views, "image": image,
+           "sharpness": st.params.sharpness, "scan": [], "scan_frame0": []}
     rot = preset != "translating-sphere"
     grid = np.deg2rad(np.linspace(-9, 3, 13)) if rot else np.linspace(-0.08, -0.02, 13)
-    for tx in grid:  # rotation: about z (axis-angle (0, 0, a)); translation: along x
-        gt = (dyn.GlobalTransform(np.array([0.0, 0.0, tx]), np.zeros(3)) if rot
-              else dyn.GlobalTransform(np.zeros(3), np.array([tx, 0.0, 0.0])))
-        ft = seq.chain.frame_transform(gt)
-        occ = renderer.OccupancyGrid(cfg.occupancy_resolution, ds.scene_aabb, cfg.occupancy_threshold)
-        renderer.update_occupancy(occ, st.params, level, point_transform=ft.point)
-        rendered, rec = renderer.render_rays(batch, st.params, occ, level, point_transform=ft.point,
-                                             dir_transform=ft.direction)
-        color, eik, mse, *_ = dyn._cotangents(st, batch, rendered, rec)
-        out["scan"].append({"tx": round(float(tx), 4), "color": color, "eikonal": eik,
-                            "total": color + cfg.eikonal_weight * eik})
+    for frame, key in ((1, "scan"), (0, "scan_frame0")):
+        batch = scene_io.sample_ray_batch(ds, frame, 1 << 16, cfg.fg_fraction, np.random.default_rng(5))
+        for tx in (grid if frame == 1 else grid - grid[len(grid) * 3 // 4]):  # frame 0: around identity
+            gt = (dyn.GlobalTransform(np.array([0.0, 0.0, tx]), np.zeros(3)) if rot
+                  else dyn.GlobalTransform(np.zeros(3), np.array([tx, 0.0, 0.0])))
+            ft = seq.chain.frame_transform(gt)
+            occ = renderer.OccupancyGrid(cfg.occupancy_resolution, ds.scene_aabb, cfg.occupancy_threshold)
+            renderer.update_occupancy(occ, st.params, level, point_transform=ft.point)
+            rendered, rec = renderer.render_rays(batch, st.params, occ, level, point_transform=ft.point,
+                                                 dir_transform=ft.direction)
+            color, eik, mse, *_ = dyn._cotangents(st, batch, rendered, rec)
+            # the same with the view directions left in frame space (isolates the colour
+            # network's view dependence from the geometry)
+            rendered2, rec2 = renderer.render_rays(batch, st.params, occ, level, point_transform=ft.point)
+            color_v0 = dyn._cotangents(st, batch, rendered2, rec2)[0]
+            out[key].append({"tx": round(float(tx), 4), "color": color, "eikonal": eik,
+                             "total": color + cfg.eikonal_weight * eik, "color_frame_view_dirs": color_v0})
     print(json.dumps(out))
     # (b) transform-only trajectories, with and without the Eikonal term in its gradient
     for use_eik in (True, False):
