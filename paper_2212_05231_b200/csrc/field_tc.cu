@@ -1762,6 +1762,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     };
     if (t == kDmaThread && in_full(blockIdx.x)) in_dma(blockIdx.x);
     int eE_cur = static_cast<int64_t>(blockIdx.x) * TILE < P ? ws.e_exp[blockIdx.x] : 0;
+    // each tile's per-sample inputs are read at the end of the previous tile (its B5)
+    int4 fe_nx = make_int4(0, 0, 0, 0);
+    BwdIn in_nx{};
+    if (static_cast<int64_t>(blockIdx.x) * TILE < P) in_nx = read_in(blockIdx.x, fe_nx);
     int ntiles_done = 0;
 #ifdef NS2B_PHASE_PROF
     __shared__ long long pacc[64];
@@ -1784,8 +1788,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, TEB);
         }
         // per-sample inputs (DMA'd during the previous tile)
-        int4 fe;
-        const BwdIn in = read_in(tile, fe);
+        const int4 fe = fe_nx;  // read at the end of the previous tile
+        const BwdIn in = in_nx;
         PMARK(19);
         const uint32_t m1 = in.mk.x & 0xFFFFu, mc1 = in.mk.x >> 16, mc2 = in.mk.y;
         const int eA1 = fe.x, eCin = fe.y, eA1c = fe.z, eA2c = fe.w;
@@ -2132,6 +2136,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
                 dma(TZ, fwt(ntile) + FW_A1C, T64B, mb_z);
             }
             if (has_next) j_store();
+            if (has_next) in_nx = read_in(ntile, fe_nx);  // TIN landed during B1
             PMARK(17);
         }
         // Tile boundary barrier: without it a warp can run into the next tile while another
