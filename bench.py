@@ -452,7 +452,8 @@ def run_ours(args, wl):
         "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": 8 * (m_global // world),
                 "d2h_bytes_per_step": 4 + 64, "ms_per_step": ms_e2e / args.steps,
                 "path": "trainer.train_step(state, dataset) with dataset.to_device(): host rng draws "
-                        "(the reference's), this rank's picks H2D (int64), rays + targets built on "
+                        "(the reference's; each step's draw runs on the host under the previous step's "
+                        "device work), this rank's picks H2D (int64), rays + targets built on "
                         "the device; P (int32) and the 8-double step report D2H",
                 "pinned_host_rays": {"value": e2e_rays, "ms_per_step": ms_e2e_rays / args.steps,
                                      "h2d_bytes_per_step": 72 * (m_global // world)}},

@@ -463,13 +463,19 @@ class DeviceSampler:
         self._build(a, b, o, d, t)
         return RayBatch(o, d, t, flags)
 
-    def sample_into(self, count, fg_fraction, rng, o, d, t, rank=0, world=1):
+    def draw_key(self, count, fg_fraction):
+        """What `_draw` depends on besides the rng: a draw made ahead is valid for any
+        later call with the same key."""
+        return (self.n_fg, self.n_bg, int(count), float(fg_fraction))
+
+    def sample_into(self, count, fg_fraction, rng, o, d, t, rank=0, world=1, draw=None):
         """Rays rank, rank + world, ... of the `count`-ray global batch (the interleaved
         data-parallel shard, `parallel.shard_slice`) into caller buffers of
         `parallel.shard_size(count, rank, world)` rows.  The rng is consumed for the whole
         global batch, as every rank (and the reference) does; only the shard's picks
-        (8 B per ray) are uploaded and only its rays are built."""
-        a, b, n_fg, all_fg = self._draw(count, fg_fraction, rng)
+        (8 B per ray) are uploaded and only its rays are built.  `draw` is a `_draw`
+        result made ahead from the same rng (then `rng` is not consumed here)."""
+        a, b, n_fg, all_fg = draw if draw is not None else self._draw(count, fg_fraction, rng)
         if all_fg:  # background picks index the foreground pool: one pool
             a, b = np.concatenate([a, b])[rank::world], b[:0]
         else:

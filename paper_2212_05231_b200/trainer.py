@@ -200,7 +200,12 @@ class TrainState:
     """Parameters, moments, occupancy, rng and step (`trainer.py:175-212`)."""
 
     def __init__(self, params, occ, config, rng, step=0, dp=None):
-        self.params, self.occ, self.config, self.rng, self.step = params, occ, config, rng, step
+        self.params, self.occ, self.config, self.step = params, occ, config, step
+        self._rng, self._ahead = rng, None
+        # with a device-resident dataset, draw the next step's ray picks on the host while
+        # the device runs this step (the rng stream and its consumers are unchanged: `rng`
+        # rewinds an unused draw before anyone else reads the generator)
+        self.draw_ahead = True
         self.dp = dp or DataParallel.from_env()
         dev = params.flat.device
         self.m_flat = torch.zeros_like(params.flat)
@@ -216,6 +221,17 @@ class TrainState:
         self.adam["sharpness_log"] = AdamState(torch.zeros(1, dtype=torch.float64, device=dev),
                                                torch.zeros(1, dtype=torch.float64, device=dev))
         self.ws = StepWorkspace(params, dev)
+
+    @property
+    def rng(self):
+        """The reference's generator, at the reference's stream position: a pick draw
+        `train_step` made ahead for the next step is rewound first."""
+        _rewind_ahead(self)
+        return self._rng
+
+    @rng.setter
+    def rng(self, g):
+        self._rng, self._ahead = g, None
 
     @classmethod
     def create(cls, config, aabb=((-1, -1, -1), (1, 1, 1)), dp=None):
@@ -263,6 +279,24 @@ def _upload_batch(ws, batch, sl, stream):
             dst.copy_(h.pin_memory(), non_blocking=True)
 
 
+def _rewind_ahead(state):
+    """Undo a pick draw made ahead (unless the generator moved since: then the caller
+    replaced or re-seeded it and the draw is simply dropped)."""
+    ah, state._ahead = state._ahead, None
+    if ah is not None and state._rng.bit_generator.state == ah[2]:
+        state._rng.bit_generator.state = ah[1]
+
+
+def _take_ahead(state, key):
+    """The draw made ahead if it is still the next draw of the stream with this key."""
+    ah = state._ahead
+    if ah is not None and ah[0] == key and state._rng.bit_generator.state == ah[2]:
+        state._ahead = None
+        return ah[3]
+    _rewind_ahead(state)
+    return None
+
+
 def train_step(state, dataset, time_index=0, batch=None):
     """One optimisation step (`trainer.py:281-310`); returns a LossReport.
 
@@ -281,7 +315,9 @@ def train_step(state, dataset, time_index=0, batch=None):
         # rank's picks go up and only its rays are built, straight into the workspace
         m_total = cfg.batch_size
         ws.rays(dp.shard_size(m_total))
-        sampler.sample_into(m_total, cfg.fg_fraction, state.rng, ws.o, ws.d, ws.tgt, dp.rank, dp.world)
+        draw_key = sampler.draw_key(m_total, cfg.fg_fraction)
+        sampler.sample_into(m_total, cfg.fg_fraction, state._rng, ws.o, ws.d, ws.tgt, dp.rank, dp.world,
+                            draw=_take_ahead(state, draw_key))
     else:
         if batch is None:
             batch = scene_io.sample_ray_batch(dataset, time_index, cfg.batch_size, cfg.fg_fraction,
@@ -356,6 +392,10 @@ def train_step(state, dataset, time_index=0, batch=None):
     ws.report[4:5].copy_(ws.flag.to(torch.float64))
     ws.report[5:6].copy_(params.sharpness_log)
     ws.report_host.copy_(ws.report, non_blocking=True)
+    if sampler is not None and state.draw_ahead:  # host rng work under the device step
+        before = state._rng.bit_generator.state
+        nxt = sampler._draw(m_total, cfg.fg_fraction, state._rng)
+        state._ahead = (draw_key, before, state._rng.bit_generator.state, nxt)
     st.synchronize()
     rep = ws.report_host.tolist()
     if rep[4] != 0:

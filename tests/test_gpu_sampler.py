@@ -58,6 +58,41 @@ def test_training_uses_device_sampler():
     assert a.rng.bit_generator.state == b.rng.bit_generator.state
 
 
+def test_draw_ahead_keeps_the_reference_stream():
+    """`train_step` draws the next step's picks while the device runs (`draw_ahead`): the
+    batches, the losses and the rng position any caller observes are those of drawing at
+    the start of each step -- across an external read of `state.rng`, a step on the host
+    sampler (other dataset), a re-seed and a checkpoint-style state read."""
+    from paper_2212_05231_b200 import trainer
+
+    ds_d = scene_io.make_synthetic("sphere", views=8, image_size=64, seed=0)
+    ds_d.to_device()
+    ds_h = scene_io.make_synthetic("sphere", views=8, image_size=64, seed=0)
+    cfg = trainer.TrainConfig(batch_size=2048, num_levels=8, table_size=2**14, seed=0, level_init=8)
+    a, b = trainer.TrainState.create(cfg), trainer.TrainState.create(cfg)
+    b.draw_ahead = False
+
+    def both(ds):
+        ra, rb = trainer.train_step(a, ds), trainer.train_step(b, ds)
+        assert ra.sample_count == rb.sample_count
+        # (same batches; the float-atomic order of the scatter drifts the parameters ~1e-7
+        # per step, so the losses of later steps agree to ~1e-6, not bit for bit)
+        assert abs(ra.total - rb.total) <= 1e-4 * abs(rb.total)
+
+    both(ds_d)
+    assert a._ahead is not None  # a draw is pending ...
+    both(ds_d)                   # ... and used
+    assert a.rng.bit_generator.state == b.rng.bit_generator.state  # rewinds the pending draw
+    both(ds_d)
+    both(ds_h)                   # host sampler: the pending draw is rewound first
+    both(ds_d)
+    a.rng, b.rng = np.random.default_rng(3), np.random.default_rng(3)
+    both(ds_d)
+    both(ds_d)
+    assert a.rng.bit_generator.state == b.rng.bit_generator.state
+    assert a._ahead is None
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_device_sampler_shards(world):
     """`DeviceSampler.sample_into` (the data-parallel path of train_step): each rank's
