@@ -255,7 +255,9 @@ def run_ours(args, wl):
     from paper_2212_05231_b200.parallel import init_from_env
     from paper_2212_05231_b200.scene_io import DeviceRaySource
 
-    dp = init_from_env()
+    # NS2B_DIST_BACKEND=gloo: ranks share one GPU with host-side collectives (tests of the
+    # multi-rank line only -- the timings of co-located ranks mean nothing)
+    dp = init_from_env(os.environ.get("NS2B_DIST_BACKEND") or None)
     rank, world = dp.rank, dp.world
     dev = torch.device("cuda", torch.cuda.current_device())
     torch.manual_seed(0)
