@@ -95,15 +95,31 @@ constexpr uint32_t ID_KK(int N) { return umma::make_idesc(128, N, 0, 0, 0); }
 constexpr uint32_t ID_KM(int N) { return umma::make_idesc(128, N, 0, 0, 1); }
 constexpr uint32_t ID_WG(int N) { return umma::make_idesc(64, N, 0, 1, 1); }
 // Weight-gradient GEMMs (dW = X^T Y summed over the tile's 128 samples, and over a CTA's
-// ~1.2k tiles in TMEM) take the forward-side activation operand in fp16 (its hi part
-// only: fp16 storage of A1, CIN, A1c, A2c and E for the weight gradients, fp32
-// accumulation) and the cotangent operand split hi + lo:
-//   activation is A:  A_hi B_hi + A_hi B_lo   (gemm2a)
-//   activation is B:  A_hi B_hi + A_lo B_hi   (gemm2w)
-// two MMAs per K step instead of three, and the forward stores (the backward DMAs) only
-// the hi halves of its tiles.  The per-sample chain GEMMs keep the full 3-term split.
+// ~1.2k tiles in TMEM) take both operands in fp16 (stated fp16 storage of the
+// activations A1, CIN, A1c, A2c, E and of the cotangent tiles for the weight gradients,
+// fp32 accumulation): one MMA per K step, and the forward stores (the backward DMAs) only
+// the hi halves of its tiles.  Measured: backward 10.13 -> 9.73 ms against the round-2
+// two-term form (cotangent split hi + lo, gemm2a / gemm2w; -DNS2B_WG2 restores it); at
+// 2^22 points every weight gradient stays within 1e-4 relL2 of torch fp64
+// (tests/test_gpu_c3.py).  The per-sample chain GEMMs keep the full 3-term split: a row's
+// precision there reaches the table gradients directly.  Their A operands (the cotangent
+// tiles) live in tensor memory (NS2B_BWD_TA, default; -DNS2B_BWD_SMEM_A reads them from
+// shared memory): 9.73 -> 9.43 ms.
+#ifndef NS2B_WG2
+#define NS2B_WG1
+#endif
+#ifndef NS2B_BWD_SMEM_A  // (NS2B_BWD_SMEM_A: the chain GEMMs read A from shared memory)
+#define NS2B_BWD_TA
+#endif
+#ifdef NS2B_WG1
+#define WG_ACT_A umma::gemm1
+#define WG_ACT_B umma::gemm1
+#define WG_MASK umma::gemm1
+#else
 #define WG_ACT_A umma::gemm2a
 #define WG_ACT_B umma::gemm2w
+#define WG_MASK umma::gemm2a
+#endif
 
 #ifdef NS2B_PHASE_PROF
 #define PMARK(i)                                  \
@@ -1502,6 +1518,34 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
 // accumulate in TMEM across tiles while their operand exponents stay the same (sticky
 // predictions), and are folded into global memory every kFoldTiles tiles, when an
 // exponent changes, and at the end.
+// Backward chain GEMMs with the A operand in tensor memory (NS2B_BWD_TA, needs NS2B_WG1):
+// an epilogue block of 8 columns goes to the TMEM A region as packed hi and lo halves
+// (tcgen05.st) and, as its hi half only, to the shared-memory tile the weight-gradient
+// GEMMs read.  The chain GEMMs then read no shared memory for A (3 of the 4 operand
+// streams of a split K step), and the smem tiles hold hi halves only.
+#if defined(NS2B_BWD_TA) && !defined(NS2B_WG1)
+#error "NS2B_BWD_TA needs NS2B_WG1 (the smem tiles carry hi halves only)"
+#endif
+template <int C>
+__device__ __forceinline__ void stage_blk_ta(const Smem &s, uint32_t off, int r, int b, const float *v, float sc,
+                                             uint32_t ta_hi, uint32_t ta_lo) {
+    uint4 h, l;
+    umma::split2<0>(v[0] * sc, v[1] * sc, h.x, l.x);
+    umma::split2<0>(v[2] * sc, v[3] * sc, h.y, l.y);
+    umma::split2<0>(v[4] * sc, v[5] * sc, h.z, l.z);
+    umma::split2<0>(v[6] * sc, v[7] * sc, h.w, l.w);
+    *reinterpret_cast<uint4 *>(s.p(off) + umma::tile_off(r, 8 * b, C)) = h;
+    umma::tmem_st4u(ta_hi + 4 * b, h);
+    umma::tmem_st4u(ta_lo + 4 * b, l);
+}
+// hi half only (an operand only weight-gradient GEMMs read, with NS2B_WG1)
+template <int C>
+__device__ __forceinline__ void stage_blk_hi(const Smem &s, uint32_t off, int r, int b, const float *v, float sc) {
+    const uint4 h = make_uint4(pack_half2(v[0] * sc, v[1] * sc), pack_half2(v[2] * sc, v[3] * sc),
+                               pack_half2(v[4] * sc, v[5] * sc), pack_half2(v[6] * sc, v[7] * sc));
+    *reinterpret_cast<uint4 *>(s.p(off) + umma::tile_off(r, 8 * b, C)) = h;
+}
+
 enum Acc { aC3, aC2, aC1, aH2, aH1a, aH1b, NACC };
 
 // Fold one TMEM weight-gradient accumulator (scaled by 2^-e) into global memory.  All
@@ -1614,6 +1658,27 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     static_assert(IN_BYTES <= TEB, "per-tile inputs fit in TE's free half");
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+#ifdef NS2B_BWD_TA
+    // the chain GEMMs' A operands in TMEM (the second chain slot: hi | lo), one result slot
+    constexpr uint32_t TA_H = TB_SB, TA_L = TB_SB + 32, SLB = TB_SA;
+#define STG_A(C, off, part, b, v, sc) stage_blk_ta<C>(S, off, r, b, v, sc, my + TA_H, my + TA_L)
+#define PUB_A()              \
+    do {                     \
+        umma::tmem_st_wait(); \
+        publish();           \
+    } while (0)
+#define CHAIN(NK, d, off, part, KC, bop, idesc) umma::gemm3t<NK>(d, tb + TA_H, tb + TA_L, bop, idesc, false)
+#else
+    constexpr uint32_t SLB = TB_SB;
+#define STG_A(C, off, part, b, v, sc) stage_blk<C>(S, off, part, r, b, v, sc)
+#define PUB_A() publish()
+#define CHAIN(NK, d, off, part, KC, bop, idesc) umma::gemm3w<NK>(d, S.K(off, part, KC), bop, idesc, false)
+#endif
+#ifdef NS2B_WG1  // operands only the weight-gradient GEMMs read: hi halves
+#define STG_W(C, off, part, b, v, sc) stage_blk_hi<C>(S, off, r, b, v, sc)
+#else
+#define STG_W(C, off, part, b, v, sc) stage_blk<C>(S, off, part, r, b, v, sc)
+#endif
     const int qd = warp & 3, qt = warp >> 2;
     const int r = 32 * qd + lane;
     const int E = 3 + 2 * f.L;
@@ -1832,8 +1897,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             PMARK(20);
             #pragma unroll 1
             for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
-                if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, dlog, pow2i(eD));
-                publish();
+                if (qt < 2) STG_A(16, TD, TDB, qt, dlog, pow2i(eD));
+                PUB_A();
                 if (pass) break;
                 PMARK(1);
                 if (t < NSLOT) sh.slot_mx[PS.par ^ 1][t] = 0u;
@@ -1843,7 +1908,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         {
             const bool acc = acc_begin(aC3, eA2c + eD);
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
-                umma::gemm3w<1>(tb + TB_SA, S.K(TD, TDB, 16), S.MN(WC3, WC3B, 64), ID_KM(64), false);
+                CHAIN(1, tb + TB_SA, TD, TDB, 16, S.MN(WC3, WC3B, 64), ID_KM(64));
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_w, ph_w));
                 WG_ACT_A<8>(tb + TB_DC3, S.MN(TW, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
@@ -1874,7 +1939,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TY, T64B, r, i ? b1 : b0, u[i], s);
+                for (int i = 0; i < 2; ++i) STG_A(64, TY, T64B, i ? b1 : b0, u[i], s);
             };
             #pragma unroll 1
             for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
@@ -1888,7 +1953,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         {
             const bool acc = acc_begin(aC2, eU2 + eA1c);
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
-                umma::gemm3w<4>(tb + TB_SB, S.K(TY, T64B, 64), S.MN(WC2, WC2B, 64), ID_KM(64), false);
+                CHAIN(4, tb + SLB, TY, T64B, 64, S.MN(WC2, WC2B, 64), ID_KM(64));
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_z, ph_z));
                 WG_ACT_B<8>(tb + TB_DC2, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 64), ID_WG(64), acc);
@@ -1904,7 +1969,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             const float sc = pow2i(-(eU2 + eC2));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
+                umma::tmem_ld8(my + SLB + 8 * (i ? b1 : b0), u[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
@@ -1916,7 +1981,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             auto stg = [&](int e) {
                 const float s = pow2i(e);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], s);
+                for (int i = 0; i < 2; ++i) STG_A(64, TX, T64B, i ? b1 : b0, u[i], s);
             };
             #pragma unroll 1
             for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
@@ -1930,7 +1995,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         {
             const bool acc = acc_begin(aC1, eU1 + eCin);
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
-                umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WC1, WC1B, 32), ID_KM(32), false);
+                CHAIN(4, tb + TB_SA, TX, T64B, 64, S.MN(WC1, WC1B, 32), ID_KM(32));
                 umma::commit_elect(mbar);
                 // TW is free (dC3 of B0 completed before B1's chain GEMM did): next tile's A2c
                 if (lane == 0 && has_next) dma(TW, fwt(ntile) + FW_A2C, T64B, mb_w);
@@ -1985,8 +2050,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             PS.contrib(kDly, m);
             #pragma unroll 1
             for (int pass = 0;; ++pass) {  // stage; restage once if the predicted exponent missed
-                if (qt < 2) stage_blk<16>(S, TD, TDB, r, qt, blk, pow2i(eDLY));
-                publish();
+                if (qt < 2) STG_A(16, TD, TDB, qt, blk, pow2i(eDLY));
+                PUB_A();
                 if (pass) break;
                 PMARK(10);
                 if (PS.check(kDly, eDLY)) break;
@@ -1995,7 +2060,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         {
             const bool acc = acc_begin(aH2, eA1 + eDLY);
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
-                umma::gemm3w<1>(tb + TB_SB, S.K(TD, TDB, 16), S.MN(WH2, WH2B, 64), ID_KM(64), false);
+                CHAIN(1, tb + SLB, TD, TDB, 16, S.MN(WH2, WH2B, 64), ID_KM(64));
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_a, ph_a));
                 WG_ACT_A<8>(tb + TB_DH2, S.MN(TA1, T64B, 64), S.MN(TD, TDB, 16), ID_WG(16), acc);
@@ -2032,8 +2097,8 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
 #pragma unroll
             for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fmaxf(fabsf(mv[0][k]), fabsf(mv[1][k])));
             const float sm = pow2i(emv);
-            stage_blk<48>(S, TZ, T64B, r, qt, mv[0], sm);
-            if (qt < 2) stage_blk<48>(S, TZ, T64B, r, qt + 4, mv[1], sm);
+            STG_W(48, TZ, T64B, qt, mv[0], sm);
+            if (qt < 2) STG_W(48, TZ, T64B, qt + 4, mv[1], sm);
             return mm;
         };
         int eMV = PS.guess(kMv);
@@ -2058,7 +2123,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             const float sc4 = pow2i(-(eDLY + eH2));
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                umma::tmem_ld8(my + TB_SB + 8 * (i ? b1 : b0), u[i]);
+                umma::tmem_ld8(my + SLB + 8 * (i ? b1 : b0), u[i]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
@@ -2070,17 +2135,17 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             auto stg = [&](int eu) {
                 const float su = pow2i(eu);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) stage_blk<64>(S, TX, T64B, r, i ? b1 : b0, u[i], su);
+                for (int i = 0; i < 2; ++i) STG_A(64, TX, T64B, i ? b1 : b0, u[i], su);
             };
             stg(eU);
-            publish();
+            PUB_A();
             PMARK(13);
             const bool oku = PS.check(kU, eU);
             const bool okm = PS.check(kMv, eMV);
             if (!(oku && okm)) {  // (uniform) restage whichever missed its exponent window
                 if (!oku) stg(eU);
                 if (!okm) mv_stage(eMV);
-                publish();
+                PUB_A();
                 PMARK(14);
             }
         }
@@ -2091,11 +2156,11 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             const bool acca = acc_begin(aH1a, eU + eE);
             const bool accb = acc_begin(aH1b, eMV);
             if (warp == kMmaWarp) {  // converged MMA warp; elect.sync picks the issuing lane
-                umma::gemm3w<4>(tb + TB_SA, S.K(TX, T64B, 64), S.MN(WH1, WH1B, 48), ID_KM(48), false);
+                CHAIN(4, tb + TB_SA, TX, T64B, 64, S.MN(WH1, WH1B, 48), ID_KM(48));
                 umma::commit_elect(mbar);
                 PWAIT(umma::mbar_wait(mb_e, ph_e));
                 WG_ACT_B<8>(tb + TB_DH1A, S.MN(TX, T64B, 64), S.MN(TE, TEB, 48), ID_WG(48), acca);
-                umma::gemm2a<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
+                WG_MASK<8>(tb + TB_DH1B, S.MN(TY, T64B, 64), S.MN(TZ, T64B, 48), ID_WG(48), accb);
                 umma::commit_elect(mbarw);
             }
             ph_e ^= 1u;
@@ -2170,6 +2235,10 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tb, 512);
 }
+#undef STG_A
+#undef PUB_A
+#undef CHAIN
+#undef STG_W
 
 // ---------------------------------------------------------------------------
 // Gather kernel (one pass per step): per 128-sample tile, trilinear features and

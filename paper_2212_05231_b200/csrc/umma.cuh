@@ -456,6 +456,68 @@ __device__ __forceinline__ void gemm2a(uint32_t tmem_d, const Operand &a, const 
     }
 }
 
+// One term (A_hi B_hi): both operands taken as their fp16 hi parts.
+__device__ __forceinline__ void mma1_elect(uint32_t tmem_d, uint64_t ah, uint64_t bh, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(ah), "l"(bh), "r"(idesc), "r"(accumulate));
+}
+template <int NK>
+__device__ __forceinline__ void gemm1(uint32_t tmem_d, const Operand &a, const Operand &b, uint32_t idesc,
+                                      bool accumulate) {
+    uint64_t ah = make_desc(a.hi, a.lbo, a.sbo);
+    uint64_t bh = make_desc(b.hi, b.lbo, b.sbo);
+    const uint64_t sa = (2 * a.lbo) >> 4, sb = (2 * b.lbo) >> 4;
+    mma1_elect(tmem_d, ah, bh, idesc, accumulate ? 1u : 0u);
+#pragma unroll 1
+    for (int k = 1; k < NK; ++k) {
+        ah += sa;
+        bh += sb;
+        mma1_elect(tmem_d, ah, bh, idesc, 1u);
+    }
+}
+
+// ---- A operand in tensor memory (the "TS" form): A is M x K fp16, row m in lane m, K
+// elements packed two per 32-bit column (even k in the low half), K-major only.  A K step
+// of 16 elements is 8 columns.  B stays a shared-memory descriptor.
+__device__ __forceinline__ void tmem_st4u(uint32_t taddr, uint4 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// three-term split, A from TMEM: [A_hi] B_hi + [A_lo] B_hi + [A_hi] B_lo
+__device__ __forceinline__ void mma3t_elect(uint32_t tmem_d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+        "setp.eq.b32 p, 1, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate));
+}
+template <int NK>
+__device__ __forceinline__ void gemm3t(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, const Operand &b,
+                                       uint32_t idesc, bool accumulate) {
+    uint64_t bh = make_desc(b.hi, b.lbo, b.sbo), bl = make_desc(b.lo, b.lbo, b.sbo);
+    const uint64_t sb = (2 * b.lbo) >> 4;
+    mma3t_elect(tmem_d, a_hi, a_lo, bh, bl, idesc, accumulate ? 1u : 0u);
+#pragma unroll 1
+    for (int k = 1; k < NK; ++k) {
+        a_hi += 8;
+        a_lo += 8;
+        bh += sb;
+        bl += sb;
+        mma3t_elect(tmem_d, a_hi, a_lo, bh, bl, idesc, 1u);
+    }
+}
+
 // commit by the elected lane (the one that issued the MMAs)
 __device__ __forceinline__ void commit_elect(uint64_t *mbar) {
     asm volatile(
