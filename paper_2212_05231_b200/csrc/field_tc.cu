@@ -2241,6 +2241,664 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
 #undef STG_W
 
 // ---------------------------------------------------------------------------
+// MLP backward, pipelined across two thread groups (field_bwd2_kernel, the default; NS2B_BWD=1
+// selects field_bwd_kernel above).  The backward of a tile is a strict chain of five
+// MMA round trips, so one tile in flight leaves the SM idle while each phase waits on its
+// GEMM.  Here the colour-net half of the chain (group C, warps 0-7) runs one tile ahead of
+// the SDF-net half (group S, warps 8-15):
+//   C0 dlog -> U2 = DLOG C3,      dC3 += A2c^T DLOG
+//   C1 u2   -> U1 = U2 C2,        dC2 += U2^T A1c
+//   C2 u1   -> DCIN = U1 C1,      dC1 += U1^T CIN
+//   C3 q, dly (and the m1 mask words) -> a two-slot handoff ring in shared memory
+//   S0 dly  -> U = DLY H2,        dH2 += A1^T DLY;   MV = [J q, q] and M1 staged
+//   S1 u    -> DE = U H1,         dH1 += U^T E,  G += M1^T MV   (Theorem 1, as field_bwd_kernel)
+//   S2 DE, q -> the scatter's inputs
+// so while one group waits on its GEMM the other runs its epilogue.  Each group has its
+// own named barrier (256 threads), MMA-issuing warp, DMA thread, mbarriers, staging-exponent
+// predictions and weight-gradient accumulators; a thread owns 32 columns of its row (half
+// qh = blocks 4qh..4qh+3 of a 64-wide tile).  Chain GEMMs read A from tensor memory (each
+// group has its own A region), weight-gradient GEMMs take fp16 x fp16 operands (NS2B_WG1).
+// J is read from L2 by group S (prefetched a tile ahead), not kept in TMEM.
+// Shared memory: weights 44 KB | C: DLOG 4 | A2c 16 | A1c 16 | U2/U1 16 | CIN 8 | inputs 2 x 9.2 |
+// S: DLY 4 | A1 16 | U 16 | M1 16 | MV 12 | E 12 | handoff 2 x 10.75  (~220 KB).
+// TMEM: C dC2 64 | dC1 32 | dC3 16 | slot 64 | A 64;  S dH2 16 | dH1a 48 | G 48 | slot 64 | A 64.
+namespace b2 {
+constexpr uint32_t TDC = TE;                    // DLOG hi   128 x 16
+constexpr uint32_t TWC = TDC + TDB;             // A2c hi    128 x 64
+constexpr uint32_t TZC = TWC + T64B;            // A1c hi
+constexpr uint32_t TYC = TZC + T64B;            // U2 hi -> U1 hi
+constexpr uint32_t TCC = TYC + T64B;            // CIN hi    128 x 32
+constexpr uint32_t IN_MK = 0, IN_NC = IN_MK + 4 * TILE * 8, IN_DC = IN_NC + NCROWS * TILE * 4,
+                   IN_DS = IN_DC + 3 * TILE * 4, IN_EX = IN_DS + TILE * 4, IN_BYTES = IN_EX + 16;
+constexpr uint32_t IN_STRIDE = (IN_BYTES + 127) / 128 * 128;
+constexpr uint32_t TIN0 = TCC + TCB;            // per-tile inputs, two slots
+constexpr uint32_t TDS = TIN0 + 2 * IN_STRIDE;  // DLY hi    128 x 16
+constexpr uint32_t TA1S = TDS + TDB;            // A1 hi
+constexpr uint32_t TXS = TA1S + T64B;           // U hi
+constexpr uint32_t TYS = TXS + T64B;            // M1
+constexpr uint32_t TMV = TYS + T64B;            // MV hi     128 x 48
+constexpr uint32_t TES = TMV + TEB;             // E hi      128 x 48
+constexpr uint32_t H_Q = 0, H_DLY = H_Q + 3 * TILE * 4, H_M1 = H_DLY + 16 * TILE * 4, H_BYTES = H_M1 + 2 * TILE * 4;
+constexpr uint32_t TH0 = TES + TEB;             // handoff ring, two slots
+constexpr uint32_t SMEM = TH0 + 2 * H_BYTES;
+static_assert(SMEM <= 220 * 1024, "bwd2 shared memory");
+// TMEM columns
+constexpr uint32_t C_DC2 = 0, C_DC1 = 64, C_DC3 = 96, C_SL = 112, C_AH = 176, C_AL = 208;
+constexpr uint32_t S_DH2 = 240, S_DH1A = 256, S_G = 304, S_SL = 352, S_AH = 416, S_AL = 448;
+}  // namespace b2
+
+// Fold one weight-gradient accumulator (scaled by 2^-e) into global memory: the 8 warps of
+// a group (lane quadrant qd, half qh) read lanes 0-15 of their quadrant (M = 64 rows).
+__device__ __noinline__ void fold_acc2(int j, int e, uint32_t my, int qh, int E, const float *__restrict__ h2row0,
+                                       const float *__restrict__ sdf_w, float *__restrict__ g_sdf,
+                                       float *__restrict__ g_color) {
+    using namespace b2;
+    const int lane = threadIdx.x & 31, qd = (threadIdx.x >> 5) & 3;
+    const int jrow = 16 * qd + lane;
+    const float sc = pow2i(-e);
+    float d[8];
+    switch (j) {
+    case aC3:  // dC3^T: row = hidden unit, col = output (3)
+        umma::tmem_ld8(my + C_DC3, d);
+        if (lane < 16 && qh == 0)
+            for (int o = 0; o < 3; ++o) atomicAdd(g_color + H * CIN + H * H + o * H + jrow, d[o] * sc);
+        break;
+    case aC2:
+        for (int b = qh; b < 8; b += 2) {
+            umma::tmem_ld8(my + C_DC2 + 8 * b, d);
+            if (lane < 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) atomicAdd(g_color + H * CIN + jrow * H + 8 * b + k, d[k] * sc);
+        }
+        break;
+    case aC1:
+        for (int b = qh; b < 4; b += 2) {
+            umma::tmem_ld8(my + C_DC1 + 8 * b, d);
+            if (lane < 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (8 * b + k < CIN) atomicAdd(g_color + jrow * CIN + 8 * b + k, d[k] * sc);
+        }
+        break;
+    case aH2:  // dH2^T: row = hidden unit, col = output unit
+        umma::tmem_ld8(my + S_DH2 + 8 * qh, d);
+        if (lane < 16)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) atomicAdd(g_sdf + H * (E + 1) + (8 * qh + k) * H + jrow, d[k] * sc);
+        break;
+    case aH1a:
+        for (int b = qh; b < 6; b += 2) {
+            umma::tmem_ld8(my + S_DH1A + 8 * b, d);
+            if (lane < 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int rc = h1_col(8 * b + k, E);
+                    if (rc >= 0) atomicAdd(g_sdf + jrow * (E + 1) + rc, d[k] * sc);
+                }
+        }
+        break;
+    default: {  // G = M1^T MV: dH1 += H2[0][j] G[j],  dH2[0][j] += H1[j] . G[j]
+        float dot = 0.f;
+        const float h2j = lane < 16 ? h2row0[jrow] : 0.f;
+        for (int b = qh; b < 6; b += 2) {
+            umma::tmem_ld8(my + S_G + 8 * b, d);
+            if (lane < 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int rc = h1_col(8 * b + k, E);
+                    if (rc >= 0) {
+                        atomicAdd(g_sdf + jrow * (E + 1) + rc, h2j * d[k] * sc);
+                        dot = fmaf(sdf_w[jrow * (E + 1) + rc], d[k], dot);
+                    }
+                }
+        }
+        if (lane < 16 && dot != 0.f) atomicAdd(g_sdf + H * (E + 1) + jrow, dot * sc);
+        break;
+    }
+    }
+}
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
+                  const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
+                  const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
+                  Workspace ws) {
+    using namespace b2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // C: [0] chain, [1] dC2 done, [2] dC1 done, [3] A2c, [4] A1c, [5] CIN, [6..7] inputs;
+    // S: [8] chain, [9] WG, [10] A1, [11] E;  handoff: [12..13] full, [14..15] empty
+    __shared__ uint64_t bars[16];
+    __shared__ uint32_t wmax[6];
+    __shared__ int wexp[6];
+    __shared__ float h2row0[H];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ uint32_t gmx[2][2][NSLOT];
+    __shared__ int gpred[2][NSLOT];
+    const Smem S{smem_raw};
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int g = warp >> 3, gw = warp & 7, tg = t & 255;
+    const int qd = gw & 3, qh = gw >> 2;
+    const int r = 32 * qd + lane;
+    const int E = 3 + 2 * f.L;
+    const int NA = f.n_active;
+    // ---- setup (all 512 threads)
+    if (t < H) h2row0[t] = f.sdf_w[H * (E + 1) + t];
+    load_weight_tiles<false>(S, f, wmax, wexp);
+    if (t < 2 * NSLOT) {
+        gmx[t / NSLOT][0][t % NSLOT] = 0u;
+        gmx[t / NSLOT][1][t % NSLOT] = 0u;
+        gpred[t / NSLOT][t % NSLOT] = 0;
+    }
+    if (t == 0) {
+        for (int i = 0; i < 12; ++i) umma::mbar_init(bars + i, 1);
+        for (int i = 12; i < 16; ++i) umma::mbar_init(bars + i, 256);
+        umma::fence_barrier_init();
+    }
+    if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 512);
+    publish();
+    const int eH1 = wexp[0], eH2 = wexp[1], eC1 = wexp[2], eC2 = wexp[3], eC3 = wexp[4];
+    const uint32_t tb = tmem_base_sh;
+    const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
+    PredScaleG PS{gmx[g], gpred[g], 1, tg == 0};
+    const int P = *count;
+    const float Pf = eik_count ? static_cast<float>(*eik_count) : 1.f;
+    const bool gn_fused = ws.flags[0] != 0;
+    const bool mma_w = gw == 7;                 // the group's MMA-issuing warp
+    const bool dma_t = gw == 6 && lane == 0;    // the group's DMA thread
+    const int64_t G = gridDim.x;
+    auto fwt = [&](int64_t tl) { return ws.fw_tiles + tl * static_cast<int64_t>(FWB); };
+    auto dma = [&](uint32_t soff, const uint8_t *gp, uint32_t bytes, uint64_t *mb) {
+        umma::bulk_g2s<true>(S.p(soff), gp, bytes, mb);
+    };
+    int acc_e[3];
+    bool acc_live[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        acc_e[j] = 0;
+        acc_live[j] = false;
+    }
+    const int acc0 = g == 0 ? aC3 : aH2;  // this group's accumulators: acc0 .. acc0 + 2
+    auto fold = [&](int jj) {
+        fold_acc2(acc0 + jj, acc_e[jj], my, qh, E, h2row0, f.sdf_w, g_sdf, g_color);
+        acc_live[jj] = false;
+    };
+    auto acc_begin = [&](int jj, int e) -> bool {  // group-uniform
+        if (acc_live[jj] && acc_e[jj] != e) {
+            fold(jj);
+            umma::fence_before_sync();
+            group_sync(g);
+            umma::fence_after_sync();
+        }
+        const bool accumulate = acc_live[jj];
+        acc_e[jj] = e;
+        acc_live[jj] = true;
+        return accumulate;
+    };
+    if (g == 0) {
+        // =============================================== group C: colour-net backward
+        uint64_t *mbar = bars, *mbar2 = bars + 1, *mbar3 = bars + 2, *mb_w = bars + 3, *mb_z = bars + 4,
+                 *mb_c = bars + 5, *mb_in = bars + 6, *hfull = bars + 12, *hempty = bars + 14;
+        uint32_t ph = 0, ph2 = 0, ph3 = 0, ph_w = 0, ph_z = 0, ph_c = 0, ph_in[2] = {0, 0}, ph_he[2] = {0, 0};
+        const bool in_dma_ok =
+            ((reinterpret_cast<uintptr_t>(dl_dc) | reinterpret_cast<uintptr_t>(dl_dsdf)) & 15u) == 0;
+        auto in_full = [&](int64_t tl) { return in_dma_ok && (tl + 1) * TILE <= P; };
+        auto in_dma = [&](int64_t tl, int s) {  // one thread
+            const uint32_t base = TIN0 + s * IN_STRIDE;
+            umma::mbar_expect_tx(mb_in + s, IN_BYTES);
+            umma::bulk_g2s_tx(S.p(base + IN_MK), ws.fw_mask + tl * 4 * TILE, 4 * TILE * 8, mb_in + s);
+            umma::bulk_g2s_tx(S.p(base + IN_NC), ws.fw_nc + tl * NCROWS * TILE, NCROWS * TILE * 4, mb_in + s);
+            umma::bulk_g2s_tx(S.p(base + IN_DC), dl_dc + 3 * tl * TILE, 3 * TILE * 4, mb_in + s);
+            umma::bulk_g2s_tx(S.p(base + IN_DS), dl_dsdf + tl * TILE, TILE * 4, mb_in + s);
+            umma::bulk_g2s_tx(S.p(base + IN_EX), ws.fw_exp + tl, 16, mb_in + s);
+        };
+        const int64_t t0 = blockIdx.x;
+        if (dma_t && t0 * TILE < P) {
+            dma(TWC, fwt(t0) + FW_A2C, T64B, mb_w);
+            dma(TZC, fwt(t0) + FW_A1C, T64B, mb_z);
+            dma(TCC, fwt(t0) + FW_CIN, TCB, mb_c);
+            if (in_full(t0)) in_dma(t0, 0);
+        }
+        int it = 0;
+        for (int64_t tile = t0; tile * TILE < P; tile += G, ++it) {
+            const int64_t p = tile * TILE + r;
+            const bool valid = p < P;
+            const int64_t ntile = tile + G;
+            const bool has_next = ntile * TILE < P;
+            const int s = it & 1;
+            PS.par ^= 1;
+            if (dma_t && has_next) {
+                umma::prefetch_l2(fwt(ntile), FWB);
+                if (in_full(ntile)) in_dma(ntile, s ^ 1);  // slot s^1 was read during the previous tile
+            }
+            // ---- per-sample inputs: masks (byte qh of each quarter word = blocks 4qh..4qh+3), dL/dc,
+            // c, dL/dsdf, normal / Eikonal cotangent, the forward's exponents
+            uint32_t m1 = 0u, mc1 = 0u, mc2 = 0u;
+            float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, cc0 = 0.f, cc1 = 0.f, cc2 = 0.f, gd = 0.f, n0 = 0.f, n1 = 0.f,
+                  n2 = 0.f;
+            int4 fe;
+            if (in_full(tile)) {
+                umma::mbar_wait(mb_in + s, ph_in[s]);
+                ph_in[s] ^= 1u;
+                const uint8_t *base = S.p(TIN0 + s * IN_STRIDE);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint2 w = *reinterpret_cast<const uint2 *>(base + IN_MK + 8 * (q * TILE + r));
+                    m1 |= ((w.x >> (8 * qh)) & 0xFFu) << (8 * q);
+                    mc1 |= ((w.x >> (16 + 8 * qh)) & 0xFFu) << (8 * q);
+                    mc2 |= ((w.y >> (8 * qh)) & 0xFFu) << (8 * q);
+                }
+                const float *nc = reinterpret_cast<const float *>(base + IN_NC) + r;
+                const float *dc = reinterpret_cast<const float *>(base + IN_DC) + 3 * r;
+                gc0 = dc[0];
+                gc1 = dc[1];
+                gc2 = dc[2];
+                cc0 = nc[3 * TILE];
+                cc1 = nc[4 * TILE];
+                cc2 = nc[5 * TILE];
+                gd = reinterpret_cast<const float *>(base + IN_DS)[r];
+                n0 = nc[0];
+                n1 = nc[TILE];
+                n2 = nc[2 * TILE];
+                fe = *reinterpret_cast<const int4 *>(base + IN_EX);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint2 w = ws.fw_mask[(tile * 4 + q) * TILE + r];
+                    m1 |= ((w.x >> (8 * qh)) & 0xFFu) << (8 * q);
+                    mc1 |= ((w.x >> (16 + 8 * qh)) & 0xFFu) << (8 * q);
+                    mc2 |= ((w.y >> (8 * qh)) & 0xFFu) << (8 * q);
+                }
+                fe = ws.fw_exp[tile];
+                if (valid) {
+                    const float *nc = ws.fw_nc + tile * NCROWS * TILE + r;
+                    gc0 = dl_dc[3 * p];
+                    gc1 = dl_dc[3 * p + 1];
+                    gc2 = dl_dc[3 * p + 2];
+                    cc0 = nc[3 * TILE];
+                    cc1 = nc[4 * TILE];
+                    cc2 = nc[5 * TILE];
+                    gd = dl_dsdf[p];
+                    n0 = nc[0];
+                    n1 = nc[TILE];
+                    n2 = nc[2 * TILE];
+                }
+            }
+            const int eA1c = fe.z, eA2c = fe.w, eCin = fe.y;
+            float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
+            if (valid) {
+                if (dl_dn_extra) {
+                    gn0 = dl_dn_extra[3 * p];
+                    gn1 = dl_dn_extra[3 * p + 1];
+                    gn2 = dl_dn_extra[3 * p + 2];
+                }
+                if (gn_fused) {  // fused by the forward (same arithmetic)
+                    gn0 += n0;
+                    gn1 += n1;
+                    gn2 += n2;
+                } else if (eik_w != 0.f) {  // trainer.py:229-235 (fp32, numpy's order)
+                    const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+                    const float coef = eik_w * (2.f * (nn - 1.f) / fmaxf(nn, 1e-12f));
+                    gn0 += coef * n0 / Pf;
+                    gn1 += coef * n1 / Pf;
+                    gn2 += coef * n2 / Pf;
+                }
+            }
+            // ------------------------------------------- C0: dlog -> U2, dC3
+            int eD;
+            {
+                float dlog[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) dlog[k] = 0.f;
+                if (qh == 0) {  // field.py:304
+                    dlog[0] = gc0 * cc0 * (1.f - cc0);
+                    dlog[1] = gc1 * cc1 * (1.f - cc1);
+                    dlog[2] = gc2 * cc2 * (1.f - cc2);
+                }
+                eD = PS.guess(kDlog);
+                PS.contrib(kDlog, fmaxf(fabsf(dlog[0]), fmaxf(fabsf(dlog[1]), fabsf(dlog[2]))));
+#pragma unroll 1
+                for (int pass = 0;; ++pass) {
+                    stage_blk_ta<16>(S, TDC, r, qh, dlog, pow2i(eD), my + C_AH, my + C_AL);
+                    umma::tmem_st_wait();
+                    group_publish(0);
+                    if (pass) break;
+                    if (tg < NSLOT) gmx[0][PS.par ^ 1][tg] = 0u;
+                    if (PS.check(kDlog, eD)) break;
+                }
+            }
+            {
+                const bool acc = acc_begin(0, eA2c + eD);
+                if (mma_w) {
+                    umma::gemm3t<1>(tb + C_SL, tb + C_AH, tb + C_AL, S.MN(WC3, WC3B, 64), ID_KM(64), false);
+                    umma::commit_elect(mbar);
+                    umma::mbar_wait(mb_w, ph_w);
+                    umma::gemm1<8>(tb + C_DC3, S.MN(TWC, T64B, 64), S.MN(TDC, TDB, 16), ID_WG(16), acc);
+                }
+                ph_w ^= 1u;
+            }
+            wait_mma(mbar, ph);
+            // ------------------------------------------- C1: u2 -> U1, dC2
+            int eU2;
+            {
+                float u[4][8], m = 0.f;
+                const float sc = pow2i(-(eD + eC3));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    umma::tmem_ld8(my + C_SL + 8 * (4 * qh + i), u[i]);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        u[i][k] = ((mc2 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                        m = fmaxf(m, fabsf(u[i][k]));
+                    }
+                }
+                eU2 = PS.guess(kU2);
+                PS.contrib(kU2, m);
+#pragma unroll 1
+                for (int pass = 0;; ++pass) {
+                    const float s2 = pow2i(eU2);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TYC, r, 4 * qh + i, u[i], s2, my + C_AH, my + C_AL);
+                    umma::tmem_st_wait();
+                    group_publish(0);
+                    if (pass) break;
+                    if (PS.check(kU2, eU2)) break;
+                }
+            }
+            {
+                const bool acc = acc_begin(1, eU2 + eA1c);
+                if (mma_w) {
+                    umma::gemm3t<4>(tb + C_SL, tb + C_AH, tb + C_AL, S.MN(WC2, WC2B, 64), ID_KM(64), false);
+                    umma::commit_elect(mbar);
+                    umma::mbar_wait(mb_z, ph_z);
+                    umma::gemm1<8>(tb + C_DC2, S.MN(TYC, T64B, 64), S.MN(TZC, T64B, 64), ID_WG(64), acc);
+                    umma::commit_elect(mbar2);  // dC2 has read U2 (TY) and A1c (TZ)
+                }
+                ph_z ^= 1u;
+            }
+            wait_mma(mbar, ph);
+            // ------------------------------------------- C2: u1 -> DCIN, dC1
+            int eU1;
+            {
+                float u[4][8], m = 0.f;
+                const float sc = pow2i(-(eU2 + eC2));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    umma::tmem_ld8(my + C_SL + 8 * (4 * qh + i), u[i]);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                        m = fmaxf(m, fabsf(u[i][k]));
+                    }
+                }
+                eU1 = PS.guess(kU1);
+                PS.contrib(kU1, m);
+                wait_mma(mbar2, ph2);  // U1 restages TY
+                if (dma_t && has_next) {  // dC3 (before U1's GEMM) and dC2 are done: next A2c, A1c
+                    dma(TWC, fwt(ntile) + FW_A2C, T64B, mb_w);
+                    dma(TZC, fwt(ntile) + FW_A1C, T64B, mb_z);
+                }
+#pragma unroll 1
+                for (int pass = 0;; ++pass) {
+                    const float s1 = pow2i(eU1);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TYC, r, 4 * qh + i, u[i], s1, my + C_AH, my + C_AL);
+                    umma::tmem_st_wait();
+                    group_publish(0);
+                    if (pass) break;
+                    if (PS.check(kU1, eU1)) break;
+                }
+            }
+            {
+                const bool acc = acc_begin(2, eU1 + eCin);
+                if (mma_w) {
+                    umma::gemm3t<4>(tb + C_SL, tb + C_AH, tb + C_AL, S.MN(WC1, WC1B, 32), ID_KM(32), false);
+                    umma::commit_elect(mbar);
+                    umma::mbar_wait(mb_c, ph_c);
+                    umma::gemm1<8>(tb + C_DC1, S.MN(TYC, T64B, 64), S.MN(TCC, TCB, 32), ID_WG(32), acc);
+                    umma::commit_elect(mbar3);  // dC1 has read U1 (TY) and CIN (TC)
+                }
+                ph_c ^= 1u;
+            }
+            wait_mma(mbar, ph);
+            // ------------------------------------------- C3: q, dly, m1 -> the handoff ring
+            {
+                const float sc3 = pow2i(-(eU1 + eC1));
+                float c0[8], c1[8];
+                umma::tmem_ld8(my + C_SL + 16 * qh, c0);
+                umma::tmem_ld8(my + C_SL + 16 * qh + 8, c1);
+                const int hs = it & 1;
+                if (it >= 2) {  // group S has read this slot (tile it - 2)
+                    umma::mbar_wait(hempty + hs, ph_he[hs]);
+                    ph_he[hs] ^= 1u;
+                }
+                float *hq = reinterpret_cast<float *>(S.p(TH0 + hs * H_BYTES + H_Q)) + r;
+                float *hd = reinterpret_cast<float *>(S.p(TH0 + hs * H_BYTES + H_DLY)) + r;
+                uint32_t *hm = reinterpret_cast<uint32_t *>(S.p(TH0 + hs * H_BYTES + H_M1)) + r;
+                if (qh == 0) {  // field.py:308-312: q = dL/dn, dly = [dd + dcin[9], dcin[10..24]]
+                    hq[0] = gn0 + c0[3] * sc3;
+                    hq[TILE] = gn1 + c0[4] * sc3;
+                    hq[2 * TILE] = gn2 + c0[5] * sc3;
+                    hd[0] = gd + c1[1] * sc3;
+#pragma unroll
+                    for (int k = 1; k < 7; ++k) hd[k * TILE] = c1[1 + k] * sc3;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) hd[(7 + k) * TILE] = c0[k] * sc3;
+                    hd[15 * TILE] = c1[0] * sc3;
+                }
+                hm[qh * TILE] = m1;
+                umma::mbar_arrive(hfull + hs);
+            }
+            // dC1 (behind the DCIN GEMM) has read CIN: the next tile's CIN
+            if (dma_t && has_next) {
+                umma::mbar_wait(mbar3, ph3);
+                umma::fence_after_sync();
+                dma(TCC, fwt(ntile) + FW_CIN, TCB, mb_c);
+            }
+            ph3 ^= 1u;
+        }
+        // all of group C's MMAs have completed once the last tile's dC1 has
+        if (it > 0) {
+            ph3 ^= 1u;  // the last tile's dC1 phase
+            wait_mma(mbar3, ph3);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj)
+            if (acc_live[jj]) fold(jj);
+    } else {
+        // =============================================== group S: SDF-net backward
+        uint64_t *mbar = bars + 8, *mbarw = bars + 9, *mb_a = bars + 10, *mb_e = bars + 11, *hfull = bars + 12,
+                 *hempty = bars + 14;
+        uint32_t ph = 0, phw = 0, ph_a = 0, ph_e = 0, ph_hf[2] = {0, 0};
+        const int64_t t0 = blockIdx.x;
+        if (dma_t && t0 * TILE < P) {
+            dma(TA1S, fwt(t0) + FW_A1, T64B, mb_a);
+            dma(TES, ws.e_tiles + t0 * 2 * TEB, TEB, mb_e);
+        }
+        bool wpend = false;
+        int it = 0;
+        for (int64_t tile = t0; tile * TILE < P; tile += G, ++it) {
+            const int64_t ntile = tile + G;
+            const bool has_next = ntile * TILE < P;
+            PS.par ^= 1;
+            float *SBt = ws.sb + tile * SBROWS * TILE;
+            if (dma_t && has_next) {
+                umma::prefetch_l2(fwt(ntile) + FW_A1, T64B);
+                umma::prefetch_l2(ws.jac + ntile * JROWS * TILE, JROWS * TILE * 4);
+                umma::prefetch_l2(ws.e_tiles + ntile * 2 * TEB, TEB);
+            }
+            const int eE = ws.e_exp[tile];
+            const int eA1 = ws.fw_exp[tile].x;
+            // d feature/dx of this thread's 8 levels (L2; the handoff wait hides their latency)
+            const float *jt = ws.jac + tile * JROWS * TILE + r;
+            float jv[8][6];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) jv[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
+            // ------------------------------------------- S0: dly -> U, dH2; MV, M1
+            const int hs = it & 1;
+            umma::mbar_wait(hfull + hs, ph_hf[hs]);
+            ph_hf[hs] ^= 1u;
+            float q0, q1, q2, dly[8];
+            uint32_t m1;
+            {
+                const float *hq = reinterpret_cast<const float *>(S.p(TH0 + hs * H_BYTES + H_Q)) + r;
+                const float *hd = reinterpret_cast<const float *>(S.p(TH0 + hs * H_BYTES + H_DLY)) + r;
+                q0 = hq[0];
+                q1 = hq[TILE];
+                q2 = hq[2 * TILE];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) dly[k] = hd[(8 * qh + k) * TILE];
+                m1 = reinterpret_cast<const uint32_t *>(S.p(TH0 + hs * H_BYTES + H_M1))[qh * TILE + r];
+            }
+            umma::mbar_arrive(hempty + hs);
+            if (wpend) {  // the previous tile's dH1 / G GEMMs read U (TX), M1 (TY), MV, E
+                wait_mma(mbarw, phw);
+                wpend = false;
+                if (dma_t) dma(TES, ws.e_tiles + tile * 2 * TEB, TEB, mb_e);
+            }
+            int eDLY, eMV;
+            {
+                float md = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) md = fmaxf(md, fabsf(dly[k]));
+                eDLY = PS.guess(kDly);
+                PS.contrib(kDly, md);
+                // mvec = [J q (features), q, 0] (field.py:326-327): half qh holds levels 8qh..8qh+7
+                // (blocks 2qh, 2qh+1) and block 4 + qh (q / zeros)
+                float mv[3][8], mm = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    mv[i >> 2][2 * (i & 3)] = jv[i][0] * q0 + jv[i][1] * q1 + jv[i][2] * q2;
+                    mv[i >> 2][2 * (i & 3) + 1] = jv[i][3] * q0 + jv[i][4] * q1 + jv[i][5] * q2;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mv[2][k] = 0.f;
+                if (qh == 0) {
+                    mv[2][0] = q0;
+                    mv[2][1] = q1;
+                    mv[2][2] = q2;
+                }
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mm = fmaxf(mm, fabsf(mv[b][k]));
+                eMV = PS.guess(kMv);
+                PS.contrib(kMv, mm);
+                // M1 (exact in fp16: hi part only) -> TY
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
+                    auto h2 = [&](int k) {
+                        return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
+                    };
+                    *reinterpret_cast<uint4 *>(S.p(TYS) + umma::tile_off(r, 8 * (4 * qh + i), 64)) =
+                        make_uint4(h2(0), h2(2), h2(4), h2(6));
+                }
+#pragma unroll 1
+                for (int pass = 0;; ++pass) {
+                    stage_blk_ta<16>(S, TDS, r, qh, dly, pow2i(eDLY), my + S_AH, my + S_AL);
+                    const float sm = pow2i(eMV);
+                    stage_blk_hi<48>(S, TMV, r, 2 * qh, mv[0], sm);
+                    stage_blk_hi<48>(S, TMV, r, 2 * qh + 1, mv[1], sm);
+                    stage_blk_hi<48>(S, TMV, r, 4 + qh, mv[2], sm);
+                    umma::tmem_st_wait();
+                    group_publish(1);
+                    if (pass) break;
+                    if (tg < NSLOT) gmx[1][PS.par ^ 1][tg] = 0u;
+                    const bool okd = PS.check(kDly, eDLY);
+                    const bool okm = PS.check(kMv, eMV);
+                    if (okd && okm) break;
+                }
+            }
+            {
+                const bool acc = acc_begin(0, eA1 + eDLY);
+                if (mma_w) {
+                    umma::gemm3t<1>(tb + S_SL, tb + S_AH, tb + S_AL, S.MN(WH2, WH2B, 64), ID_KM(64), false);
+                    umma::commit_elect(mbar);
+                    umma::mbar_wait(mb_a, ph_a);
+                    umma::gemm1<8>(tb + S_DH2, S.MN(TA1S, T64B, 64), S.MN(TDS, TDB, 16), ID_WG(16), acc);
+                }
+                ph_a ^= 1u;
+            }
+            wait_mma(mbar, ph);
+            // ------------------------------------------- S1: u -> DE, dH1, G
+            int eU;
+            {
+                float u[4][8], mu = 0.f;
+                const float sc4 = pow2i(-(eDLY + eH2));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    umma::tmem_ld8(my + S_SL + 8 * (4 * qh + i), u[i]);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
+                        mu = fmaxf(mu, fabsf(u[i][k]));
+                    }
+                }
+                eU = PS.guess(kU);
+                PS.contrib(kU, mu);
+#pragma unroll 1
+                for (int pass = 0;; ++pass) {
+                    const float su = pow2i(eU);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TXS, r, 4 * qh + i, u[i], su, my + S_AH, my + S_AL);
+                    umma::tmem_st_wait();
+                    group_publish(1);
+                    if (pass) break;
+                    if (PS.check(kU, eU)) break;
+                }
+            }
+            {
+                // Theorem 1 through one accumulator (see field_bwd_kernel)
+                const bool acca = acc_begin(1, eU + eE);
+                const bool accb = acc_begin(2, eMV);
+                if (mma_w) {
+                    umma::gemm3t<4>(tb + S_SL, tb + S_AH, tb + S_AL, S.MN(WH1, WH1B, 48), ID_KM(48), false);
+                    umma::commit_elect(mbar);
+                    umma::mbar_wait(mb_e, ph_e);
+                    umma::gemm1<8>(tb + S_DH1A, S.MN(TXS, T64B, 64), S.MN(TES, TEB, 48), ID_WG(48), acca);
+                    umma::gemm1<8>(tb + S_G, S.MN(TYS, T64B, 64), S.MN(TMV, TEB, 48), ID_WG(48), accb);
+                    umma::commit_elect(mbarw);
+                }
+                ph_e ^= 1u;
+                wpend = true;
+            }
+            wait_mma(mbar, ph);
+            // ------------------------------------------- S2: scatter inputs
+            // dH2 (before the DE GEMM) is done: TA1 takes the next tile's A1
+            if (dma_t && has_next) dma(TA1S, fwt(ntile) + FW_A1, T64B, mb_a);
+            {
+                const float sde = pow2i(-(eU + eH1));
+                float de0[8], de1[8];
+                umma::tmem_ld8(my + S_SL + 16 * qh, de0);
+                umma::tmem_ld8(my + S_SL + 16 * qh + 8, de1);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (16 * qh + k < 2 * NA) __stcs(SBt + (16 * qh + k) * TILE + r, de0[k] * sde);
+                    if (16 * qh + 8 + k < 2 * NA) __stcs(SBt + (16 * qh + 8 + k) * TILE + r, de1[k] * sde);
+                }
+                if (qh == 0) {
+                    __stcs(SBt + 64 * TILE + r, q0);
+                    __stcs(SBt + 65 * TILE + r, q1);
+                    __stcs(SBt + 66 * TILE + r, q2);
+                }
+            }
+            // the next tile's S0 waits on its handoff slot; the slot reset of the exponent maxima
+            // happens after S0's barrier, so no tile-boundary barrier is needed
+        }
+        if (wpend) wait_mma(mbarw, phw);
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj)
+            if (acc_live[jj]) fold(jj);
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tb, 512);
+}
+
+// ---------------------------------------------------------------------------
 // Gather kernel (one pass per step): per 128-sample tile, trilinear features and
 // d feature/dx for the active levels (_kernels.py:67-119 without corner records),
 // 4 levels (32 float2 loads) in flight per thread.  Features are staged straight into
@@ -2601,6 +3259,9 @@ static int ensure_tc_attrs() {
         e = cudaFuncSetAttribute(field_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_BWD));
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(field_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(b2::SMEM));
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(field_fwd2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(SMEM_FWD2));
     if (e == cudaSuccess)
@@ -2623,6 +3284,28 @@ static bool use_fwd1() {
 }
 
 static int fwd_mode();
+
+// NS2B_BWD=1 selects the one-group backward (field_bwd_kernel); the default is the
+// two-group pipelined field_bwd2_kernel (input cotangents, want_xin, always use the former)
+static bool use_bwd1() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NS2B_BWD");
+        v = (e && atoi(e) == 1) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static void launch_bwd(const FieldDev &f, int64_t ntiles, const int32_t *count, const float *dl_dc,
+                       const float *dl_dsdf, const float *dl_dn_extra, float eik_w, const int64_t *eik_count,
+                       float *g_sdf, float *g_color, const Workspace &ws, int want_xin, cudaStream_t st) {
+    if (want_xin || use_bwd1())
+        field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_BWD, st>>>(
+            f, count, dl_dc, dl_dsdf, dl_dn_extra, eik_w, eik_count, g_sdf, g_color, ws, want_xin);
+    else
+        field_bwd2_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, b2::SMEM, st>>>(
+            f, count, dl_dc, dl_dsdf, dl_dn_extra, eik_w, eik_count, g_sdf, g_color, ws);
+}
 
 static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, float *sdf, float *colors,
                        float *normals, float *geo, double *eik_sum, const Workspace &ws, cudaStream_t st,
@@ -2702,9 +3385,8 @@ int field_stage_tc(int which, const ns2b_field_t *field, const float *pos32, con
         return check_launch("field_mlp_forward");
     case 2:
         NS2B_REQUIRE(eik_weight == 0.0 || eik_count != nullptr, "eik_count required with eik_weight");
-        tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-            f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws,
-            0);
+        tc::launch_bwd(f, ntiles, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count,
+                       grad_sdf, grad_color, ws, 0, st);
         return check_launch("field_mlp_backward");
     default:
         tc::field_scatter_kernel<<<grid_for(ntiles, 1, 1 << 30), tc::TILE, 0, st>>>(f, pos32, count, ws,
@@ -2750,9 +3432,8 @@ int field_backward_tc(const ns2b_field_t *field, const float *pos32, const int32
     if (capacity <= 0) return NS2B_OK;
     const int64_t ntiles = (capacity + tc::TILE - 1) / tc::TILE;
     const tc::Workspace ws = tc::ws_carve(workspace, ntiles);
-    tc::field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), tc::MLP_THREADS, tc::SMEM_BWD, st>>>(
-        f, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count, grad_sdf, grad_color, ws,
-        dl_dx != nullptr);
+    tc::launch_bwd(f, ntiles, count, dl_dc, dl_dsdf, dl_dn_extra, static_cast<float>(eik_weight), eik_count,
+                   grad_sdf, grad_color, ws, dl_dx != nullptr, st);
     if ((rc = check_launch("field_backward_tc"))) return rc;
     if (dl_dx != nullptr) {
         tc::field_input_levels_kernel<<<grid_for(ntiles, 1, kNumSMs * 8), tc::TILE, 0, st>>>(

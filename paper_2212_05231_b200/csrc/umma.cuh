@@ -242,6 +242,11 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
     }
 }
 
+// Plain arrive (release.cta): one of the barrier's expected arrivals.
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
 // Several bulk copies completing one mbarrier phase: one arrive + expect_tx for the
 // total, then the copies (complete_tx only).  Evict-first: data read exactly once.
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
