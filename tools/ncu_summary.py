@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 NAMES = {"field_gather_kernel": "field_gather", "field_fwd_kernel": "field_mlp_forward", "field_fwd2_kernel": "field_mlp_forward",
-         "field_bwd_kernel": "field_mlp_backward", "field_scatter_kernel": "field_scatter"}
+         "field_bwd_kernel": "field_mlp_backward", "field_bwd2_kernel": "field_mlp_backward", "field_scatter_kernel": "field_scatter"}
 ROWS = ("Memory Throughput", "DRAM Throughput", "Duration", "Compute (SM) Throughput", "Issue Slots Busy",
         "L2 Hit Rate", "Warp Cycles Per Issued Instruction", "Block Size", "Grid Size",
         "Registers Per Thread", "Dynamic Shared Memory Per Block", "Achieved Occupancy")
