@@ -137,6 +137,13 @@ NS2B_API int ns2b_rays_from_picks(const int64_t *picks, int64_t n, int64_t n_fir
 NS2B_API int ns2b_march_count(const double *origins, const double *dirs, int64_t nrays,
                      const ns2b_occ_t *occ, int32_t *counts, void *stream);
 
+/* Pass 1 that also records each ray's kept candidates (keep_mask: nrays x 16 uint32, bit
+ * k of word w = candidate 32w + k), so ns2b_march_fill_masked computes the positions of
+ * the kept candidates only.  Same counts as ns2b_march_count. */
+NS2B_API int ns2b_march_count_masked(const double *origins, const double *dirs, int64_t nrays,
+                                     const ns2b_occ_t *occ, int32_t *counts, uint32_t *keep_mask,
+                                     void *stream);
+
 /* Exclusive scan of counts -> offsets (nrays+1); offsets[nrays] = P.  Workspace
  * query: pass ws == NULL to receive the byte size in *ws_bytes. */
 NS2B_API int ns2b_scan_offsets(const int32_t *counts, int64_t nrays, int32_t *offsets, void *ws,
@@ -147,6 +154,11 @@ NS2B_API int ns2b_scan_offsets(const int32_t *counts, int64_t nrays, int32_t *of
 NS2B_API int ns2b_march_fill(const double *origins, const double *dirs, int64_t nrays,
                     const ns2b_occ_t *occ, const int32_t *offsets, int32_t *ray_ids, double *t,
                     double *pos64, float *pos32, void *stream);
+
+/* Pass 2 from pass 1's keep masks (same outputs as ns2b_march_fill, bit for bit). */
+NS2B_API int ns2b_march_fill_masked(const double *origins, const double *dirs, int64_t nrays,
+                                    const ns2b_occ_t *occ, const int32_t *offsets, const uint32_t *keep_mask,
+                                    int32_t *ray_ids, double *t, double *pos64, float *pos32, void *stream);
 
 /* eval_field forward (field.py:208-244) over the samples [0, *count): sdf d (P),
  * colors (P,3) and optionally normals (P,3), geometry feature g (P,15).  View directions

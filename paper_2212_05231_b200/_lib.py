@@ -62,6 +62,8 @@ _SIGS = {
     "ns2b_march_count": (ctypes.c_int, [P, P, I64, ctypes.POINTER(OccT), P, P]),
     "ns2b_scan_offsets": (ctypes.c_int, [P, I64, P, P, ctypes.POINTER(SZ), P]),
     "ns2b_march_fill": (ctypes.c_int, [P, P, I64, ctypes.POINTER(OccT), P, P, P, P, P, P]),
+    "ns2b_march_count_masked": (ctypes.c_int, [P, P, I64, ctypes.POINTER(OccT), P, P, P]),
+    "ns2b_march_fill_masked": (ctypes.c_int, [P, P, I64, ctypes.POINTER(OccT), P, P, P, P, P, P, P]),
     "ns2b_field_forward": (ctypes.c_int, [ctypes.POINTER(FieldT), P, P, P, P, I64, P, P, P, P, P,
                                           P, P]),
     "ns2b_field_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),

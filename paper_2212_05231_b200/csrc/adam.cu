@@ -29,25 +29,59 @@ __global__ void finite_kernel(const float *__restrict__ g, Segs s, int32_t *__re
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flag, static_cast<int32_t>(bad));
 }
 
+// one element (the numba loop's arithmetic, op for op)
+__device__ __forceinline__ void adam_elem(float &p, float g32, float &m, float &v, double lr, double c1, double c2,
+                                          double b1, double b2, double eps) {
+    const double g = static_cast<double>(g32);
+    const float mi = static_cast<float>(__dadd_rn(__dmul_rn(b1, static_cast<double>(m)), __dmul_rn(1.0 - b1, g)));
+    const float vi = static_cast<float>(
+        __dadd_rn(__dmul_rn(b2, static_cast<double>(v)), __dmul_rn(__dmul_rn(1.0 - b2, g), g)));
+    m = mi;
+    v = vi;
+    const double step = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(static_cast<double>(mi), c1)),
+                                  __dadd_rn(sqrt(__ddiv_rn(static_cast<double>(vi), c2)), eps));
+    p = static_cast<float>(__dsub_rn(static_cast<double>(p), step));
+}
+
+// With 16-B aligned buffers, segments whose buffer offset is a multiple of 4 are walked 4 elements per thread with
+// 16-B loads and stores (the table segment: all but ~9k of the parameters); the rest,
+// and every segment's tail, element by element.  Same per-element arithmetic either way.
 __global__ void adam_multi_kernel(float *__restrict__ param, const float *__restrict__ grad,
                                   float *__restrict__ m, float *__restrict__ v, Segs s, double b1,
-                                  double b2, double eps, const int32_t *__restrict__ flag) {
+                                  double b2, double eps, const int32_t *__restrict__ flag, bool vec_ok) {
     if (flag && *flag) return;
-    const int64_t total = s.off[s.n];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int k = 0;
-        while (k + 1 < s.n && i >= s.off[k + 1]) ++k;
-        const int64_t j = s.base[k] + (i - s.off[k]);
-        const double g = static_cast<double>(grad[j]);
-        const float mi = static_cast<float>(__dadd_rn(__dmul_rn(b1, static_cast<double>(m[j])), __dmul_rn(1.0 - b1, g)));
-        const float vi = static_cast<float>(
-            __dadd_rn(__dmul_rn(b2, static_cast<double>(v[j])), __dmul_rn(__dmul_rn(1.0 - b2, g), g)));
-        m[j] = mi;
-        v[j] = vi;
-        const double step = __ddiv_rn(__dmul_rn(s.lr[k], __ddiv_rn(static_cast<double>(mi), s.c1[k])),
-                                      __dadd_rn(sqrt(__ddiv_rn(static_cast<double>(vi), s.c2[k])), eps));
-        param[j] = static_cast<float>(__dsub_rn(static_cast<double>(param[j]), step));
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < s.n; ++k) {
+        const int64_t len = s.off[k + 1] - s.off[k], base = s.base[k];
+        const double lr = s.lr[k], c1 = s.c1[k], c2 = s.c2[k];
+        int64_t done = 0;
+        if (vec_ok && (base & 3) == 0) {
+            const int64_t n4 = len >> 2;
+            float4 *p4 = reinterpret_cast<float4 *>(param + base);
+            const float4 *g4 = reinterpret_cast<const float4 *>(grad + base);
+            float4 *m4 = reinterpret_cast<float4 *>(m + base);
+            float4 *v4 = reinterpret_cast<float4 *>(v + base);
+            for (int64_t i = tid; i < n4; i += nth) {
+                float4 pp = p4[i], mm = m4[i], vv = v4[i];
+                const float4 gg = g4[i];
+                adam_elem(pp.x, gg.x, mm.x, vv.x, lr, c1, c2, b1, b2, eps);
+                adam_elem(pp.y, gg.y, mm.y, vv.y, lr, c1, c2, b1, b2, eps);
+                adam_elem(pp.z, gg.z, mm.z, vv.z, lr, c1, c2, b1, b2, eps);
+                adam_elem(pp.w, gg.w, mm.w, vv.w, lr, c1, c2, b1, b2, eps);
+                p4[i] = pp;
+                m4[i] = mm;
+                v4[i] = vv;
+            }
+            done = n4 << 2;
+        }
+        for (int64_t i = done + tid; i < len; i += nth) {
+            const int64_t j = base + i;
+            float pp = param[j], mm = m[j], vv = v[j];
+            adam_elem(pp, grad[j], mm, vv, lr, c1, c2, b1, b2, eps);
+            param[j] = pp;
+            m[j] = mm;
+            v[j] = vv;
+        }
     }
 }
 
@@ -113,7 +147,9 @@ int ns2b_adam_multi(float *param, const float *grad, float *m, float *v, const i
     }
     if (s.off[s.n] == 0) return NS2B_OK;
     adam_multi_kernel<<<grid_for(s.off[s.n], 256, kNumSMs * 8), 256, 0, as_stream(stream)>>>(
-        param, grad, m, v, s, beta1, beta2, eps, flag);
+        param, grad, m, v, s, beta1, beta2, eps, flag,
+        ((reinterpret_cast<uintptr_t>(param) | reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(m) |
+          reinterpret_cast<uintptr_t>(v)) & 15u) == 0);
     return check_launch("adam_multi");
 }
 

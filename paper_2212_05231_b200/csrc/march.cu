@@ -73,8 +73,13 @@ __device__ __forceinline__ bool candidate(const OccArgs &g, const double *o, con
     return g.bits[(static_cast<int64_t>(cell[0]) * g.G + cell[1]) * g.G + cell[2]] != 0;
 }
 
+// keep masks (optional): 16 words per ray, bit k of word w = candidate 32 w + k kept, so the
+// fill pass computes positions for the kept candidates only (no second occupancy test)
+constexpr int kMaskWords = 16;
+
 __global__ void march_count_kernel(const double *__restrict__ origins, const double *__restrict__ dirs,
-                                   int64_t nrays, OccArgs g, int32_t *__restrict__ counts) {
+                                   int64_t nrays, OccArgs g, int32_t *__restrict__ counts,
+                                   uint32_t *__restrict__ keep_mask) {
     const int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -92,7 +97,9 @@ __global__ void march_count_kernel(const double *__restrict__ origins, const dou
                 double t, pos[3];
                 keep = candidate(g, o, d, t0, k, t, pos);
             }
-            kept += __popc(__ballot_sync(0xffffffffu, keep));
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep_mask && lane == 0) keep_mask[r * kMaskWords + (base >> 5)] = bal;
+            kept += __popc(bal);
         }
         if (lane == 0) counts[r] = kept;
     }
@@ -100,7 +107,8 @@ __global__ void march_count_kernel(const double *__restrict__ origins, const dou
 
 __global__ void march_fill_kernel(const double *__restrict__ origins, const double *__restrict__ dirs,
                                   int64_t nrays, OccArgs g, const int32_t *__restrict__ offsets,
-                                  int32_t *__restrict__ ray_ids, double *__restrict__ tout,
+                                  const uint32_t *__restrict__ keep_mask, int32_t *__restrict__ ray_ids,
+                                  double *__restrict__ tout,
                                   double *__restrict__ pos64, float *__restrict__ pos32) {
     const int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -116,8 +124,19 @@ __global__ void march_fill_kernel(const double *__restrict__ origins, const doub
             int k = base + lane;
             bool keep = false;
             double t = 0.0, pos[3] = {0.0, 0.0, 0.0};
-            if (k < n) keep = candidate(g, o, d, t0, k, t, pos);
-            unsigned bal = __ballot_sync(0xffffffffu, keep);
+            unsigned bal;
+            if (keep_mask) {  // the count pass's verdicts: t and the position of kept candidates only
+                bal = keep_mask[r * kMaskWords + (base >> 5)];
+                keep = (bal >> lane) & 1u;
+                if (keep) {
+                    t = __dadd_rn(t0, __dmul_rn(__dadd_rn(static_cast<double>(k), 0.5), g.step));
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) pos[a] = __dadd_rn(o[a], __dmul_rn(t, d[a]));
+                }
+            } else {
+                if (k < n) keep = candidate(g, o, d, t0, k, t, pos);
+                bal = __ballot_sync(0xffffffffu, keep);
+            }
             if (keep) {
                 int64_t s = out + __popc(bal & ((1u << lane) - 1u));
                 ray_ids[s] = static_cast<int32_t>(r);
@@ -142,14 +161,19 @@ using namespace ns2b;
 
 extern "C" {
 
-int ns2b_march_count(const double *origins, const double *dirs, int64_t nrays,
-                     const ns2b_occ_t *occ, int32_t *counts, void *stream) {
+int ns2b_march_count_masked(const double *origins, const double *dirs, int64_t nrays,
+                            const ns2b_occ_t *occ, int32_t *counts, uint32_t *keep_mask, void *stream) {
     NS2B_REQUIRE(occ && occ->bits && occ->resolution > 0, "invalid occupancy grid");
     if (nrays == 0) return NS2B_OK;
     OccArgs g = make_occ(occ);
     int blocks = grid_for(nrays * 32, 256, kNumSMs * 16);
-    march_count_kernel<<<blocks, 256, 0, as_stream(stream)>>>(origins, dirs, nrays, g, counts);
+    march_count_kernel<<<blocks, 256, 0, as_stream(stream)>>>(origins, dirs, nrays, g, counts, keep_mask);
     return check_launch("march_count");
+}
+
+int ns2b_march_count(const double *origins, const double *dirs, int64_t nrays,
+                     const ns2b_occ_t *occ, int32_t *counts, void *stream) {
+    return ns2b_march_count_masked(origins, dirs, nrays, occ, counts, nullptr, stream);
 }
 
 int ns2b_scan_offsets(const int32_t *counts, int64_t nrays, int32_t *offsets, void *ws,
@@ -174,16 +198,23 @@ int ns2b_scan_offsets(const int32_t *counts, int64_t nrays, int32_t *offsets, vo
     return NS2B_OK;
 }
 
-int ns2b_march_fill(const double *origins, const double *dirs, int64_t nrays,
-                    const ns2b_occ_t *occ, const int32_t *offsets, int32_t *ray_ids, double *t,
-                    double *pos64, float *pos32, void *stream) {
+int ns2b_march_fill_masked(const double *origins, const double *dirs, int64_t nrays,
+                           const ns2b_occ_t *occ, const int32_t *offsets, const uint32_t *keep_mask,
+                           int32_t *ray_ids, double *t, double *pos64, float *pos32, void *stream) {
     NS2B_REQUIRE(occ && occ->bits && occ->resolution > 0, "invalid occupancy grid");
     if (nrays == 0) return NS2B_OK;
     OccArgs g = make_occ(occ);
     int blocks = grid_for(nrays * 32, 256, kNumSMs * 16);
-    march_fill_kernel<<<blocks, 256, 0, as_stream(stream)>>>(origins, dirs, nrays, g, offsets,
+    march_fill_kernel<<<blocks, 256, 0, as_stream(stream)>>>(origins, dirs, nrays, g, offsets, keep_mask,
                                                              ray_ids, t, pos64, pos32);
     return check_launch("march_fill");
+}
+
+int ns2b_march_fill(const double *origins, const double *dirs, int64_t nrays,
+                    const ns2b_occ_t *occ, const int32_t *offsets, int32_t *ray_ids, double *t,
+                    double *pos64, float *pos32, void *stream) {
+    return ns2b_march_fill_masked(origins, dirs, nrays, occ, offsets, nullptr, ray_ids, t, pos64, pos32,
+                                  stream);
 }
 
 }  // extern "C"

@@ -1,6 +1,6 @@
 """Occupancy marching + NeuS volume rendering on B200 (API of `hashsdf/renderer.py`).
 
-Device kernels (libns2b): `ns2b_march_count` / `ns2b_scan_offsets` / `ns2b_march_fill`
+Device kernels (libns2b): `ns2b_march_count(_masked)` / `ns2b_scan_offsets` / `ns2b_march_fill(_masked)`
 (K1, fp64, bit-exact sample sets), `ns2b_field_forward` (K2), `ns2b_composite`
 (K3: per-ray alpha / transmittance / weights / colour, optionally fused with the
 Huber loss and the compositing backward) and `ns2b_composite_backward` (K4).
@@ -168,12 +168,17 @@ class _ScanWorkspace:
 _scan_ws = _ScanWorkspace()
 
 
-def march_count_and_scan(o, d, occ, counts, offsets, stream=None):
-    """Kernel pass 1 + exclusive scan (device only, no sync)."""
+def march_count_and_scan(o, d, occ, counts, offsets, stream=None, keep_mask=None):
+    """Kernel pass 1 + exclusive scan (device only, no sync).  With `keep_mask` (m x 16
+    int32) pass 1 also records each ray's kept candidates for `ns2b_march_fill_masked`."""
     st = _lib.stream_ptr(stream)
     m = o.shape[0]
     s = occ.struct()
-    _lib.call("ns2b_march_count", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(counts), st)
+    if keep_mask is not None:
+        _lib.call("ns2b_march_count_masked", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(counts),
+                  _lib.ptr(keep_mask), st)
+    else:
+        _lib.call("ns2b_march_count", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(counts), st)
     buf, need = _scan_ws.get(counts, m, offsets)
     _lib.call("ns2b_scan_offsets", _lib.ptr(counts), m, _lib.ptr(offsets), _lib.ptr(buf),
               ctypes.byref(need), st)
@@ -200,23 +205,31 @@ def intersect_aabb(origins, dirs, lo, hi):
     return torch.clamp(near.amax(dim=1), min=0.0), far.amin(dim=1)
 
 
-def march_rays(origins, dirs, occ, need_t=True, need_pos64=True):
-    """Fixed-stride marching with empty-space skipping (`renderer.py:171-192`)."""
+def march_rays(origins, dirs, occ, need_t=True, need_pos64=True, masked=True):
+    """Fixed-stride marching with empty-space skipping (`renderer.py:171-192`).  `masked`:
+    pass 1 records the kept candidates and pass 2 computes only their positions (same
+    outputs, bit for bit)."""
     o = as_device(origins, torch.float64).reshape(-1, 3).contiguous()
     d = as_device(dirs, torch.float64).reshape(-1, 3).contiguous()
     m = o.shape[0]
     dev = o.device
     counts = torch.empty(m, dtype=torch.int32, device=dev)
     offsets = torch.empty(m + 1, dtype=torch.int32, device=dev)
-    march_count_and_scan(o, d, occ, counts, offsets)
+    keep = torch.empty((m, 16), dtype=torch.int32, device=dev) if masked else None
+    march_count_and_scan(o, d, occ, counts, offsets, keep_mask=keep)
     P = int(offsets[m].item())
     ray_ids = torch.empty(P, dtype=torch.int32, device=dev)
     t = torch.empty(P, dtype=torch.float64, device=dev) if need_t else None
     p64 = torch.empty((P, 3), dtype=torch.float64, device=dev) if need_pos64 else None
     p32 = torch.empty((P, 3), dtype=torch.float32, device=dev)
     s = occ.struct()
-    _lib.call("ns2b_march_fill", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(offsets),
-              _lib.ptr(ray_ids), _lib.ptr(t), _lib.ptr(p64), _lib.ptr(p32), _lib.stream_ptr())
+    if masked:
+        _lib.call("ns2b_march_fill_masked", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(offsets),
+                  _lib.ptr(keep), _lib.ptr(ray_ids), _lib.ptr(t), _lib.ptr(p64), _lib.ptr(p32),
+                  _lib.stream_ptr())
+    else:
+        _lib.call("ns2b_march_fill", _lib.ptr(o), _lib.ptr(d), m, ctypes.byref(s), _lib.ptr(offsets),
+                  _lib.ptr(ray_ids), _lib.ptr(t), _lib.ptr(p64), _lib.ptr(p32), _lib.stream_ptr())
     return MarchResult(ray_ids, t, p64, m, offsets, p32, offsets[m:m + 1], P)
 
 

@@ -174,6 +174,7 @@ class StepWorkspace:
             self.d = torch.empty((m, 3), dtype=torch.float64, device=d)
             self.tgt = torch.empty((m, 3), dtype=torch.float64, device=d)
             self.counts = torch.empty(m, dtype=torch.int32, device=d)
+            self.keep_mask = torch.empty((m, 16), dtype=torch.int32, device=d)  # march pass 1 -> 2
             self.offsets = torch.empty(m + 1, dtype=torch.int32, device=d)
             self.rendered = torch.empty((m, 3), dtype=torch.float64, device=d)
             self.resid = torch.empty(m, dtype=torch.float64, device=d)
@@ -330,7 +331,7 @@ def train_step(state, dataset, time_index=0, batch=None):
     timers = getattr(state, "timers", None)
     # K1: march (count, scan) -> P -> fill
     with _Timer(timers, "march_count_scan", st):
-        renderer.march_count_and_scan(ws.o, ws.d, occ, ws.counts, ws.offsets, st)
+        renderer.march_count_and_scan(ws.o, ws.d, occ, ws.counts, ws.offsets, st, keep_mask=ws.keep_mask)
     ws.p_host.copy_(ws.offsets[m:m + 1], non_blocking=True)
     st.synchronize()
     P = int(ws.p_host[0])
@@ -338,8 +339,9 @@ def train_step(state, dataset, time_index=0, batch=None):
     ws.samples(max(P, 1))
     o = occ.struct()
     with _Timer(timers, "march_fill", st):
-        _lib.call("ns2b_march_fill", _lib.ptr(ws.o), _lib.ptr(ws.d), m, ctypes.byref(o),
-                  _lib.ptr(ws.offsets), _lib.ptr(ws.ray_ids), None, None, _lib.ptr(ws.pos32), sp)
+        _lib.call("ns2b_march_fill_masked", _lib.ptr(ws.o), _lib.ptr(ws.d), m, ctypes.byref(o),
+                  _lib.ptr(ws.offsets), _lib.ptr(ws.keep_mask), _lib.ptr(ws.ray_ids), None, None,
+                  _lib.ptr(ws.pos32), sp)
     count = ws.offsets[m:m + 1]
     ws.sums.zero_()
     s = params.sharpness

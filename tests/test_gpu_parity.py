@@ -100,7 +100,8 @@ def sphere64():
     return oscene.make_synthetic("sphere", views=8, seed=0, image_size=64)
 
 
-def test_march_bit_exact(sphere64):
+@pytest.mark.parametrize("masked", [True, False])
+def test_march_bit_exact(sphere64, masked):
     ost = _c1_state()
     orender.update_occupancy(ost.occ, ost.params, 8)
     b = oscene.sample_ray_batch(sphere64, 0, 4096, 0.9, np.random.default_rng(1))
@@ -112,7 +113,7 @@ def test_march_bit_exact(sphere64):
     ref = orender.march_rays(o, d, ost.occ)
     pocc = prender.OccupancyGrid(128)
     pocc.set_bits(ost.occ.bits)
-    got = prender.march_rays(o, d, pocc)
+    got = prender.march_rays(o, d, pocc, masked=masked)
     assert got.sample_count == ref.ray_ids.shape[0]
     assert_exact(np_(got.ray_ids).astype(np.int64), ref.ray_ids, "ray ids")
     assert_exact(np_(got.t), ref.t, "t")
