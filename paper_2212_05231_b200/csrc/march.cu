@@ -13,6 +13,7 @@ namespace ns2b {
 struct OccArgs {
     int G;
     double lo[3], hi[3], ext[3], step;
+    double scale[3];  // G / ext: the fast path of the cell index (see candidate)
     const uint8_t *bits;
 };
 
@@ -23,6 +24,7 @@ static OccArgs make_occ(const ns2b_occ_t *o) {
         a.lo[k] = o->lo[k];
         a.hi[k] = o->hi[k];
         a.ext[k] = o->hi[k] - o->lo[k];
+        a.scale[k] = static_cast<double>(o->resolution) / a.ext[k];
     }
     a.step = o->step_size;
     a.bits = o->bits;
@@ -65,8 +67,20 @@ __device__ __forceinline__ bool candidate(const OccArgs &g, const double *o, con
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         pos[a] = __dadd_rn(o[a], __dmul_rn(t, d[a]));
-        double u = __dmul_rn(__ddiv_rn(__dsub_rn(pos[a], g.lo[a]), g.ext[a]), static_cast<double>(g.G));
-        long long ci = static_cast<long long>(u);  // astype(int64): truncation toward zero
+        // the reference's cell index is trunc(((pos - lo) / ext) * G); (pos - lo) * (G / ext)
+        // is within a few ulp of it (|u| <~ G: ~1e-13 absolute), so away from an integer
+        // boundary its truncation is the same and the fp64 division is skipped
+        const double du = __dsub_rn(pos[a], g.lo[a]);
+        const double ua = __dmul_rn(du, g.scale[a]);
+        const double fa = floor(ua);
+        const double fr = __dsub_rn(ua, fa);
+        long long ci;
+        if (fr > 1e-9 && fr < 1.0 - 1e-9) {
+            ci = static_cast<long long>(fa);  // == trunc(u) for u >= 0; u < 0 clamps to 0 either way
+        } else {
+            const double u = __dmul_rn(__ddiv_rn(du, g.ext[a]), static_cast<double>(g.G));
+            ci = static_cast<long long>(u);  // astype(int64): truncation toward zero
+        }
         ci = ci < 0 ? 0 : (ci > g.G - 1 ? g.G - 1 : ci);
         cell[a] = static_cast<int>(ci);
     }
