@@ -1242,32 +1242,16 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 p1 = jx[1] * scd;
                 p2 = jx[2] * scd;
             }
-#pragma unroll 1
-            for (int l0 = 8 * qh; l0 < min(NA, 8 * qh + 8); l0 += 4) {  // 4 levels per batch:
-                // the first batch was loaded during P1's GEMMs; the second's 24 loads go out
-                // together (L2-resident)
-                float jd[4][2], jv[4][6];
-                const bool first = l0 == 8 * qh;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    umma::tmem_ld2(my + SA + 2 * (l0 + i), jd[i][0], jd[i][1]);
-                    if constexpr (kG) {  // J from TMEM (the G phase put it there)
-                        float jl[8];
-                        umma::tmem_ld8(my + TJ + 8 * (l0 + i), jl);
-#pragma unroll
-                        for (int k = 0; k < 6; ++k) jv[i][k] = jl[k];
-                    } else {
-                        const float *jr = jt + 6 * (l0 + i) * TILE;
-#pragma unroll
-                        for (int k = 0; k < 6; ++k)
-                            jv[i][k] = first ? jv0[i][k] : (l0 + i < NA ? __ldcs(jr + k * TILE) : 0.f);
-                    }
-                }
+            // 4 levels per batch: the j_d feature rows go to the scatter's inputs, the normal
+            // accumulates d . J
+            auto batch = [&](int l0, const float (&jv)[4][6]) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int l = l0 + i;
+                    float jd0, jd1;
+                    umma::tmem_ld2(my + SA + 2 * l, jd0, jd1);
                     if (l < NA) {
-                        const float d0 = jd[i][0] * scd, d1 = jd[i][1] * scd;
+                        const float d0 = jd0 * scd, d1 = jd1 * scd;
                         __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
                         __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
                         p0 = fmaf(d0, jv[i][0], fmaf(d1, jv[i][3], p0));
@@ -1275,6 +1259,32 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                         p2 = fmaf(d0, jv[i][2], fmaf(d1, jv[i][5], p2));
                     }
                 }
+            };
+            if constexpr (kG) {  // J from TMEM (the G phase put it there)
+#pragma unroll 1
+                for (int l0 = 8 * qh; l0 < min(NA, 8 * qh + 8); l0 += 4) {
+                    float jv[4][6];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        float jl[8];
+                        umma::tmem_ld8(my + TJ + 8 * (l0 + i), jl);
+#pragma unroll
+                        for (int k = 0; k < 6; ++k) jv[i][k] = jl[k];
+                    }
+                    batch(l0, jv);
+                }
+            } else {
+                // the first batch was loaded during P1's GEMMs; the second's 24 loads
+                // (L2-resident) are issued before the first batch is consumed
+                const int l1 = 8 * qh + 4;
+                float jv1[4][6];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int k = 0; k < 6; ++k)
+                        jv1[i][k] = l1 + i < NA ? __ldcs(jt + (6 * (l1 + i) + k) * TILE) : 0.f;
+                if (8 * qh < NA) batch(8 * qh, jv0);
+                if (l1 < NA) batch(l1, jv1);
             }
             float *xn = xch + 2 * TILE;  // [2][3][128]
             xn[(3 * qh + 0) * TILE + r] = p0;
@@ -2377,6 +2387,18 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int g = warp >> 3, gw = warp & 7, tg = t & 255;
+#ifdef NS2B_PHASE_PROF  // cycles group C waits for a free handoff slot [0], S for a full one [1], loop totals [2, 3]
+    __shared__ long long bpw[4];
+    if (t < 4) bpw[t] = 0;
+#define BPW(i, stmt)                                      \
+    do {                                                  \
+        const long long w0_ = clock64();                  \
+        stmt;                                             \
+        if (tg == 0) bpw[i] += clock64() - w0_;           \
+    } while (0)
+#else
+#define BPW(i, stmt) stmt
+#endif
     const int qd = gw & 3, qh = gw >> 2;
     const int r = 32 * qd + lane;
     const int E = 3 + 2 * f.L;
@@ -2668,7 +2690,7 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 umma::tmem_ld8(my + C_SL + 16 * qh + 8, c1);
                 const int hs = it & 1;
                 if (it >= 2) {  // group S has read this slot (tile it - 2)
-                    umma::mbar_wait(hempty + hs, ph_he[hs]);
+                    BPW(0, umma::mbar_wait(hempty + hs, ph_he[hs]));
                     ph_he[hs] ^= 1u;
                 }
                 float *hq = reinterpret_cast<float *>(S.p(TH0 + hs * H_BYTES + H_Q)) + r;
@@ -2738,7 +2760,7 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 for (int k = 0; k < 6; ++k) jv[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
             // ------------------------------------------- S0: dly -> U, dH2; MV, M1
             const int hs = it & 1;
-            umma::mbar_wait(hfull + hs, ph_hf[hs]);
+            BPW(1, umma::mbar_wait(hfull + hs, ph_hf[hs]));
             ph_hf[hs] ^= 1u;
             float q0, q1, q2, dly[8];
             uint32_t m1;
@@ -2895,8 +2917,12 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
     }
     umma::fence_before_sync();
     __syncthreads();
+#ifdef NS2B_PHASE_PROF
+    if (blockIdx.x == 0 && t == 0) printf("PHASEPROF bwd2 C-waits-free %lld S-waits-full %lld\n", bpw[0], bpw[1]);
+#endif
     if (warp == 0) umma::tmem_dealloc(tb, 512);
 }
+#undef BPW
 
 // ---------------------------------------------------------------------------
 // Gather kernel (one pass per step): per 128-sample tile, trilinear features and
@@ -2905,7 +2931,11 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
 // the fp16 hi/lo E-tile layout the MLP kernels DMA into shared memory.
 constexpr int GATHER_BLOCK = TILE;
 
+#ifdef NS2B_GATHER_MINB
+__global__ void __launch_bounds__(GATHER_BLOCK, NS2B_GATHER_MINB)
+#else
 __global__ void __launch_bounds__(GATHER_BLOCK)
+#endif
 field_gather_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ ray_ids,
                     const double *__restrict__ dirs, const int32_t *__restrict__ count, Workspace ws) {
     __shared__ float raw[32][TILE + 1];
@@ -3129,7 +3159,10 @@ __device__ __forceinline__ void red_add_f32x4(float *addr, float a, float b, flo
     atomicAdd(reinterpret_cast<float4 *>(addr), make_float4(a, b, c, d));
 }
 
-__global__ void __launch_bounds__(TILE, 6)
+#ifndef NS2B_SCATTER_MINB
+#define NS2B_SCATTER_MINB 6
+#endif
+__global__ void __launch_bounds__(TILE, NS2B_SCATTER_MINB)
 field_scatter_kernel(FieldDev f, const float *__restrict__ pos, const int32_t *__restrict__ count,
                      const Workspace ws, float *__restrict__ g_tab, int agg_levels) {
     __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
