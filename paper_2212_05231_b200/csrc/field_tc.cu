@@ -1161,8 +1161,10 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         int eA1;
         float d_sdf;
         {
+            // raw accumulator values; the result scale 2^-(eE + eH1) (a power of two: exact) is
+            // applied to the partial SDF sum once and folded into the staging scale
             float z[4][8], ma = 0.f, dpart = 0.f;
-            const float sc = pow2i(-(eE + eH1));
+            const int esc = -(eE + eH1);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int b = 4 * qh + i;
@@ -1171,17 +1173,17 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 for (int k = 0; k < 8; ++k) {
                     const bool on = z[i][k] > 0.f;
                     m1 |= on ? (1u << (8 * i + k)) : 0u;
-                    const float a = on ? z[i][k] * sc : 0.f;
+                    const float a = on ? z[i][k] : 0.f;
                     z[i][k] = a;
                     ma = fmaxf(ma, a);
                     dpart = fmaf(h2row0[8 * b + k], a, dpart);
                 }
             }
-            xch[qh * TILE + r] = dpart;
+            xch[qh * TILE + r] = dpart * pow2i(esc);
             eA1 = PS.guess(kA1);
-            PS.contrib(kA1, ma);
+            PS.contrib(kA1, ma * pow2i(esc));
             auto stg = [&](int e) {
-                const float sa = pow2i(e);
+                const float sa = pow2i(e + esc);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) stage_blk<64>(S, AB, T64B, r, 4 * qh + i, z[i], sa);
             };
@@ -1365,8 +1367,10 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         uint32_t mc1 = 0u, mc2 = 0u;
         int eA1c, eA2c;
         {
+            // raw accumulator values: the result scale 2^-(eCin + eC1) is folded into the
+            // staging scale (one multiply per element; powers of two, exact)
             float z[4][8], m = 0.f;
-            const float sc = pow2i(-(eCin + eC1));
+            const int esc = -(eCin + eC1);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 umma::tmem_ld8(my + SA + 8 * (4 * qh + i), z[i]);
@@ -1374,14 +1378,14 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 for (int k = 0; k < 8; ++k) {
                     const bool on = z[i][k] > 0.f;
                     mc1 |= on ? (1u << (8 * i + k)) : 0u;
-                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    z[i][k] = on ? z[i][k] : 0.f;
                     m = fmaxf(m, z[i][k]);
                 }
             }
             eA1c = PS.guess(kA1c);
-            PS.contrib(kA1c, m);
+            PS.contrib(kA1c, m * pow2i(esc));
             auto stg = [&](int e) {
-                const float s = pow2i(e);
+                const float s = pow2i(e + esc);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) stage_blk<64>(S, AB, T64B, r, 4 * qh + i, z[i], s);
             };
@@ -1410,8 +1414,11 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         PMARK(10);
         // ------------------------------------------------ P4: a2c (hi, store only) -> EB; logits
         {
+            // raw accumulator values: the result scale 2^-(eA1c + eC2) is applied to the logit
+            // partials once and folded into the staging scale (powers of two: exact)
             float z[4][8], m = 0.f;
-            const float sc = pow2i(-(eA1c + eC2));
+            const int esc = -(eA1c + eC2);
+            const float sc = pow2i(esc);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 umma::tmem_ld8(my + SB + 8 * (4 * qh + i), z[i]);
@@ -1419,12 +1426,12 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 for (int k = 0; k < 8; ++k) {
                     const bool on = z[i][k] > 0.f;
                     mc2 |= on ? (1u << (8 * i + k)) : 0u;
-                    z[i][k] = on ? z[i][k] * sc : 0.f;
+                    z[i][k] = on ? z[i][k] : 0.f;
                     m = fmaxf(m, z[i][k]);
                 }
             }
             eA2c = PS.guess(kA2c);
-            PS.contrib(kA2c, m);
+            PS.contrib(kA2c, m * sc);
             float lp0 = 0.f, lp1 = 0.f, lp2 = 0.f;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1436,9 +1443,9 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                     lp2 = fmaf(c3w[2][8 * b + k], z[i][k], lp2);
                 }
             }
-            lgx[(3 * qh + 0) * TILE + r] = lp0;
-            lgx[(3 * qh + 1) * TILE + r] = lp1;
-            lgx[(3 * qh + 2) * TILE + r] = lp2;
+            lgx[(3 * qh + 0) * TILE + r] = lp0 * sc;
+            lgx[(3 * qh + 1) * TILE + r] = lp1 * sc;
+            lgx[(3 * qh + 2) * TILE + r] = lp2 * sc;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {  // mask bytes [m1 | mc1 | mc2][block][row]
                 const int b = 4 * qh + i;
@@ -1447,7 +1454,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 mkx[(2 * 8 + b) * TILE + r] = static_cast<uint8_t>(mc2 >> (8 * i));
             }
             auto stg = [&](int e) {  // hi part only: the backward's weight-gradient GEMMs read nothing else
-                const float s = pow2i(e);
+                const float s = pow2i(e + esc);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const uint4 h = make_uint4(pack_half2(z[i][0] * s, z[i][1] * s), pack_half2(z[i][2] * s, z[i][3] * s),
@@ -2602,22 +2609,24 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
             // ------------------------------------------- C1: u2 -> U1, dC2
             int eU2;
             {
+                // raw accumulator values: the result scale 2^-(eD + eC3) is folded into the
+                // staging scale (one multiply per element; powers of two, exact)
                 float u[4][8], m = 0.f;
-                const float sc = pow2i(-(eD + eC3));
+                const int esc = -(eD + eC3);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     umma::tmem_ld8(my + C_SL + 8 * (4 * qh + i), u[i]);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        u[i][k] = ((mc2 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                        u[i][k] = ((mc2 >> (8 * i + k)) & 1u) ? u[i][k] : 0.f;
                         m = fmaxf(m, fabsf(u[i][k]));
                     }
                 }
                 eU2 = PS.guess(kU2);
-                PS.contrib(kU2, m);
+                PS.contrib(kU2, m * pow2i(esc));
 #pragma unroll 1
                 for (int pass = 0;; ++pass) {
-                    const float s2 = pow2i(eU2);
+                    const float s2 = pow2i(eU2 + esc);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TYC, r, 4 * qh + i, u[i], s2, my + C_AH, my + C_AL);
                     umma::tmem_st_wait();
@@ -2642,18 +2651,18 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
             int eU1;
             {
                 float u[4][8], m = 0.f;
-                const float sc = pow2i(-(eU2 + eC2));
+                const int esc = -(eU2 + eC2);  // folded into the staging scale (see C1)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     umma::tmem_ld8(my + C_SL + 8 * (4 * qh + i), u[i]);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] * sc : 0.f;
+                        u[i][k] = ((mc1 >> (8 * i + k)) & 1u) ? u[i][k] : 0.f;
                         m = fmaxf(m, fabsf(u[i][k]));
                     }
                 }
                 eU1 = PS.guess(kU1);
-                PS.contrib(kU1, m);
+                PS.contrib(kU1, m * pow2i(esc));
                 wait_mma(mbar2, ph2);  // U1 restages TY
                 if (dma_t && has_next) {  // dC3 (before U1's GEMM) and dC2 are done: next A2c, A1c
                     dma(TWC, fwt(ntile) + FW_A2C, T64B, mb_w);
@@ -2661,7 +2670,7 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 }
 #pragma unroll 1
                 for (int pass = 0;; ++pass) {
-                    const float s1 = pow2i(eU1);
+                    const float s1 = pow2i(eU1 + esc);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TYC, r, 4 * qh + i, u[i], s1, my + C_AH, my + C_AL);
                     umma::tmem_st_wait();
@@ -2849,21 +2858,21 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
             int eU;
             {
                 float u[4][8], mu = 0.f;
-                const float sc4 = pow2i(-(eDLY + eH2));
+                const int esc = -(eDLY + eH2);  // folded into the staging scale (see C1)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     umma::tmem_ld8(my + S_SL + 8 * (4 * qh + i), u[i]);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] * sc4 : 0.f;
+                        u[i][k] = ((m1 >> (8 * i + k)) & 1u) ? u[i][k] : 0.f;
                         mu = fmaxf(mu, fabsf(u[i][k]));
                     }
                 }
                 eU = PS.guess(kU);
-                PS.contrib(kU, mu);
+                PS.contrib(kU, mu * pow2i(esc));
 #pragma unroll 1
                 for (int pass = 0;; ++pass) {
-                    const float su = pow2i(eU);
+                    const float su = pow2i(eU + esc);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) stage_blk_ta<64>(S, TXS, r, 4 * qh + i, u[i], su, my + S_AH, my + S_AL);
                     umma::tmem_st_wait();
