@@ -1246,14 +1246,15 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             }
             // 4 levels per batch: the j_d feature rows go to the scatter's inputs, the normal
             // accumulates d . J
-            auto batch = [&](int l0, const float (&jv)[4][6]) {
+            // this half's 8 levels of j_d (16 columns) in one TMEM load
+            float jda[16];
+            umma::tmem_ld16(my + SA + 16 * qh, jda);
+            auto batch = [&](int l0, int jo, const float (&jv)[4][6]) {  // jo: 0 / 4, a literal
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int l = l0 + i;
-                    float jd0, jd1;
-                    umma::tmem_ld2(my + SA + 2 * l, jd0, jd1);
                     if (l < NA) {
-                        const float d0 = jd0 * scd, d1 = jd1 * scd;
+                        const float d0 = jda[2 * (jo + i)] * scd, d1 = jda[2 * (jo + i) + 1] * scd;
                         __stcs(SBt + (32 + 2 * l) * TILE + r, d0);  // j_d feature rows for the scatter (Eq. 9)
                         __stcs(SBt + (33 + 2 * l) * TILE + r, d1);
                         p0 = fmaf(d0, jv[i][0], fmaf(d1, jv[i][3], p0));
@@ -1263,8 +1264,10 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 }
             };
             if constexpr (kG) {  // J from TMEM (the G phase put it there)
-#pragma unroll 1
-                for (int l0 = 8 * qh; l0 < min(NA, 8 * qh + 8); l0 += 4) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int l0 = 8 * qh + 4 * h;
+                    if (l0 >= NA) break;
                     float jv[4][6];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -1273,7 +1276,7 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
 #pragma unroll
                         for (int k = 0; k < 6; ++k) jv[i][k] = jl[k];
                     }
-                    batch(l0, jv);
+                    batch(l0, 4 * h, jv);
                 }
             } else {
                 // the first batch was loaded during P1's GEMMs; the second's 24 loads
@@ -1285,8 +1288,8 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
 #pragma unroll
                     for (int k = 0; k < 6; ++k)
                         jv1[i][k] = l1 + i < NA ? __ldcs(jt + (6 * (l1 + i) + k) * TILE) : 0.f;
-                if (8 * qh < NA) batch(8 * qh, jv0);
-                if (l1 < NA) batch(l1, jv1);
+                if (8 * qh < NA) batch(8 * qh, 0, jv0);
+                if (l1 < NA) batch(l1, 4, jv1);
             }
             float *xn = xch + 2 * TILE;  // [2][3][128]
             xn[(3 * qh + 0) * TILE + r] = p0;
