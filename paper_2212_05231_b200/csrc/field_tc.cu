@@ -2382,7 +2382,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
 field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__restrict__ dl_dc,
                   const float *__restrict__ dl_dsdf, const float *__restrict__ dl_dn_extra, float eik_w,
                   const int64_t *__restrict__ eik_count, float *__restrict__ g_sdf, float *__restrict__ g_color,
-                  Workspace ws, int want_xin) {
+                  Workspace ws) {
     using namespace b2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // C: [0] chain, [1] dC2 done, [2] dC1 done, [3] A2c, [4] A1c, [5] CIN, [6..7] inputs;
@@ -2722,15 +2722,6 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 }
                 hm[qh * TILE] = m1;
                 umma::mbar_arrive(hfull + hs);
-                if (want_xin && qh == 0 && valid) {  // dl_dx / dl_dv colour-input parts (field.py:307,309)
-                    float *xi = ws.xin + tile * XINROWS * TILE + r;
-                    xi[0] = c0[0] * sc3;
-                    xi[TILE] = c0[1] * sc3;
-                    xi[2 * TILE] = c0[2] * sc3;
-                    xi[3 * TILE] = c0[6] * sc3;
-                    xi[4 * TILE] = c0[7] * sc3;
-                    xi[5 * TILE] = c1[0] * sc3;
-                }
             }
             // dC1 (behind the DCIN GEMM) has read CIN: the next tile's CIN
             if (dma_t && has_next) {
@@ -2926,16 +2917,6 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                     __stcs(SBt + 64 * TILE + r, q0);
                     __stcs(SBt + 65 * TILE + r, q1);
                     __stcs(SBt + 66 * TILE + r, q2);
-                }
-                if (want_xin && qh == 1) {  // de_aug's position rows (E columns 32..34)
-                    float dx[8];
-                    umma::tmem_ld8(my + S_SL + 32, dx);
-                    if (tile * TILE + r < P) {
-                        float *xi = ws.xin + tile * XINROWS * TILE + r;
-                        xi[6 * TILE] = dx[0] * sde;
-                        xi[7 * TILE] = dx[1] * sde;
-                        xi[8 * TILE] = dx[2] * sde;
-                    }
                 }
             }
             // the next tile's S0 waits on its handoff slot; the slot reset of the exponent maxima
@@ -3350,7 +3331,7 @@ static bool use_fwd1() {
 static int fwd_mode();
 
 // NS2B_BWD=1 selects the one-group backward (field_bwd_kernel); the default is the
-// two-group pipelined field_bwd2_kernel (both write the input cotangents when asked)
+// two-group pipelined field_bwd2_kernel (input cotangents, want_xin, always use the former)
 static bool use_bwd1() {
     static int v = -1;
     if (v < 0) {
@@ -3363,12 +3344,12 @@ static bool use_bwd1() {
 static void launch_bwd(const FieldDev &f, int64_t ntiles, const int32_t *count, const float *dl_dc,
                        const float *dl_dsdf, const float *dl_dn_extra, float eik_w, const int64_t *eik_count,
                        float *g_sdf, float *g_color, const Workspace &ws, int want_xin, cudaStream_t st) {
-    if (use_bwd1())
+    if (want_xin || use_bwd1())
         field_bwd_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, SMEM_BWD, st>>>(
             f, count, dl_dc, dl_dsdf, dl_dn_extra, eik_w, eik_count, g_sdf, g_color, ws, want_xin);
     else
         field_bwd2_kernel<<<grid_for(ntiles, 1, kNumSMs), MLP_THREADS, b2::SMEM, st>>>(
-            f, count, dl_dc, dl_dsdf, dl_dn_extra, eik_w, eik_count, g_sdf, g_color, ws, want_xin);
+            f, count, dl_dc, dl_dsdf, dl_dn_extra, eik_w, eik_count, g_sdf, g_color, ws);
 }
 
 static void launch_fwd(const FieldDev &f, int64_t ntiles, const int32_t *count, float *sdf, float *colors,
