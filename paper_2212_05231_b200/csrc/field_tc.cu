@@ -902,6 +902,17 @@ struct PredScaleG {
     }
 };
 
+// A 0/1 mask byte as 8 fp16 values (1.0 = 0x3C00): entry b of a 256-entry table, so a
+// thread stages its 32 mask bits with four shared-memory loads instead of ~80 ALU ops
+__device__ __forceinline__ void mask_lut_init(uint4 *lut) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        auto h2 = [&](int k) {
+            return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u);
+        };
+        lut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
+    }
+}
+
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
@@ -934,6 +945,8 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     __shared__ uint32_t gmx[2][2][NSLOT];
     __shared__ int gpred[2][NSLOT];
     __shared__ LevelSm lvs[NS2B_MAX_LEVELS];
+    __shared__ uint4 m1lut[256];
+    mask_lut_init(m1lut);
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int g = warp >> 3, gw = warp & 7, tg = t & 255;
@@ -1189,14 +1202,9 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             };
             stg(eA1);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {  // M1 (exact in fp16: hi part only) into EB (E is dead)
-                const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
-                auto h2 = [&](int k) {
-                    return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
-                };
+            for (int i = 0; i < 4; ++i)  // M1 (exact in fp16: hi part only) into EB (E is dead)
                 *reinterpret_cast<uint4 *>(S.p(EB) + umma::tile_off(r, 8 * (4 * qh + i), 64)) =
-                    make_uint4(h2(0), h2(2), h2(4), h2(6));
-            }
+                    m1lut[(m1 >> (8 * i)) & 0xFFu];
             group_publish(g);
             PMARK(2);
             if (!kG && tg < NSLOT) gmx[g][PS.par ^ 1][tg] = 0u;
@@ -2394,6 +2402,8 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
     __shared__ uint32_t tmem_base_sh;
     __shared__ uint32_t gmx[2][2][NSLOT];
     __shared__ int gpred[2][NSLOT];
+    __shared__ uint4 m1lut[256];
+    mask_lut_init(m1lut);
     const Smem S{smem_raw};
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int g = warp >> 3, gw = warp & 7, tg = t & 255;
@@ -2822,14 +2832,9 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 PS.contrib(kMv, mm);
                 // M1 (exact in fp16: hi part only) -> TY
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t bits = (m1 >> (8 * i)) & 0xFFu;
-                    auto h2 = [&](int k) {
-                        return ((bits >> k) & 1u ? 0x3C00u : 0u) | ((bits >> (k + 1)) & 1u ? 0x3C000000u : 0u);
-                    };
+                for (int i = 0; i < 4; ++i)
                     *reinterpret_cast<uint4 *>(S.p(TYS) + umma::tile_off(r, 8 * (4 * qh + i), 64)) =
-                        make_uint4(h2(0), h2(2), h2(4), h2(6));
-                }
+                        m1lut[(m1 >> (8 * i)) & 0xFFu];
 #pragma unroll 1
                 for (int pass = 0;; ++pass) {
                     stage_blk_ta<16>(S, TDS, r, qh, dly, pow2i(eDLY), my + S_AH, my + S_AL);
