@@ -1225,11 +1225,18 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
         const float *jt = ws.jac + tile * JROWS * TILE + r;
         float jv0[4][6];
         if constexpr (!kG) {
+            const float *jt0 = jt + 48 * qh * TILE;  // this half's 8 levels
+            if (8 * qh + 8 <= NA) {  // all active (the common case): plain loads
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int k = 0; k < 6; ++k)
-                    jv0[i][k] = 8 * qh + i < NA ? __ldcs(jt + (6 * (8 * qh + i) + k) * TILE) : 0.f;
+                    for (int k = 0; k < 6; ++k) jv0[i][k] = __ldcs(jt0 + (6 * i + k) * TILE);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) jv0[i][k] = 8 * qh + i < NA ? __ldcs(jt0 + (6 * i + k) * TILE) : 0.f;
+            }
         }
         wait_mma(mbar, phase);
         PMARK(4);
@@ -1291,11 +1298,18 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 // (L2-resident) are issued before the first batch is consumed
                 const int l1 = 8 * qh + 4;
                 float jv1[4][6];
+                const float *jt1 = jt + 6 * l1 * TILE;
+                if (8 * qh + 8 <= NA) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int k = 0; k < 6; ++k)
-                        jv1[i][k] = l1 + i < NA ? __ldcs(jt + (6 * (l1 + i) + k) * TILE) : 0.f;
+                        for (int k = 0; k < 6; ++k) jv1[i][k] = __ldcs(jt1 + (6 * i + k) * TILE);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int k = 0; k < 6; ++k) jv1[i][k] = l1 + i < NA ? __ldcs(jt1 + (6 * i + k) * TILE) : 0.f;
+                }
                 if (8 * qh < NA) batch(8 * qh, 0, jv0);
                 if (l1 < NA) batch(l1, 4, jv1);
             }
