@@ -1,37 +1,50 @@
-// K2/K5 on the 5th-gen tensor cores: fused field forward / backward with tcgen05.
+// K2/K5 on the 5th-gen tensor cores: the field's MLP forward / backward with tcgen05, plus
+// the hash-grid gather and the table scatter around them.
 //
-// One CTA = 128 threads = one 128-sample tile at a time (persistent loop); thread t
-// owns sample t of the tile AND TMEM lane t, so every per-sample epilogue (ReLU,
-// masks, normals, sigmoid, losses, scatter) is plain per-thread code on the rows that
-// tcgen05.ld returns.  Every dense contraction is a UMMA issued by thread 0:
+// Kernels (one training step launches gather -> fwd2 -> [composite] -> bwd2 -> scatter):
+//   field_gather_kernel   one 128-sample tile per block: trilinear features, d feature/dx
+//                         (J), the encoding tile E pre-staged in the UMMA layout;
+//   field_fwd2_kernel     persistent, 512 threads = two 256-thread groups, each running
+//                         its own 128-sample tile (two tiles in flight per SM);
+//   field_bwd2_kernel     persistent, 512 threads = group C (colour-net half of the chain)
+//                         a tile ahead of group S (SDF-net half), handoff through a
+//                         two-slot shared-memory ring;
+//   field_scatter_kernel  one tile per block, first + second-order table gradients (Eq. 9)
+//                         as float2 / x-pair float4 REDs;
+//   field_fwd_kernel / field_bwd_kernel: the one-tile versions (NS2B_FWD=1 / NS2B_BWD=1;
+//                         the dynamic path's input cotangents use field_bwd_kernel).
 //
-//   chain GEMMs (M = 128 samples): operand tiles [sample][feature] (K-major A) x the
-//     weights (K-major view for W^T, MN-major view of the same tile for W);
-//   weight-gradient GEMMs (M = 64 weight rows, K = the 128 samples of the tile):
-//     MN-major views of the same per-sample tiles; each finished per-tile accumulator
-//     is folded into an fp32 shared-memory sum (one global RED per element per CTA).
+// A tile is 128 samples = 128 TMEM lanes; a warp reads its lane quadrant (warp % 4), and
+// the warps sharing a quadrant split each row's columns, so every per-sample epilogue
+// (ReLU, masks, normals, sigmoid, losses, cotangents) is plain per-thread code on the rows
+// tcgen05.ld returns.  Every dense contraction is a UMMA issued by one elected lane of an
+// MMA warp:
+//   chain GEMMs (M = 128 samples): operand tiles [sample][feature] (K-major A, in shared
+//     memory or -- the backward's cotangent tiles -- in TMEM) x the weights (K-major view
+//     for W^T, MN-major view of the same tile for W);
+//   weight-gradient GEMMs (M = 64 weight rows, K = the 128 samples of the tile): MN-major
+//     views of the per-sample tiles, accumulated in TMEM across a CTA's tiles and folded to
+//     global memory on a scale change and at the end.
 //
-// Precision: every operand is fp16 with the three-term hi/lo split (A_hi B_hi +
-// A_lo B_hi + A_hi B_lo, fp32 accumulation in TMEM).  The split is fp32-accurate only
-// while the lo parts stay normal, so every staged tile (per tile) and every weight
-// matrix (per CTA) is scaled by an exact power of two putting its max in
-// [2^13, 2^14); GEMM results are multiplied back by 2^-(eA+eB).  This also keeps the
-// cotangents (dL/dc ~ 1/m) in range.
+// Precision: chain GEMMs use fp16 with the three-term hi/lo split (A_hi B_hi + A_lo B_hi +
+// A_hi B_lo, fp32 accumulation in TMEM); it is fp32-accurate only while the lo parts stay
+// normal, so every staged tile (per tile, predicted exponents) and every weight matrix (per
+// CTA) is scaled by an exact power of two putting its max in [2^13, 2^14); GEMM results are
+// multiplied back by 2^-(eA+eB) (folded into the next staging scale where one follows).
+// Weight-gradient GEMMs take both operands as fp16 (stated, fp32 accumulation).
 //
 // Encoding column order inside the tiles: [features 0..31 | x y z | 1 | 0 x 12] (48),
 // so a level's feature pair is 4-byte aligned; H1 / dH1 are permuted accordingly.
 //
 // Algorithm per tile (field.py:208-331, relu_mlp.py:94-216):
-//   P0 gather features + dfeature/dx (J -> TMEM);  Z1 = E H1^T
-//   P1 a1 = relu(Z1), s1 = H2[0].m1;  Y = A1 H2^T,  JD = S1 H1          (j_d)
-//   P2 n = j_d J; cin = [x,n,v,y];  Zc1 = CIN C1^T
-//   P3 Zc2 = A1c C2^T;  P4 LOG = A2c C3^T;  P5 c = sigmoid  (forward ends here)
-//   P5 dlogits -> U2 = DLOG C3,  dC3 += A2c^T DLOG
-//   P6 u2 -> U1 = U2 C2,         dC2 += U2^T A1c
-//   P7 u1 -> DCIN = U1 C1,       dC1 += U1^T CIN
-//   P8 q, dly -> U = DLY H2,     dH2 += A1^T DLY
-//   P9 u, mvec=[Jq,q] -> DE = U H1, PV = MV H1^T,  dH1 += U^T E + S1^T MV  (Thm 1)
-//   P10 dH2[0] += sum pv (PV^T ONES);  fused first+second-order table scatter (Eq. 9)
+//   forward   P0 Z1 = E H1^T;  P1 a1 = relu(Z1), d (fp32 FMAs);  Y = A1 H2^T,  JD = M1 H1'
+//             (j_d);  P2 n = j_d J, cin = [x, n, v, y];  Zc1 = CIN C1^T;  P3 Zc2 = A1c C2^T;
+//             P4 logits (FMAs);  P5 c = sigmoid  (+ the Eikonal cotangent when fused)
+//   backward  dlog -> U2 = DLOG C3, dC3 += A2c^T DLOG;  u2 -> U1 = U2 C2, dC2 += U2^T A1c;
+//             u1 -> DCIN = U1 C1, dC1 += U1^T CIN;  q, dly -> U = DLY H2, dH2 += A1^T DLY;
+//             u, mvec = [J q, q] -> DE = U H1, dH1 += U^T E, G += M1^T MV (Theorem 1:
+//             dH1 += diag(H2[0]) G, dH2[0] += rowdot(H1, G) at fold time);  DE, j_d, q ->
+//             the scatter's inputs
 #include <cstdio>
 
 #include "field_common.cuh"
