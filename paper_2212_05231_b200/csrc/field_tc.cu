@@ -329,13 +329,25 @@ struct Workspace {
     float *xv;
     uint8_t *fw_tiles;
     int4 *fw_exp;
-    uint2 *fw_mask;
+    uint32_t *fw_mask;  // [tile][m1 | mc1 | mc2][half][128]: a row's 32 hidden-unit bits of a half (blocks 4h..4h+3)
     float *fw_nc;
     float *xin;
     int *flags;  // [0]: 1 when the forward stored the Eikonal cotangent (not n) in fw_nc rows 0-2
 };
+// mask word of (kind, half) for row r of a tile
+__device__ __forceinline__ int64_t mask_idx(int64_t tile, int kind, int h, int r) {
+    return (tile * 6 + kind * 2 + h) * TILE + r;
+}
+// the one-group kernels' quarter view: quarter q owns blocks q and q + 4, as
+// (m1 | mc1 << 16, mc2) with block q in the low byte of each 16-bit field
+__device__ __forceinline__ uint2 mask_quarter(const uint32_t *w6, int stride, int q) {
+    auto q16 = [&](int kind) {
+        return ((w6[(2 * kind) * stride] >> (8 * q)) & 0xFFu) | (((w6[(2 * kind + 1) * stride] >> (8 * q)) & 0xFFu) << 8);
+    };
+    return make_uint2(q16(0) | (q16(1) << 16), q16(2));
+}
 __host__ __device__ inline size_t ws_tile_bytes() {
-    return 2 * static_cast<size_t>(TEB) + FWB + sizeof(int4) + sizeof(int) + 4 * TILE * sizeof(uint2) +
+    return 2 * static_cast<size_t>(TEB) + FWB + sizeof(int4) + sizeof(int) + 6 * TILE * sizeof(uint32_t) +
            (JROWS + SBROWS + XVROWS + NCROWS + XINROWS) * TILE * sizeof(float);
 }
 __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
@@ -347,8 +359,8 @@ __host__ inline Workspace ws_carve(void *base, int64_t ntiles) {
     b += ntiles * static_cast<size_t>(FWB);
     w.fw_exp = reinterpret_cast<int4 *>(b);
     b += ntiles * sizeof(int4);
-    w.fw_mask = reinterpret_cast<uint2 *>(b);
-    b += ntiles * 4 * TILE * sizeof(uint2);
+    w.fw_mask = reinterpret_cast<uint32_t *>(b);
+    b += ntiles * 6 * TILE * sizeof(uint32_t);
     w.fw_nc = reinterpret_cast<float *>(b);
     b += ntiles * NCROWS * TILE * sizeof(float);
     w.jac = reinterpret_cast<float *>(b);
@@ -818,7 +830,15 @@ field_fwd_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restric
             umma::bulk_s2g(fwt + FW_A2C, S.p(TY), T64B);
             ws.fw_exp[tile] = make_int4(eA1, eCin, eA1c, eA2c);
         }
-        ws.fw_mask[(tile * 4 + qt) * TILE + r] = make_uint2(m1 | (mc1 << 16), mc2);
+        {  // this quarter's two blocks: byte qt of the half-0 word (block qt) and of the half-1 word
+            uint8_t *mb = reinterpret_cast<uint8_t *>(ws.fw_mask);
+            const uint32_t qw[3] = {m1, mc1, mc2};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                mb[4 * mask_idx(tile, k, 0, r) + qt] = static_cast<uint8_t>(qw[k]);
+                mb[4 * mask_idx(tile, k, 1, r) + qt] = static_cast<uint8_t>(qw[k] >> 8);
+            }
+        }
         // ------------------------------------------------ P5: colours
         {
             if (qt == 0) {
@@ -994,7 +1014,6 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
     const uint32_t EB = gbase + F2_EB, AB = gbase + F2_AB;
     float *xch = reinterpret_cast<float *>(S.p(gbase + F2_XCH));  // [2][128] d | [2][3][128] normal
     float *lgx = reinterpret_cast<float *>(S.p(gbase + F2_LG));   // [2][3][128] logit partials
-    uint8_t *mkx = S.p(gbase + F2_MK);                            // [3][8][128] mask bytes
     const uint32_t tb = tmem_base_sh + g * (kG ? 256 : 128);
     const uint32_t my = tb + (static_cast<uint32_t>(qd * 32) << 16);
     const uint32_t SA = 0, SB = 64, TJ = 128;  // TJ (kG): 16 levels x 8 columns of J
@@ -1484,13 +1503,6 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
             lgx[(3 * qh + 0) * TILE + r] = lp0 * sc;
             lgx[(3 * qh + 1) * TILE + r] = lp1 * sc;
             lgx[(3 * qh + 2) * TILE + r] = lp2 * sc;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {  // mask bytes [m1 | mc1 | mc2][block][row]
-                const int b = 4 * qh + i;
-                mkx[(0 * 8 + b) * TILE + r] = static_cast<uint8_t>(m1 >> (8 * i));
-                mkx[(1 * 8 + b) * TILE + r] = static_cast<uint8_t>(mc1 >> (8 * i));
-                mkx[(2 * 8 + b) * TILE + r] = static_cast<uint8_t>(mc2 >> (8 * i));
-            }
             auto stg = [&](int e) {  // hi part only: the backward's weight-gradient GEMMs read nothing else
                 const float s = pow2i(e + esc);
 #pragma unroll
@@ -1529,15 +1541,9 @@ field_fwd2_kernel(FieldDev f, const int32_t *__restrict__ count, float *__restri
                 col_out[3 * p + 2] = cc2;
             }
         }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {  // the backward's layout: quarter q holds blocks q and q + 4
-            const int q = 2 * qh + j;
-            auto word = [&](int kind) {
-                return static_cast<uint32_t>(mkx[(kind * 8 + q) * TILE + r]) |
-                       (static_cast<uint32_t>(mkx[(kind * 8 + q + 4) * TILE + r]) << 8);
-            };
-            ws.fw_mask[(tile * 4 + q) * TILE + r] = make_uint2(word(0) | (word(1) << 16), word(2));
-        }
+        ws.fw_mask[mask_idx(tile, 0, qh, r)] = m1;  // this half's 32 hidden-unit bits
+        ws.fw_mask[mask_idx(tile, 1, qh, r)] = mc1;
+        ws.fw_mask[mask_idx(tile, 2, qh, r)] = mc2;
         PMARK(12);
     }
 #ifdef NS2B_PHASE_PROF
@@ -1707,7 +1713,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     // ... and TE's second half (E also arrives as its hi part) holds a full tile's per-sample
     // inputs, DMA'd while the previous tile runs: masks [4][128] uint2 | n, c [6][128] |
     // dL/dc [128][3] | dL/dsdf [128] | the forward's exponents (int4)
-    constexpr uint32_t TIN = TE + TEB, IN_MK = TIN, IN_NC = IN_MK + 4 * TILE * 8,
+    constexpr uint32_t TIN = TE + TEB, IN_MK = TIN, IN_NC = IN_MK + 6 * TILE * 4,
                        IN_DC = IN_NC + NCROWS * TILE * 4, IN_DS = IN_DC + 3 * TILE * 4, IN_EX = IN_DS + TILE * 4,
                        IN_BYTES = IN_EX + 16 - TIN;
     static_assert(IN_BYTES <= TEB, "per-tile inputs fit in TE's free half");
@@ -1831,7 +1837,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
     auto in_full = [&](int64_t tl) { return in_dma_ok && (tl + 1) * TILE <= P; };
     auto in_dma = [&](int64_t tl) {  // one thread
         umma::mbar_expect_tx(mb_in, IN_BYTES);
-        umma::bulk_g2s_tx(S.p(IN_MK), ws.fw_mask + tl * 4 * TILE, 4 * TILE * 8, mb_in);
+        umma::bulk_g2s_tx(S.p(IN_MK), ws.fw_mask + tl * 6 * TILE, 6 * TILE * 4, mb_in);
         umma::bulk_g2s_tx(S.p(IN_NC), ws.fw_nc + tl * NCROWS * TILE, NCROWS * TILE * 4, mb_in);
         umma::bulk_g2s_tx(S.p(IN_DC), dl_dc + 3 * tl * TILE, 3 * TILE * 4, mb_in);
         umma::bulk_g2s_tx(S.p(IN_DS), dl_dsdf + tl * TILE, TILE * 4, mb_in);
@@ -1842,7 +1848,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
         if (in_full(tl)) {
             umma::mbar_wait(mb_in, ph_in);
             ph_in ^= 1u;
-            v.mk = *reinterpret_cast<const uint2 *>(S.p(IN_MK) + 8 * (qt * TILE + r));
+            v.mk = mask_quarter(reinterpret_cast<const uint32_t *>(S.p(IN_MK)) + r, TILE, qt);
             const float *nc = reinterpret_cast<const float *>(S.p(IN_NC)) + r;
             if (qt == 0) {
                 const float *dc = reinterpret_cast<const float *>(S.p(IN_DC)) + 3 * r;
@@ -1861,7 +1867,7 @@ field_bwd_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__r
             return v;
         }
         const int64_t pp = tl * TILE + r;
-        v.mk = ws.fw_mask[(tl * 4 + qt) * TILE + r];
+        v.mk = mask_quarter(ws.fw_mask + mask_idx(tl, 0, 0, r), TILE, qt);
         fe = ws.fw_exp[tl];
         if (pp < P) {
             const float *nc = ws.fw_nc + tl * NCROWS * TILE + r;
@@ -2323,7 +2329,7 @@ constexpr uint32_t TWC = TDC + TDB;             // A2c hi    128 x 64
 constexpr uint32_t TZC = TWC + T64B;            // A1c hi
 constexpr uint32_t TYC = TZC + T64B;            // U2 hi -> U1 hi
 constexpr uint32_t TCC = TYC + T64B;            // CIN hi    128 x 32
-constexpr uint32_t IN_MK = 0, IN_NC = IN_MK + 4 * TILE * 8, IN_DC = IN_NC + NCROWS * TILE * 4,
+constexpr uint32_t IN_MK = 0, IN_NC = IN_MK + 6 * TILE * 4, IN_DC = IN_NC + NCROWS * TILE * 4,
                    IN_DS = IN_DC + 3 * TILE * 4, IN_EX = IN_DS + TILE * 4, IN_BYTES = IN_EX + 16;
 constexpr uint32_t IN_STRIDE = (IN_BYTES + 127) / 128 * 128;
 constexpr uint32_t TIN0 = TCC + TCB;            // per-tile inputs, two slots
@@ -2514,7 +2520,7 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
         auto in_dma = [&](int64_t tl, int s) {  // one thread
             const uint32_t base = TIN0 + s * IN_STRIDE;
             umma::mbar_expect_tx(mb_in + s, IN_BYTES);
-            umma::bulk_g2s_tx(S.p(base + IN_MK), ws.fw_mask + tl * 4 * TILE, 4 * TILE * 8, mb_in + s);
+            umma::bulk_g2s_tx(S.p(base + IN_MK), ws.fw_mask + tl * 6 * TILE, 6 * TILE * 4, mb_in + s);
             umma::bulk_g2s_tx(S.p(base + IN_NC), ws.fw_nc + tl * NCROWS * TILE, NCROWS * TILE * 4, mb_in + s);
             umma::bulk_g2s_tx(S.p(base + IN_DC), dl_dc + 3 * tl * TILE, 3 * TILE * 4, mb_in + s);
             umma::bulk_g2s_tx(S.p(base + IN_DS), dl_dsdf + tl * TILE, TILE * 4, mb_in + s);
@@ -2549,13 +2555,10 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 umma::mbar_wait(mb_in + s, ph_in[s]);
                 ph_in[s] ^= 1u;
                 const uint8_t *base = S.p(TIN0 + s * IN_STRIDE);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint2 w = *reinterpret_cast<const uint2 *>(base + IN_MK + 8 * (q * TILE + r));
-                    m1 |= ((w.x >> (8 * qh)) & 0xFFu) << (8 * q);
-                    mc1 |= ((w.x >> (16 + 8 * qh)) & 0xFFu) << (8 * q);
-                    mc2 |= ((w.y >> (8 * qh)) & 0xFFu) << (8 * q);
-                }
+                const uint32_t *mw = reinterpret_cast<const uint32_t *>(base + IN_MK) + qh * TILE + r;
+                m1 = mw[0];  // this half's 32 hidden-unit bits of each mask
+                mc1 = mw[2 * TILE];
+                mc2 = mw[4 * TILE];
                 const float *nc = reinterpret_cast<const float *>(base + IN_NC) + r;
                 const float *dc = reinterpret_cast<const float *>(base + IN_DC) + 3 * r;
                 gc0 = dc[0];
@@ -2570,13 +2573,9 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 n2 = nc[2 * TILE];
                 fe = *reinterpret_cast<const int4 *>(base + IN_EX);
             } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint2 w = ws.fw_mask[(tile * 4 + q) * TILE + r];
-                    m1 |= ((w.x >> (8 * qh)) & 0xFFu) << (8 * q);
-                    mc1 |= ((w.x >> (16 + 8 * qh)) & 0xFFu) << (8 * q);
-                    mc2 |= ((w.y >> (8 * qh)) & 0xFFu) << (8 * q);
-                }
+                m1 = ws.fw_mask[mask_idx(tile, 0, qh, r)];
+                mc1 = ws.fw_mask[mask_idx(tile, 1, qh, r)];
+                mc2 = ws.fw_mask[mask_idx(tile, 2, qh, r)];
                 fe = ws.fw_exp[tile];
                 if (valid) {
                     const float *nc = ws.fw_nc + tile * NCROWS * TILE + r;
