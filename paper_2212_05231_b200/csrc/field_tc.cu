@@ -2646,6 +2646,9 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
             }
             wait_mma(mbar, ph);
             // ------------------------------------------- C1: u2 -> U1, dC2
+            // the previous tile's dC1 ran before this tile's U2 GEMM in the MMA pipe: TC takes
+            // this tile's CIN (needed by C2's dC1), with no wait on the issuing thread
+            if (dma_t && it > 0) dma(TCC, fwt(tile) + FW_CIN, TCB, mb_c);
             int eU2;
             {
                 // raw accumulator values: the result scale 2^-(eD + eC3) is folded into the
@@ -2758,12 +2761,6 @@ field_bwd2_kernel(FieldDev f, const int32_t *__restrict__ count, const float *__
                 }
                 hm[qh * TILE] = m1;
                 umma::mbar_arrive(hfull + hs);
-            }
-            // dC1 (behind the DCIN GEMM) has read CIN: the next tile's CIN
-            if (dma_t && has_next) {
-                umma::mbar_wait(mbar3, ph3);
-                umma::fence_after_sync();
-                dma(TCC, fwt(ntile) + FW_CIN, TCB, mb_c);
             }
             ph3 ^= 1u;
         }
